@@ -1,0 +1,866 @@
+// C-ABI and C++ host drivers of the B200 TT-SVD hot path (include/ttsvd_cu.h).
+//
+// Host side mirrors the reference drivers:
+//   run_chain / tt_svd_tsqr        tt_svd.hpp:159-199, 281-290   (Alg. 2)
+//   tt_svd_distributed             tt_svd.hpp:520-631            (Alg. 5)
+// and launches the sm_100a kernels of ttsvd_kernels.cuh.  There is no CPU
+// fallback anywhere in this library: every numeric step runs on the device.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cfloat>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/ttsvd_cu.h"
+#include "ttsvd_kernels.cuh"
+
+using namespace ttsvd_b200;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const std::string& msg) {
+    g_last_error = msg;
+    return code;
+}
+
+#define TT_CUDA(call)                                                                                     \
+    do {                                                                                                  \
+        cudaError_t e_ = (call);                                                                          \
+        if (e_ != cudaSuccess) {                                                                          \
+            return fail(e_ == cudaErrorMemoryAllocation ? TTSVD_ERR_ALLOCATION : TTSVD_ERR_DEVICE,        \
+                        std::string(#call) + ": " + cudaGetErrorString(e_));                              \
+        }                                                                                                 \
+    } while (0)
+
+#define TT_TRY(call)                 \
+    do {                             \
+        int rc_ = (call);            \
+        if (rc_ != TTSVD_OK) return rc_; \
+    } while (0)
+
+struct DevBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+};
+
+}  // namespace
+
+struct ttsvd_cu_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    int num_sms = 148;
+    int coop_max_blocks = 0;  // co-resident CTAs of jacobi_coop_kernel
+    int64_t launches = 0;
+    bool timing = false;
+    // grow-only device workspaces
+    DevBuf ws_R, ws_R2, ws_A, ws_V, ws_sigma, ws_flags, ws_work[2], ws_X, ws_send, ws_recv;
+    DevBuf host_stage;  // pinned
+    cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+};
+
+struct ttsvd_cu_tt {
+    std::vector<int64_t> dims, ranks;
+    std::vector<std::vector<double>> cores;
+    std::vector<ttsvd_cu_step> steps;
+    std::vector<std::vector<double>> sigmas;
+};
+
+namespace {
+
+int ensure(DevBuf& b, size_t bytes) {
+    if (b.bytes >= bytes) return TTSVD_OK;
+    if (b.p) cudaFree(b.p);
+    b.p = nullptr;
+    b.bytes = 0;
+    const size_t alloc = std::max<size_t>(bytes, 256);
+    TT_CUDA(cudaMalloc(&b.p, alloc));
+    b.bytes = alloc;
+    return TTSVD_OK;
+}
+
+int ensure_host(DevBuf& b, size_t bytes) {
+    if (b.bytes >= bytes) return TTSVD_OK;
+    if (b.p) cudaFreeHost(b.p);
+    b.p = nullptr;
+    b.bytes = 0;
+    TT_CUDA(cudaMallocHost(&b.p, std::max<size_t>(bytes, 4096)));
+    b.bytes = std::max<size_t>(bytes, 4096);
+    return TTSVD_OK;
+}
+
+template <class T>
+T* as(DevBuf& b) {
+    return static_cast<T*>(b.p);
+}
+
+int64_t padded_stride_h(int64_t n) {
+    if (n < 1) return -1;
+    if (n <= 64) return 64;
+    int64_t q = (n + 63) / 64;
+    if (q % 2 == 0) ++q;
+    return 64 * q;
+}
+
+int check_launch(ttsvd_cu_ctx* ctx, const char* what) {
+    ctx->launches += 1;
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(TTSVD_ERR_DEVICE, std::string(what) + ": " + cudaGetErrorString(e));
+    return TTSVD_OK;
+}
+
+int set_device(ttsvd_cu_ctx* ctx) {
+    if (!ctx) return fail(TTSVD_ERR_INVALID, "null context");
+    TT_CUDA(cudaSetDevice(ctx->device));
+    return TTSVD_OK;
+}
+
+constexpr int kTsqrThreads = 256;
+constexpr int kSmemLimit = 227 * 1024;
+
+// ---------------------------------------------------------------- K_TSQR ----
+struct TsqrPlan {
+    int bt, ldb, r_in_smem;
+    size_t smem;
+};
+
+TsqrPlan tsqr_plan(int m) {
+    TsqrPlan p;
+    p.r_in_smem = (m <= 64);
+    const size_t r_bytes = p.r_in_smem ? (size_t)m * m * 8 : 0;
+    const size_t tile_budget = m <= 64 ? 64 * 1024 : 160 * 1024;
+    int bt = (int)std::max<size_t>(1, tile_budget / ((size_t)m * 8));
+    bt = std::min(bt, 2048);
+    if (bt >= 32) bt = bt / 32 * 32;
+    p.bt = bt;
+    p.ldb = bt;
+    p.smem = r_bytes + (size_t)p.ldb * m * 8 + (kTsqrThreads / 32 + 4) * 8;
+    return p;
+}
+
+int launch_tsqr_kernel(ttsvd_cu_ctx* ctx, const TsqrArgs& a, int grid, size_t smem) {
+    static bool attr_set = false;
+    if (!attr_set) {
+        TT_CUDA(cudaFuncSetAttribute(tsqr_tile_kernel<kTsqrThreads>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     kSmemLimit));
+        attr_set = true;
+    }
+    tsqr_tile_kernel<kTsqrThreads><<<grid, kTsqrThreads, smem, ctx->stream>>>(a);
+    return check_launch(ctx, "tsqr_tile_kernel");
+}
+
+// Fixed index-ordered merge tree over `count` parts (each m*m) in buf_a; the
+// result lands in R_final.  Level l pairs (2i, 2i+1); an odd tail is carried.
+int merge_tree(ttsvd_cu_ctx* ctx, double* parts, int64_t count, int m, double* R_final) {
+    if (count == 1) {
+        TT_CUDA(cudaMemcpyAsync(R_final, parts, (size_t)m * m * 8, cudaMemcpyDeviceToDevice, ctx->stream));
+        return TTSVD_OK;
+    }
+    TT_TRY(ensure(ctx->ws_R2, (size_t)((count + 1) / 2) * m * m * 8));
+    TsqrPlan p = tsqr_plan(m);
+    double* src = parts;
+    double* bufs[2] = {as<double>(ctx->ws_R2), parts};
+    int flip = 0;
+    while (count > 1) {
+        const int64_t next = (count + 1) / 2;
+        double* dst = (next == 1) ? R_final : bufs[flip];
+        TsqrArgs a{src, count, (int64_t)m, dst, m, p.bt, p.ldb, 1, p.r_in_smem};
+        TT_TRY(launch_tsqr_kernel(ctx, a, (int)next, p.smem));
+        src = dst;
+        count = next;
+        flip ^= 1;
+    }
+    return TTSVD_OK;
+}
+
+// R (m x m) of X (n x m, ld) — n may be smaller than m (the structured kernel
+// does not need n >= m; gram_triangular's square padding is implicit).
+int tsqr_device(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t ld, double* R) {
+    TsqrPlan p = tsqr_plan(m);
+    const int64_t min_rows = std::max<int64_t>(p.bt, 8 * (int64_t)m);
+    int64_t G = std::max<int64_t>(1, n / min_rows);
+    G = std::min<int64_t>(G, 2 * (int64_t)ctx->num_sms);
+    TT_TRY(ensure(ctx->ws_R, (size_t)G * m * m * 8));
+    double* parts = as<double>(ctx->ws_R);
+    TsqrArgs a{X, n, ld, G == 1 ? R : parts, m, p.bt, p.ldb, 0, p.r_in_smem};
+    TT_TRY(launch_tsqr_kernel(ctx, a, (int)G, p.smem));
+    if (G == 1) return TTSVD_OK;
+    return merge_tree(ctx, parts, G, m, R);
+}
+
+// ----------------------------------------------------------------- K_SVD ----
+int transpose_device(ttsvd_cu_ctx* ctx, const double* src, int64_t rows, int64_t cols, int64_t ld, double* dst) {
+    dim3 block(32, 8);
+    dim3 grid((unsigned)((cols + 31) / 32), (unsigned)((rows + 31) / 32));
+    transpose_kernel<<<grid, block, 0, ctx->stream>>>(src, rows, cols, ld, dst);
+    return check_launch(ctx, "transpose_kernel");
+}
+
+constexpr int kJacobiThreads = 256;
+constexpr int kJacobiSmemThreads = 512;
+
+// One-sided Jacobi on A (n x m, ld n, device, overwritten).  With Vacc the
+// rotations are accumulated.  Returns sweeps used via *sweeps.
+int jacobi_device(ttsvd_cu_ctx* ctx, double* A, int n, int m, double* Vacc) {
+    TT_TRY(ensure(ctx->ws_flags, 64 * sizeof(int)));
+    int* flags = as<int>(ctx->ws_flags);
+    TT_CUDA(cudaMemsetAsync(flags, 0, 64 * sizeof(int), ctx->stream));
+    JacobiArgs a{A, Vacc, n, m, flags, flags + 40, 30};
+    const size_t smem = ((size_t)n * m + (Vacc ? (size_t)m * m : 0)) * 8;
+    if (smem <= 200 * 1024) {
+        static bool attr = false;
+        if (!attr) {
+            TT_CUDA(cudaFuncSetAttribute(jacobi_smem_kernel<kJacobiSmemThreads>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit));
+            attr = true;
+        }
+        jacobi_smem_kernel<kJacobiSmemThreads><<<1, kJacobiSmemThreads, smem, ctx->stream>>>(a);
+        TT_TRY(check_launch(ctx, "jacobi_smem_kernel"));
+    } else {
+        const int warps_per = kJacobiThreads / 32;
+        int grid = (m / 2 + warps_per - 1) / warps_per;
+        grid = std::max(1, std::min(grid, ctx->coop_max_blocks));
+        void* args[] = {&a};
+        TT_CUDA(cudaLaunchCooperativeKernel((const void*)jacobi_coop_kernel<kJacobiThreads>, dim3(grid),
+                                            dim3(kJacobiThreads), args, 0, ctx->stream));
+        TT_TRY(check_launch(ctx, "jacobi_coop_kernel"));
+    }
+    return TTSVD_OK;
+}
+
+int jacobi_status(ttsvd_cu_ctx* ctx, int* sweeps) {
+    int h = 0;
+    TT_CUDA(cudaMemcpyAsync(&h, as<int>(ctx->ws_flags) + 40, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    TT_CUDA(cudaStreamSynchronize(ctx->stream));
+    *sweeps = h;
+    if (h < 0) return fail(TTSVD_ERR_CONVERGENCE, "jacobi_svd: no convergence in 30 sweeps");
+    return TTSVD_OK;
+}
+
+int finalize_device(ttsvd_cu_ctx* ctx, const double* A, int n, int m, const double* Vacc, double* sigma, double* Uout,
+                    double* Vout) {
+    const size_t smem = (size_t)m * 8 + (size_t)2 * m * sizeof(int) + 64 * 8;
+    jacobi_finalize_kernel<512><<<1, 512, smem, ctx->stream>>>(A, n, m, Vacc, sigma, Uout, Vout);
+    return check_launch(ctx, "jacobi_finalize_kernel");
+}
+
+// Right singular vectors of a work matrix given as the columns to
+// orthogonalise: A_src (n x m, ld) is copied/transposed into the workspace
+// first.  Output: sigma[m] and Vout (n x m, ld n) = normalised columns.
+int svd_columns(ttsvd_cu_ctx* ctx, const double* src, int64_t src_rows, int64_t src_cols, int64_t src_ld,
+                bool transpose, double* sigma, double* Vout, int* sweeps) {
+    const int64_t n = transpose ? src_cols : src_rows;
+    const int64_t m = transpose ? src_rows : src_cols;
+    TT_TRY(ensure(ctx->ws_A, (size_t)n * m * 8));
+    double* A = as<double>(ctx->ws_A);
+    if (transpose) {
+        TT_TRY(transpose_device(ctx, src, src_rows, src_cols, src_ld, A));
+    } else {
+        TT_CUDA(cudaMemcpy2DAsync(A, n * 8, src, src_ld * 8, n * 8, m, cudaMemcpyDeviceToDevice, ctx->stream));
+    }
+    TT_TRY(jacobi_device(ctx, A, (int)n, (int)m, nullptr));
+    TT_TRY(jacobi_status(ctx, sweeps));
+    return finalize_device(ctx, A, (int)n, (int)m, nullptr, sigma, Vout, nullptr);
+}
+
+// ---------------------------------------------------------------- K_TSMM ----
+template <int KC>
+int launch_tsmm(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t ldx, const double* V, int64_t ldv, int k,
+                double* Y, int64_t out_rows, int64_t ldy) {
+    const size_t smem = (size_t)m * KC * 8;
+    static bool attr = false;
+    if (!attr) {
+        TT_CUDA(cudaFuncSetAttribute(tsmm_kernel<KC>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit));
+        attr = true;
+    }
+    const int chunks = (k + KC - 1) / KC;
+    int64_t blocks = (n + 255) / 256;
+    blocks = std::min<int64_t>(blocks, (int64_t)ctx->num_sms * 8);
+    dim3 grid((unsigned)std::max<int64_t>(blocks, 1), (unsigned)chunks);
+    tsmm_kernel<KC><<<grid, 256, smem, ctx->stream>>>(X, n, m, ldx, V, ldv, k, Y, out_rows, ldy);
+    return check_launch(ctx, "tsmm_kernel");
+}
+
+int tsmm_device(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t ldx, const double* V, int64_t ldv, int k,
+                double* Y, int64_t out_rows, int64_t out_cols, int64_t ldy) {
+    int rc;
+    if (k <= 1) rc = launch_tsmm<1>(ctx, X, n, m, ldx, V, ldv, k, Y, out_rows, ldy);
+    else if (k <= 2) rc = launch_tsmm<2>(ctx, X, n, m, ldx, V, ldv, k, Y, out_rows, ldy);
+    else if (k <= 4) rc = launch_tsmm<4>(ctx, X, n, m, ldx, V, ldv, k, Y, out_rows, ldy);
+    else if (k <= 8) rc = launch_tsmm<8>(ctx, X, n, m, ldx, V, ldv, k, Y, out_rows, ldy);
+    else if (k <= 16 || (size_t)m * 32 * 8 > 200 * 1024) rc = launch_tsmm<16>(ctx, X, n, m, ldx, V, ldv, k, Y, out_rows, ldy);
+    else rc = launch_tsmm<32>(ctx, X, n, m, ldx, V, ldv, k, Y, out_rows, ldy);
+    if (rc != TTSVD_OK) return rc;
+    if (ldy > out_rows) {
+        const int64_t pad = (ldy - out_rows) * out_cols;
+        const int blocks = (int)std::min<int64_t>((pad + 255) / 256, 1024);
+        zero_padding_kernel<<<blocks, 256, 0, ctx->stream>>>(Y, out_rows, ldy, out_cols);
+        TT_TRY(check_launch(ctx, "zero_padding_kernel"));
+    }
+    return TTSVD_OK;
+}
+
+// --------------------------------------------------------------- drivers ----
+// tt_svd.hpp:111-118 choose_rank + small_svd.hpp:49-63 select_rank (host
+// scalar arithmetic on the singular values copied back once per step).
+int64_t select_rank_h(const double* sigma, int64_t m, double delta, int64_t r_max) {
+    double tail = 0.0;
+    int64_t r_delta = m;
+    for (int64_t j = m; j-- > 0;) {
+        tail += sigma[j] * sigma[j];
+        if (tail <= delta * delta) r_delta = j;
+        else break;
+    }
+    int64_t r = std::min(r_max, r_delta);
+    if (r < 1) r = 1;
+    return std::min(r, std::max<int64_t>(m, 1));
+}
+
+int64_t choose_rank_h(const double* sigma, int64_t len, int64_t cols, int64_t nsig, double delta, int64_t r_max,
+                      int64_t rows) {
+    const double sigma1 = len > 0 ? sigma[0] : 0.0;
+    const double zero_level = 32.0 * DBL_EPSILON * sigma1 * std::sqrt((double)std::max(rows, cols));
+    const double delta_eff = std::max(delta, zero_level);
+    return std::min(select_rank_h(sigma, len, delta_eff, r_max), nsig);
+}
+
+double sigma_norm_h(const double* s, int64_t m) {
+    double t = 0.0;
+    for (int64_t j = 0; j < m; ++j) t += s[j] * s[j];
+    return std::sqrt(t);
+}
+
+struct Timer {
+    ttsvd_cu_ctx* ctx;
+    bool on;
+    explicit Timer(ttsvd_cu_ctx* c) : ctx(c), on(c->timing) {}
+    void mark(int i) {
+        if (on) cudaEventRecord(ctx->ev[i], ctx->stream);
+    }
+    double ms(int a, int b) {
+        if (!on) return 0.0;
+        float t = 0.f;
+        cudaEventSynchronize(ctx->ev[b]);
+        cudaEventElapsedTime(&t, ctx->ev[a], ctx->ev[b]);
+        return (double)t;
+    }
+};
+
+struct WorkView {
+    const double* data;
+    int64_t rows, cols, ld;
+};
+
+// D2H of `count` doubles through the pinned stage (synchronises the stream).
+int d2h(ttsvd_cu_ctx* ctx, double* dst, const double* src, size_t count) {
+    TT_TRY(ensure_host(ctx->host_stage, count * 8));
+    TT_CUDA(cudaMemcpyAsync(ctx->host_stage.p, src, count * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    TT_CUDA(cudaStreamSynchronize(ctx->stream));
+    std::memcpy(dst, ctx->host_stage.p, count * 8);
+    return TTSVD_OK;
+}
+
+// Alg. 2 loop (tt_svd.hpp:159-199).
+int run_chain(ttsvd_cu_ctx* ctx, WorkView cur, const std::vector<int64_t>& dims, int64_t r_max, double eps,
+              int64_t d_for_delta, ttsvd_cu_tt* out) {
+    const int64_t d = (int64_t)dims.size();
+    out->dims = dims;
+    out->cores.assign(d, {});
+    out->ranks.assign(d + 1, 1);
+    double delta = -1.0;
+    int64_t r = 1;
+    int which = 0;
+    Timer tm(ctx);
+    std::vector<double> sig, Vh;
+    for (int64_t i = d - 1; i >= 1; --i) {
+        const int64_t n_i = dims[i];
+        const int64_t m = n_i * r;
+        if (m != cur.cols) return fail(TTSVD_ERR_SHAPE, "run_chain: work matrix width mismatch");
+        ttsvd_cu_step st{};
+        st.rows = cur.rows;
+        st.cols = m;
+        const bool tall = cur.rows >= cur.cols;
+        const int64_t nsig = tall ? m : cur.rows;
+        TT_TRY(ensure(ctx->ws_sigma, (size_t)std::max<int64_t>(m, nsig) * 8));
+        TT_TRY(ensure(ctx->ws_V, (size_t)m * std::max<int64_t>(nsig, 1) * 8));
+        double* d_sigma = as<double>(ctx->ws_sigma);
+        double* d_V = as<double>(ctx->ws_V);
+        int sweeps = 0;
+        tm.mark(0);
+        if (tall) {
+            TT_TRY(ensure(ctx->ws_X, (size_t)m * m * 8));
+            double* R = as<double>(ctx->ws_X);
+            TT_TRY(tsqr_device(ctx, cur.data, cur.rows, (int)m, cur.ld, R));
+            tm.mark(1);
+            // one-sided Jacobi on R^T: its orthogonalised columns are R's right
+            // singular vectors scaled by sigma (no rotation accumulation)
+            TT_TRY(svd_columns(ctx, R, m, m, m, true, d_sigma, d_V, &sweeps));
+        } else {
+            tm.mark(1);
+            // wide step (tt_svd.hpp:91-103): Jacobi on W^T, V := its U
+            TT_TRY(svd_columns(ctx, cur.data, cur.rows, cur.cols, cur.ld, true, d_sigma, d_V, &sweeps));
+        }
+        tm.mark(2);
+        sig.resize(nsig);
+        TT_TRY(d2h(ctx, sig.data(), d_sigma, nsig));
+        if (delta < 0.0) {
+            if (d_for_delta < 2) return fail(TTSVD_ERR_DEGENERATE, "derive_delta: requires d >= 2");
+            delta = eps / std::sqrt((double)(d_for_delta - 1)) * sigma_norm_h(sig.data(), nsig);
+        }
+        const int64_t rnew = choose_rank_h(sig.data(), nsig, cur.cols, nsig, delta, r_max, cur.rows);
+        st.nsig = nsig;
+        st.rank = rnew;
+        // core_from_vt (tt_svd.hpp:121-128) from the first rnew columns of V
+        Vh.resize((size_t)m * rnew);
+        TT_TRY(d2h(ctx, Vh.data(), d_V, (size_t)m * rnew));
+        std::vector<double> core((size_t)(rnew * n_i * r));
+        for (int64_t b = 0; b < r; ++b)
+            for (int64_t x = 0; x < n_i; ++x)
+                for (int64_t a = 0; a < rnew; ++a) core[a + rnew * (x + n_i * b)] = Vh[a * m + (x + n_i * b)];
+        out->cores[i] = std::move(core);
+        out->ranks[i] = rnew;
+        // fused TSMM + reshape into the next step's padded layout
+        const int64_t n_next = dims[i - 1];
+        const int64_t out_rows = cur.rows / n_next;
+        const int64_t out_cols = n_next * rnew;
+        const int64_t ldy = padded_stride_h(out_rows);
+        TT_TRY(ensure(ctx->ws_work[which], (size_t)ldy * out_cols * 8));
+        double* Y = as<double>(ctx->ws_work[which]);
+        tm.mark(3);
+        TT_TRY(tsmm_device(ctx, cur.data, cur.rows, (int)m, cur.ld, d_V, m, (int)rnew, Y, out_rows, out_cols, ldy));
+        tm.mark(4);
+        if (tm.on) {
+            st.t_tsqr_ms = tm.ms(0, 1);
+            st.t_svd_ms = tm.ms(1, 2);
+            st.t_tsmm_ms = tm.ms(3, 4);
+        }
+        out->steps.push_back(st);
+        out->sigmas.push_back(sig);
+        cur = WorkView{Y, out_rows, out_cols, ldy};
+        which ^= 1;
+        r = rnew;
+    }
+    // T^(1): the final 1 x (n_1 r_1) work matrix (tt_svd.hpp:193-197)
+    std::vector<double> first((size_t)(dims[0] * r));
+    if (cur.rows == 1) {
+        // row 0 of every column: stride ld
+        std::vector<double> tmp((size_t)cur.cols);
+        TT_TRY(ensure_host(ctx->host_stage, (size_t)cur.cols * 8));
+        TT_CUDA(cudaMemcpy2DAsync(ctx->host_stage.p, 8, cur.data, cur.ld * 8, 8, cur.cols, cudaMemcpyDeviceToHost,
+                                  ctx->stream));
+        TT_CUDA(cudaStreamSynchronize(ctx->stream));
+        std::memcpy(first.data(), ctx->host_stage.p, (size_t)cur.cols * 8);
+    } else {
+        for (int64_t l = 0; l < dims[0] * r; ++l) {
+            double v;
+            TT_TRY(d2h(ctx, &v, cur.data + (l / cur.rows) * cur.ld + l % cur.rows, 1));
+            first[l] = v;
+        }
+    }
+    out->cores[0] = std::move(first);
+    out->ranks[0] = 1;
+    out->ranks[1] = r;
+    out->ranks[d] = 1;
+    return TTSVD_OK;
+}
+
+}  // namespace
+
+// =========================================================================
+extern "C" {
+
+const char* ttsvd_cu_version(void) { return "ttsvd_cu 0.1 (sm_100a)"; }
+const char* ttsvd_cu_last_error(void) { return g_last_error.c_str(); }
+
+int64_t ttsvd_cu_padded_stride(int64_t n) { return padded_stride_h(n); }
+
+int ttsvd_cu_ctx_create(int device, void* stream, ttsvd_cu_ctx** out) {
+    if (!out) return fail(TTSVD_ERR_INVALID, "null out");
+    *out = nullptr;
+    int count = 0;
+    TT_CUDA(cudaGetDeviceCount(&count));
+    if (device < 0 || device >= count) return fail(TTSVD_ERR_DEVICE, "no such CUDA device");
+    TT_CUDA(cudaSetDevice(device));
+    auto* c = new ttsvd_cu_ctx();
+    c->device = device;
+    c->stream = static_cast<cudaStream_t>(stream);
+    cudaDeviceProp prop{};
+    if (cudaGetDeviceProperties(&prop, device) != cudaSuccess || prop.major < 10) {
+        delete c;
+        return fail(TTSVD_ERR_DEVICE, "ttsvd_cu requires an sm_100 (Blackwell) device");
+    }
+    c->num_sms = prop.multiProcessorCount;
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, jacobi_coop_kernel<kJacobiThreads>, kJacobiThreads, 0);
+    c->coop_max_blocks = std::max(1, per_sm) * c->num_sms;
+    for (auto& e : c->ev) cudaEventCreate(&e);
+    *out = c;
+    return TTSVD_OK;
+}
+
+int ttsvd_cu_ctx_destroy(ttsvd_cu_ctx* ctx) {
+    if (!ctx) return TTSVD_OK;
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    for (DevBuf* b : {&ctx->ws_R, &ctx->ws_R2, &ctx->ws_A, &ctx->ws_V, &ctx->ws_sigma, &ctx->ws_flags, &ctx->ws_work[0],
+                      &ctx->ws_work[1], &ctx->ws_X, &ctx->ws_send, &ctx->ws_recv})
+        if (b->p) cudaFree(b->p);
+    if (ctx->host_stage.p) cudaFreeHost(ctx->host_stage.p);
+    for (auto& e : ctx->ev)
+        if (e) cudaEventDestroy(e);
+    delete ctx;
+    return TTSVD_OK;
+}
+
+int ttsvd_cu_ctx_set_stream(ttsvd_cu_ctx* ctx, void* stream) {
+    if (!ctx) return fail(TTSVD_ERR_INVALID, "null context");
+    ctx->stream = static_cast<cudaStream_t>(stream);
+    return TTSVD_OK;
+}
+
+int ttsvd_cu_synchronize(ttsvd_cu_ctx* ctx) {
+    TT_TRY(set_device(ctx));
+    TT_CUDA(cudaStreamSynchronize(ctx->stream));
+    return TTSVD_OK;
+}
+
+int64_t ttsvd_cu_ctx_launches(const ttsvd_cu_ctx* ctx) { return ctx ? ctx->launches : -1; }
+
+int ttsvd_cu_ctx_set_timing(ttsvd_cu_ctx* ctx, int on) {
+    if (!ctx) return fail(TTSVD_ERR_INVALID, "null context");
+    ctx->timing = on != 0;
+    return TTSVD_OK;
+}
+
+int ttsvd_cu_tsqr(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int64_t m, int64_t ldx, double* R) {
+    TT_TRY(set_device(ctx));
+    if (m < 1) return fail(TTSVD_ERR_DIMENSION, "tsqr: needs at least one column");
+    if (n < m) return fail(TTSVD_ERR_DIMENSION, "tsqr: requires n >= m");
+    if (m > 4096) return fail(TTSVD_ERR_DIMENSION, "tsqr: m > 4096 not supported");
+    if (!X || !R || ldx < n) return fail(TTSVD_ERR_INVALID, "tsqr: bad pointer or leading dimension");
+    return tsqr_device(ctx, X, n, (int)m, ldx, R);
+}
+
+int ttsvd_cu_reduce_block(ttsvd_cu_ctx* ctx, const double* M, int64_t rows, int64_t m, int64_t ldm,
+                          const double* R_in, int64_t r_m, double* R_out) {
+    TT_TRY(set_device(ctx));
+    if (r_m != m) return fail(TTSVD_ERR_DIMENSION_MISMATCH, "reduce_block: R.m != M.cols");
+    if (m < 1 || rows < 0 || !R_in || !R_out || (rows > 0 && (!M || ldm < rows)))
+        return fail(TTSVD_ERR_INVALID, "reduce_block: bad arguments");
+    // stage [R_in, M] as two parts of a 2-part merge (M as an m-row block when
+    // rows <= m, else through the sweep path with R_in folded in afterwards)
+    if (rows == 0) {
+        TT_CUDA(cudaMemcpyAsync(R_out, R_in, (size_t)m * m * 8, cudaMemcpyDeviceToDevice, ctx->stream));
+        return TTSVD_OK;
+    }
+    TT_TRY(ensure(ctx->ws_send, (size_t)2 * m * m * 8));
+    double* parts = as<double>(ctx->ws_send);
+    TT_CUDA(cudaMemcpyAsync(parts, R_in, (size_t)m * m * 8, cudaMemcpyDeviceToDevice, ctx->stream));
+    TT_TRY(tsqr_device(ctx, M, rows, (int)m, ldm, parts + m * m));
+    return merge_tree(ctx, parts, 2, (int)m, R_out);
+}
+
+int ttsvd_cu_combine_factors(ttsvd_cu_ctx* ctx, const double* parts, int64_t P, int64_t m, double* R) {
+    TT_TRY(set_device(ctx));
+    if (P < 1) return fail(TTSVD_ERR_DIMENSION_MISMATCH, "combine_factors: empty list");
+    if (m < 1 || !parts || !R) return fail(TTSVD_ERR_INVALID, "combine_factors: bad arguments");
+    TT_TRY(ensure(ctx->ws_recv, (size_t)P * m * m * 8));
+    double* buf = as<double>(ctx->ws_recv);
+    TT_CUDA(cudaMemcpyAsync(buf, parts, (size_t)P * m * m * 8, cudaMemcpyDeviceToDevice, ctx->stream));
+    return merge_tree(ctx, buf, P, (int)m, R);
+}
+
+int ttsvd_cu_small_svd(ttsvd_cu_ctx* ctx, const double* R, int64_t m, double* sigma, double* V) {
+    TT_TRY(set_device(ctx));
+    if (m > 4096) return fail(TTSVD_ERR_DIMENSION_MISMATCH, "small_svd: m exceeds 4096");
+    if (m < 1 || !R || !sigma || !V) return fail(TTSVD_ERR_INVALID, "small_svd: bad arguments");
+    int sweeps = 0;
+    TT_TRY(svd_columns(ctx, R, m, m, m, true, sigma, V, &sweeps));
+    TT_CUDA(cudaStreamSynchronize(ctx->stream));
+    return TTSVD_OK;
+}
+
+int ttsvd_cu_jacobi_svd(ttsvd_cu_ctx* ctx, const double* A, int64_t n, int64_t m, int64_t lda, double* sigma,
+                        double* V, double* U) {
+    TT_TRY(set_device(ctx));
+    if (n < m) return fail(TTSVD_ERR_DIMENSION, "jacobi_svd: requires n >= m");
+    if (m < 1 || !A || !sigma || !V || lda < n) return fail(TTSVD_ERR_INVALID, "jacobi_svd: bad arguments");
+    TT_TRY(ensure(ctx->ws_A, (size_t)n * m * 8));
+    TT_TRY(ensure(ctx->ws_X, (size_t)m * m * 8));
+    double* W = as<double>(ctx->ws_A);
+    double* Vacc = as<double>(ctx->ws_X);
+    TT_CUDA(cudaMemcpy2DAsync(W, n * 8, A, lda * 8, n * 8, m, cudaMemcpyDeviceToDevice, ctx->stream));
+    TT_TRY(jacobi_device(ctx, W, (int)n, (int)m, Vacc));
+    int sweeps = 0;
+    TT_TRY(jacobi_status(ctx, &sweeps));
+    double* Uout = U;
+    if (!Uout) {
+        TT_TRY(ensure(ctx->ws_V, (size_t)n * m * 8));
+        Uout = as<double>(ctx->ws_V);
+    }
+    TT_TRY(finalize_device(ctx, W, (int)n, (int)m, Vacc, sigma, Uout, V));
+    TT_CUDA(cudaStreamSynchronize(ctx->stream));
+    return TTSVD_OK;
+}
+
+int ttsvd_cu_select_rank(ttsvd_cu_ctx* ctx, const double* sigma, int64_t m, double delta, int64_t r_max,
+                         int64_t* rank_host) {
+    TT_TRY(set_device(ctx));
+    if (!sigma || !rank_host || m < 0) return fail(TTSVD_ERR_INVALID, "select_rank: bad arguments");
+    std::vector<double> s((size_t)std::max<int64_t>(m, 1));
+    if (m > 0) TT_TRY(d2h(ctx, s.data(), sigma, (size_t)m));
+    *rank_host = select_rank_h(s.data(), m, delta, r_max);
+    return TTSVD_OK;
+}
+
+int ttsvd_cu_derive_delta(double norm_source, double eps, int64_t d, double* delta_host) {
+    if (d < 2) return fail(TTSVD_ERR_DEGENERATE, "derive_delta: requires d >= 2");
+    if (!delta_host) return fail(TTSVD_ERR_INVALID, "derive_delta: null out");
+    *delta_host = eps / std::sqrt((double)(d - 1)) * norm_source;
+    return TTSVD_OK;
+}
+
+int ttsvd_cu_tsmm_reshape(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int64_t m, int64_t ldx, const double* V,
+                          int64_t k, int64_t ldv, double* Y, int64_t out_rows, int64_t out_cols, int64_t ldy) {
+    TT_TRY(set_device(ctx));
+    if (k > m) return fail(TTSVD_ERR_SHAPE, "tsmm_reshape: k > m (kernel only shrinks)");
+    if (out_rows < 1 || out_cols < 1 || n * k != out_rows * out_cols)
+        return fail(TTSVD_ERR_SHAPE, "tsmm_reshape: out shape does not hold n*k elements");
+    if (!X || !V || !Y || ldx < n || ldv < m || ldy < out_rows || k < 1)
+        return fail(TTSVD_ERR_INVALID, "tsmm_reshape: bad pointer or leading dimension");
+    if ((size_t)m * 8 > 200 * 1024) return fail(TTSVD_ERR_SHAPE, "tsmm_reshape: m too large");
+    return tsmm_device(ctx, X, n, (int)m, ldx, V, ldv, (int)k, Y, out_rows, out_cols, ldy);
+}
+
+int ttsvd_cu_tt_svd(ttsvd_cu_ctx* ctx, const double* X, const int64_t* dims, int64_t d, int64_t ldx, int64_t r_max,
+                    double eps, ttsvd_cu_tt** out) {
+    TT_TRY(set_device(ctx));
+    if (!out || !dims || !X) return fail(TTSVD_ERR_INVALID, "tt_svd: null argument");
+    *out = nullptr;
+    if (d < 2) return fail(TTSVD_ERR_DEGENERATE, "tt_svd_tsqr: requires d >= 2");
+    int64_t total = 1;
+    for (int64_t i = 0; i < d; ++i) {
+        if (dims[i] < 1) return fail(TTSVD_ERR_DIMENSION, "Shape: extents must be >= 1");
+        total *= dims[i];
+    }
+    const int64_t rows = total / dims[d - 1];
+    if (ldx < rows) return fail(TTSVD_ERR_LAYOUT, "tt_svd: leading stride below the row count");
+    if (r_max <= 0) r_max = INT64_MAX;
+    auto* tt = new ttsvd_cu_tt();
+    std::vector<int64_t> dv(dims, dims + d);
+    int rc = run_chain(ctx, WorkView{X, rows, dims[d - 1], ldx}, dv, r_max, eps, d, tt);
+    if (rc != TTSVD_OK) {
+        delete tt;
+        return rc;
+    }
+    *out = tt;
+    return TTSVD_OK;
+}
+
+int ttsvd_cu_tt_svd_host(ttsvd_cu_ctx* ctx, const double* X_host, const int64_t* dims, int64_t d, int64_t ldx,
+                         int64_t r_max, double eps, ttsvd_cu_tt** out) {
+    TT_TRY(set_device(ctx));
+    if (!X_host || !dims || d < 1) return fail(TTSVD_ERR_INVALID, "tt_svd_host: null argument");
+    int64_t total = 1;
+    for (int64_t i = 0; i < d; ++i) total *= dims[i];
+    const size_t bytes = (size_t)ldx * dims[d - 1] * 8;
+    (void)total;
+    TT_TRY(ensure(ctx->ws_recv, bytes));
+    TT_CUDA(cudaMemcpyAsync(ctx->ws_recv.p, X_host, bytes, cudaMemcpyHostToDevice, ctx->stream));
+    return ttsvd_cu_tt_svd(ctx, as<double>(ctx->ws_recv), dims, d, ldx, r_max, eps, out);
+}
+
+int ttsvd_cu_tt_svd_distributed(ttsvd_cu_ctx* ctx, const double* const* slabs, int64_t n_slabs, int64_t part0,
+                                int64_t P_total, const int64_t* ldims, int64_t d_local, int64_t ld_slab,
+                                int64_t r_max, double eps, ttsvd_cu_exchange_fn exchange, void* user,
+                                ttsvd_cu_tt** out) {
+    TT_TRY(set_device(ctx));
+    if (!out || !slabs || !ldims || n_slabs < 1 || d_local < 1) return fail(TTSVD_ERR_PARTITION, "tt_svd_distributed: no partitions");
+    *out = nullptr;
+    if (P_total < n_slabs || part0 < 0 || part0 + n_slabs > P_total || P_total % n_slabs != 0)
+        return fail(TTSVD_ERR_PARTITION, "tt_svd_distributed: inconsistent partition counts");
+    if (n_slabs != P_total && !exchange)
+        return fail(TTSVD_ERR_INVALID, "tt_svd_distributed: exchange callback required across processes");
+    if (r_max <= 0) r_max = INT64_MAX;
+    const int64_t d = d_local + 1;
+    int64_t total = 1;
+    for (int64_t i = 0; i < d_local; ++i) total *= ldims[i];
+    auto* tt = new ttsvd_cu_tt();
+    std::vector<int64_t> gdims(d);
+    gdims[0] = P_total;
+    for (int64_t i = 0; i < d_local; ++i) gdims[i + 1] = ldims[i];
+    auto done = [&](int rc) -> int {
+        if (rc != TTSVD_OK) {
+            delete tt;
+            return rc;
+        }
+        *out = tt;
+        return (int)TTSVD_OK;
+    };
+    if (P_total == 1) {
+        gdims[0] = 1;
+        const int64_t rows = d_local == 1 ? 1 : total / ldims[d_local - 1];
+        return done(run_chain(ctx, WorkView{slabs[0], rows, ldims[d_local - 1], ld_slab}, gdims, r_max, eps, d, tt));
+    }
+    // per-slab state: ping-pong buffers owned here
+    std::vector<WorkView> cur(n_slabs);
+    std::vector<DevBuf> bufs(2 * n_slabs);
+    auto free_bufs = [&]() {
+        for (auto& b : bufs)
+            if (b.p) cudaFree(b.p);
+    };
+    for (int64_t p = 0; p < n_slabs; ++p) {
+        if (d_local == 1) cur[p] = WorkView{slabs[p], 1, ldims[0], ld_slab};
+        else cur[p] = WorkView{slabs[p], total / ldims[d_local - 1], ldims[d_local - 1], ld_slab};
+    }
+    tt->dims = gdims;
+    tt->cores.assign(d, {});
+    tt->ranks.assign(d + 1, 1);
+    double delta = -1.0;
+    int64_t r = 1;
+    int flip = 0;
+    std::vector<double> sig, Vh;
+    int rc = TTSVD_OK;
+    for (int64_t i = d_local - 1; i >= 0 && rc == TTSVD_OK; --i) {
+        const int64_t n_i = ldims[i];
+        const int64_t m = n_i * r;
+        const size_t mm = (size_t)m * m;
+        if ((rc = ensure(ctx->ws_send, n_slabs * mm * 8)) != TTSVD_OK) break;
+        if ((rc = ensure(ctx->ws_recv, P_total * mm * 8)) != TTSVD_OK) break;
+        double* send = as<double>(ctx->ws_send);
+        double* recv = n_slabs == P_total ? send : as<double>(ctx->ws_recv);
+        // gram_triangular per local partition (tt_svd.hpp:204-210, 573)
+        for (int64_t p = 0; p < n_slabs && rc == TTSVD_OK; ++p)
+            rc = tsqr_device(ctx, cur[p].data, cur[p].rows, (int)m, cur[p].ld, send + p * mm);
+        if (rc != TTSVD_OK) break;
+        if (n_slabs != P_total) {
+            if (exchange(user, send, recv, (int64_t)(n_slabs * mm), (void*)ctx->stream) != 0) {
+                rc = fail(TTSVD_ERR_DEVICE, "tt_svd_distributed: exchange failed");
+                break;
+            }
+        }
+        // pinned-order combine over all partitions (tt_svd.hpp:575)
+        if ((rc = ensure(ctx->ws_X, mm * 8)) != TTSVD_OK) break;
+        double* R = as<double>(ctx->ws_X);
+        if ((rc = ensure(ctx->ws_R2, ((P_total + 1) / 2) * mm * 8)) != TTSVD_OK) break;
+        if ((rc = merge_tree(ctx, recv, P_total, (int)m, R)) != TTSVD_OK) break;
+        // duplicated small SVD (tt_svd.hpp:579-606): identical on every process
+        if ((rc = ensure(ctx->ws_sigma, (size_t)m * 8)) != TTSVD_OK) break;
+        if ((rc = ensure(ctx->ws_V, mm * 8)) != TTSVD_OK) break;
+        double* d_sigma = as<double>(ctx->ws_sigma);
+        double* d_V = as<double>(ctx->ws_V);
+        int sweeps = 0;
+        if ((rc = svd_columns(ctx, R, m, m, m, true, d_sigma, d_V, &sweeps)) != TTSVD_OK) break;
+        sig.resize(m);
+        if ((rc = d2h(ctx, sig.data(), d_sigma, m)) != TTSVD_OK) break;
+        const int64_t global_rows = cur[0].rows * P_total;
+        const int64_t nsig = std::min(m, global_rows);
+        if (delta < 0.0) delta = eps / std::sqrt((double)(d - 1)) * sigma_norm_h(sig.data(), m);
+        const int64_t rnew = choose_rank_h(sig.data(), m, m, nsig, delta, r_max, global_rows);
+        Vh.resize((size_t)m * rnew);
+        if ((rc = d2h(ctx, Vh.data(), d_V, (size_t)m * rnew)) != TTSVD_OK) break;
+        std::vector<double> core((size_t)(rnew * n_i * r));
+        for (int64_t b = 0; b < r; ++b)
+            for (int64_t x = 0; x < n_i; ++x)
+                for (int64_t a = 0; a < rnew; ++a) core[a + rnew * (x + n_i * b)] = Vh[a * m + (x + n_i * b)];
+        tt->cores[i + 1] = std::move(core);
+        tt->ranks[i + 1] = rnew;
+        ttsvd_cu_step st{};
+        st.rows = global_rows;
+        st.cols = m;
+        st.nsig = nsig;
+        st.rank = rnew;
+        tt->steps.push_back(st);
+        tt->sigmas.push_back(sig);
+        for (int64_t p = 0; p < n_slabs && rc == TTSVD_OK; ++p) {
+            const int64_t out_rows = i >= 1 ? cur[p].rows / ldims[i - 1] : 1;
+            const int64_t out_cols = i >= 1 ? ldims[i - 1] * rnew : rnew;
+            const int64_t ldy = padded_stride_h(out_rows);
+            DevBuf& b = bufs[2 * p + flip];
+            if ((rc = ensure(b, (size_t)ldy * out_cols * 8)) != TTSVD_OK) break;
+            rc = tsmm_device(ctx, cur[p].data, cur[p].rows, (int)m, cur[p].ld, d_V, m, (int)rnew, as<double>(b),
+                             out_rows, out_cols, ldy);
+            cur[p] = WorkView{as<double>(b), out_rows, out_cols, ldy};
+        }
+        flip ^= 1;
+        r = rnew;
+    }
+    if (rc == TTSVD_OK) {
+        // gather T^(1) (tt_svd.hpp:616-621): row 0 of each partition's 1 x r matrix
+        const size_t cnt = (size_t)n_slabs * r;
+        rc = ensure(ctx->ws_send, cnt * 8);
+        if (rc == TTSVD_OK) rc = ensure(ctx->ws_recv, (size_t)P_total * r * 8);
+        double* send = as<double>(ctx->ws_send);
+        for (int64_t p = 0; p < n_slabs && rc == TTSVD_OK; ++p) {
+            cudaError_t e = cudaMemcpy2DAsync(send + p * r, 8, cur[p].data, cur[p].ld * 8, 8, r,
+                                              cudaMemcpyDeviceToDevice, ctx->stream);
+            if (e != cudaSuccess) rc = fail(TTSVD_ERR_DEVICE, cudaGetErrorString(e));
+        }
+        double* recv = send;
+        if (rc == TTSVD_OK && n_slabs != P_total) {
+            recv = as<double>(ctx->ws_recv);
+            if (exchange(user, send, recv, (int64_t)cnt, (void*)ctx->stream) != 0)
+                rc = fail(TTSVD_ERR_DEVICE, "tt_svd_distributed: exchange failed");
+        }
+        std::vector<double> vals((size_t)P_total * r);
+        if (rc == TTSVD_OK) rc = d2h(ctx, vals.data(), recv, vals.size());
+        if (rc == TTSVD_OK) {
+            std::vector<double> first((size_t)P_total * r);
+            for (int64_t p = 0; p < P_total; ++p)
+                for (int64_t b = 0; b < r; ++b) first[p + P_total * b] = vals[p * r + b];
+            tt->cores[0] = std::move(first);
+            tt->ranks[0] = 1;
+            tt->ranks[1] = r;
+            tt->ranks[d] = 1;
+        }
+    }
+    cudaStreamSynchronize(ctx->stream);
+    free_bufs();
+    (void)part0;
+    return done(rc);
+}
+
+int64_t ttsvd_cu_tt_d(const ttsvd_cu_tt* tt) { return tt ? (int64_t)tt->dims.size() : -1; }
+
+int ttsvd_cu_tt_ranks(const ttsvd_cu_tt* tt, int64_t* ranks) {
+    if (!tt || !ranks) return fail(TTSVD_ERR_INVALID, "tt_ranks: null");
+    std::copy(tt->ranks.begin(), tt->ranks.end(), ranks);
+    return TTSVD_OK;
+}
+
+int ttsvd_cu_tt_core(const ttsvd_cu_tt* tt, int64_t j, double* dst) {
+    if (!tt || !dst || j < 0 || j >= (int64_t)tt->cores.size()) return fail(TTSVD_ERR_INVALID, "tt_core: bad index");
+    std::copy(tt->cores[j].begin(), tt->cores[j].end(), dst);
+    return TTSVD_OK;
+}
+
+int64_t ttsvd_cu_tt_nsteps(const ttsvd_cu_tt* tt) { return tt ? (int64_t)tt->steps.size() : -1; }
+
+int ttsvd_cu_tt_step(const ttsvd_cu_tt* tt, int64_t s, ttsvd_cu_step* o) {
+    if (!tt || !o || s < 0 || s >= (int64_t)tt->steps.size()) return fail(TTSVD_ERR_INVALID, "tt_step: bad index");
+    *o = tt->steps[s];
+    return TTSVD_OK;
+}
+
+int ttsvd_cu_tt_sigma(const ttsvd_cu_tt* tt, int64_t s, double* dst) {
+    if (!tt || !dst || s < 0 || s >= (int64_t)tt->sigmas.size()) return fail(TTSVD_ERR_INVALID, "tt_sigma: bad index");
+    std::copy(tt->sigmas[s].begin(), tt->sigmas[s].end(), dst);
+    return TTSVD_OK;
+}
+
+void ttsvd_cu_tt_free(ttsvd_cu_tt* tt) { delete tt; }
+
+int ttsvd_cu_gen_uniform(ttsvd_cu_ctx* ctx, uint64_t seed, int64_t total, int64_t rows, int64_t ld, double* X) {
+    TT_TRY(set_device(ctx));
+    if (!X || rows < 1 || ld < rows || total < 0) return fail(TTSVD_ERR_INVALID, "gen_uniform: bad arguments");
+    const int64_t blocks = std::min<int64_t>((total + 255) / 256, (int64_t)ctx->num_sms * 16);
+    gen_uniform_kernel<<<(unsigned)std::max<int64_t>(blocks, 1), 256, 0, ctx->stream>>>(seed, total, rows, ld, X);
+    return check_launch(ctx, "gen_uniform_kernel");
+}
+
+}  // extern "C"

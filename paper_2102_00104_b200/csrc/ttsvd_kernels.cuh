@@ -1,0 +1,498 @@
+// sm_100a kernels of the TT-SVD hot path (arXiv 2102.00104, Alg. 2/5/6).
+//
+//   K_TSQR   tsqr_tile_kernel      Q-less structured Householder over row tiles,
+//                                  per-CTA flat tree (tsqr.hpp:247-292) and the
+//                                  index-ordered merge tree (tsqr.hpp:230-240)
+//   K_SVD    jacobi_kernel         one-sided Jacobi (small_svd.hpp:72-114) in a
+//                                  parallel round-robin order; single CTA with
+//                                  the matrix in shared memory, or a cooperative
+//                                  grid with the matrix in L2
+//            jacobi_finalize       norms, stable descending sort, normalisation
+//                                  and the deterministic completion
+//                                  (small_svd.hpp:133-191)
+//   K_TSMM   tsmm_kernel           Y = reshape(X V) written straight into the
+//                                  next step's padded layout (tsmm.hpp:20-71)
+//
+// All arithmetic is fp64.  Everything here is deterministic for a fixed launch
+// shape: no floating-point atomics, fixed reduction trees.
+#pragma once
+
+#include <cooperative_groups.h>
+#include <cstdint>
+#include <cfloat>
+
+namespace ttsvd_b200 {
+
+namespace cg = cooperative_groups;
+
+constexpr int kWarp = 32;
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+__device__ __forceinline__ double ldg_stream(const double* p) {
+    double v;
+    asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+    return v;
+}
+
+// ---------------------------------------------------------------------------
+// Synthetic input: counter-based uniform[-1,1) (restated in oracle/ttsvd_oracle.c
+// orc_gen_uniform; both steps are exact in fp64 so host and device agree).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint64_t splitmix64(uint64_t z) {
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    return z ^ (z >> 31);
+}
+
+__global__ void gen_uniform_kernel(uint64_t seed, int64_t total, int64_t rows, int64_t ld, double* X) {
+    for (int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; l < total; l += (int64_t)gridDim.x * blockDim.x) {
+        const uint64_t z = splitmix64(seed + (uint64_t)(l + 1) * 0x9E3779B97F4A7C15ULL);
+        const double u = (double)(z >> 11) * 0x1.0p-53;
+        const int64_t j = l / rows;
+        X[j * ld + (l - j * rows)] = 2.0 * u - 1.0;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K_TSQR — structured Householder reduction of [R; B] over row tiles.
+//
+// One CTA owns a job: a contiguous row range of a column-major matrix and a
+// running m x m upper-triangular R.  Each tile of `bt` rows is staged in shared
+// memory and folded into R column by column.  Reflector j spans R(j,j) and
+// the tile's column j (R's rows above j are final, rows below are zero), the
+// reference's eps_fp trick (tsqr.hpp:120-142) keeps it branch-free:
+//     t = eps + ||u||^2, alpha = -sign(u0) sqrt(t + eps), t -= alpha u0,
+//     beta = 1/sqrt(t), v = beta (u - alpha e1), ||v||^2 = 2.
+// The trailing columns are updated by warps (one column per warp at a time,
+// lanes over rows, shuffle reduction).  Two modes:
+//   mode 0 (sweep):  job g = rows [g*n/G, (g+1)*n/G) of X, R starts at 0;
+//   mode 1 (merge):  job i stacks part 2i+1 (m x m, ld m) under part 2i —
+//                    one level of the fixed index-ordered merge tree.
+// ---------------------------------------------------------------------------
+struct TsqrArgs {
+    const double* X;   // mode 0: matrix; mode 1: parts base (count * m*m)
+    int64_t n;         // mode 0: rows; mode 1: number of parts at this level
+    int64_t ld;        // mode 0: leading dimension
+    double* R_out;     // job outputs, m*m each (ld m)
+    int m;
+    int bt;            // tile rows
+    int ldb;           // tile leading dimension in shared memory
+    int mode;
+    int r_in_smem;
+};
+
+template <int NT>
+__global__ void __launch_bounds__(NT) tsqr_tile_kernel(TsqrArgs a) {
+    extern __shared__ __align__(16) double smem[];
+    constexpr int NW = NT / kWarp;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int m = a.m;
+    const int64_t job = blockIdx.x;
+
+    const double* X;
+    int64_t row0, row1, ld;
+    const double* R_init = nullptr;
+    double* R_out = a.R_out + job * (int64_t)m * m;
+    if (a.mode == 0) {
+        const int64_t G = gridDim.x;
+        const int64_t base = a.n / G, rem = a.n % G;
+        row0 = job * base + (job < rem ? job : rem);
+        row1 = row0 + base + (job < rem ? 1 : 0);
+        X = a.X;
+        ld = a.ld;
+    } else {
+        const int64_t count = a.n;
+        R_init = a.X + (2 * job) * (int64_t)m * m;
+        if (2 * job + 1 < count) {
+            X = a.X + (2 * job + 1) * (int64_t)m * m;
+            row0 = 0;
+            row1 = m;
+        } else {
+            X = nullptr;
+            row0 = row1 = 0;
+        }
+        ld = m;
+    }
+
+    double* R = a.r_in_smem ? smem : R_out;
+    double* B = smem + (a.r_in_smem ? m * m : 0);
+    double* red = B + (int64_t)a.ldb * m;  // NW + 4 doubles
+
+    for (int e = tid; e < m * m; e += NT) R[e] = R_init ? R_init[e] : 0.0;
+    __syncthreads();
+
+    const double eps = DBL_MIN;
+    for (int64_t r0 = row0; r0 < row1; r0 += a.bt) {
+        const int rows = (int)((row1 - r0) < (int64_t)a.bt ? (row1 - r0) : (int64_t)a.bt);
+        for (int j = 0; j < m; ++j) {
+            const double* src = X + j * ld + r0;
+            double* dst = B + j * a.ldb;
+            for (int i = tid; i < rows; i += NT) dst[i] = src[i];
+        }
+        __syncthreads();
+        for (int j = 0; j < m; ++j) {
+            const double* bj = B + j * a.ldb;
+            double s = 0.0;
+            for (int i = tid; i < rows; i += NT) s += bj[i] * bj[i];
+            s = warp_sum(s);
+            if (lane == 0) red[warp] = s;
+            __syncthreads();
+            if (tid == 0) {
+                double tot = 0.0;
+                for (int w = 0; w < NW; ++w) tot += red[w];
+                const double u0 = R[j * m + j];
+                double t = eps + (u0 * u0 + tot);
+                double alpha = sqrt(t + eps);
+                alpha = (u0 > 0.0) ? -alpha : alpha;
+                t -= alpha * u0;
+                const double beta = 1.0 / sqrt(t);
+                red[NW + 0] = alpha;
+                red[NW + 1] = beta;
+                red[NW + 2] = (u0 - alpha) * beta;
+            }
+            __syncthreads();
+            const double alpha = red[NW + 0], beta = red[NW + 1], v0 = red[NW + 2];
+            for (int k = j + 1 + warp; k < m; k += NW) {
+                double* bk = B + k * a.ldb;
+                double p = 0.0;
+                for (int i = lane; i < rows; i += kWarp) p += bj[i] * bk[i];
+                p = warp_sum(p);
+                const double rjk = R[k * m + j];
+                const double g = v0 * rjk + beta * p;
+                const double gb = g * beta;
+                for (int i = lane; i < rows; i += kWarp) bk[i] -= gb * bj[i];
+                if (lane == 0) R[k * m + j] = rjk - g * v0;
+            }
+            __syncthreads();
+            if (tid == 0) R[j * m + j] = alpha;
+        }
+        __syncthreads();
+    }
+    if (a.r_in_smem) {
+        for (int e = tid; e < m * m; e += NT) R_out[e] = R[e];
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K_SVD — one-sided Jacobi on the columns of A (n x m, ld n).
+//
+// Pairs follow the circle method: in round r (0 <= r < mp-1, mp = m rounded
+// up to even) pair i is (r, mp-1) for i = 0 and ((r+i) mod (mp-1),
+// (r-i) mod (mp-1)) otherwise; every unordered pair meets once per sweep, and
+// the mp/2 pairs of a round are independent.  The rotation and the skip rule
+// are the reference's (small_svd.hpp:84-108): skip if |gamma| <= 1e2 eps
+// sqrt(alpha beta); converged after a sweep without rotations; at most 30
+// sweeps.  With `acc` the rotations are also applied to Vacc (m x m) — that
+// gives jacobi_svd()'s V.  Without it the orthogonalised columns themselves
+// are the wanted singular vectors (the driver runs this on R^T or W^T).
+// ---------------------------------------------------------------------------
+struct JacobiArgs {
+    double* A;     // n x m, ld n (global)
+    double* Vacc;  // m x m or nullptr
+    int n, m;
+    int* sweep_flags;  // >= max_sweeps ints, zeroed (cooperative mode)
+    int* status;       // out: sweeps used, or -1 if not converged
+    int max_sweeps;
+};
+
+__device__ __forceinline__ void circle_pair(int r, int i, int mp, int& p, int& q) {
+    const int M1 = mp - 1;
+    if (i == 0) {
+        p = r;
+        q = M1;
+    } else {
+        p = (r + i) % M1;
+        q = (r - i + M1) % M1;
+    }
+    if (p > q) {
+        const int t = p;
+        p = q;
+        q = t;
+    }
+}
+
+__device__ __forceinline__ bool jacobi_pair(double* ap, double* aq, int n, double* vp, double* vq, int m, int lane) {
+    double al = 0.0, be = 0.0, ga = 0.0;
+    for (int i = lane; i < n; i += kWarp) {
+        const double x = ap[i], y = aq[i];
+        al += x * x;
+        be += y * y;
+        ga += x * y;
+    }
+    al = warp_sum(al);
+    be = warp_sum(be);
+    ga = warp_sum(ga);
+    const double tol = 1e2 * DBL_EPSILON;
+    if (fabs(ga) <= tol * sqrt(al * be)) return false;
+    const double zeta = (be - al) / (2.0 * ga);
+    const double t = ((zeta >= 0.0) ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+    const double c = 1.0 / sqrt(1.0 + t * t);
+    const double s = c * t;
+    for (int i = lane; i < n; i += kWarp) {
+        const double x = ap[i], y = aq[i];
+        ap[i] = c * x - s * y;
+        aq[i] = s * x + c * y;
+    }
+    if (vp) {
+        for (int i = lane; i < m; i += kWarp) {
+            const double x = vp[i], y = vq[i];
+            vp[i] = c * x - s * y;
+            vq[i] = s * x + c * y;
+        }
+    }
+    return true;
+}
+
+// single CTA, A (and Vacc) resident in shared memory
+template <int NT>
+__global__ void __launch_bounds__(NT) jacobi_smem_kernel(JacobiArgs a) {
+    extern __shared__ __align__(16) double smem[];
+    constexpr int NW = NT / kWarp;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int n = a.n, m = a.m, mp = (m + 1) & ~1;
+    double* A = smem;
+    double* V = a.Vacc ? smem + (int64_t)n * m : nullptr;
+    for (int64_t e = tid; e < (int64_t)n * m; e += NT) A[e] = a.A[e];
+    if (V)
+        for (int e = tid; e < m * m; e += NT) V[e] = (e % (m + 1) == 0) ? 1.0 : 0.0;
+    __syncthreads();
+    int sweep = 0;
+    bool converged = (m < 2);
+    for (; sweep < a.max_sweeps && !converged; ++sweep) {
+        int rotated = 0;
+        for (int r = 0; r < mp - 1; ++r) {
+            for (int i = warp; i < mp / 2; i += NW) {
+                int p, q;
+                circle_pair(r, i, mp, p, q);
+                if (q >= m) continue;
+                if (jacobi_pair(A + (int64_t)p * n, A + (int64_t)q * n, n, V ? V + p * m : nullptr,
+                                V ? V + q * m : nullptr, m, lane))
+                    rotated = 1;
+            }
+            __syncthreads();
+        }
+        converged = __syncthreads_or(rotated) == 0;
+    }
+    for (int64_t e = tid; e < (int64_t)n * m; e += NT) a.A[e] = A[e];
+    if (V)
+        for (int e = tid; e < m * m; e += NT) a.Vacc[e] = V[e];
+    if (tid == 0) *a.status = converged ? sweep : -1;
+}
+
+// cooperative grid, A (and Vacc) in global memory (L2 resident); grid.sync per round
+template <int NT>
+__global__ void __launch_bounds__(NT) jacobi_coop_kernel(JacobiArgs a) {
+    cg::grid_group grid = cg::this_grid();
+    constexpr int NW = NT / kWarp;
+    const int lane = threadIdx.x & 31;
+    const int gw = blockIdx.x * NW + (threadIdx.x >> 5);
+    const int tw = gridDim.x * NW;
+    const int n = a.n, m = a.m, mp = (m + 1) & ~1;
+    double* A = a.A;
+    double* V = a.Vacc;
+    if (V) {
+        for (int64_t e = blockIdx.x * (int64_t)NT + threadIdx.x; e < (int64_t)m * m; e += (int64_t)gridDim.x * NT)
+            V[e] = (e % (m + 1) == 0) ? 1.0 : 0.0;
+        grid.sync();
+    }
+    int sweep = 0;
+    bool converged = (m < 2);
+    for (; sweep < a.max_sweeps && !converged; ++sweep) {
+        int rotated = 0;
+        for (int r = 0; r < mp - 1; ++r) {
+            for (int i = gw; i < mp / 2; i += tw) {
+                int p, q;
+                circle_pair(r, i, mp, p, q);
+                if (q >= m) continue;
+                if (jacobi_pair(A + (int64_t)p * n, A + (int64_t)q * n, n, V ? V + (int64_t)p * m : nullptr,
+                                V ? V + (int64_t)q * m : nullptr, m, lane))
+                    rotated = 1;
+            }
+            grid.sync();
+        }
+        if (rotated && lane == 0) atomicAdd(&a.sweep_flags[sweep], 1);
+        grid.sync();
+        converged = *((volatile int*)&a.sweep_flags[sweep]) == 0;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) *a.status = converged ? sweep : -1;
+}
+
+// Column norms, stable descending order, sigma, normalised columns -> Uout
+// (n x m) with the reference's canonical completion for sigma <= n eps sigma_1
+// (small_svd.hpp:133-191), and Vacc permuted -> Vout (m x m) when given.
+// One CTA.  smem: norms[m], pos[m] (as double), deficient flags.
+template <int NT>
+__global__ void __launch_bounds__(NT) jacobi_finalize_kernel(const double* A, int n, int m, const double* Vacc,
+                                                             double* sigma, double* Uout, double* Vout) {
+    extern __shared__ __align__(16) double smem[];
+    constexpr int NW = NT / kWarp;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    double* norms = smem;
+    int* pos = reinterpret_cast<int*>(norms + m);
+    int* src_of = pos + m;
+    double* red = reinterpret_cast<double*>(src_of + m);  // 2m ints keep 8-byte alignment
+    for (int j = warp; j < m; j += NW) {
+        double s = 0.0;
+        const double* c = A + (int64_t)j * n;
+        for (int i = lane; i < n; i += kWarp) s += c[i] * c[i];
+        s = warp_sum(s);
+        if (lane == 0) norms[j] = sqrt(s);
+    }
+    __syncthreads();
+    for (int j = tid; j < m; j += NT) {
+        const double x = norms[j];
+        int p = 0;
+        for (int i = 0; i < m; ++i) {
+            const double y = norms[i];
+            p += (y > x) || (y == x && i < j);
+        }
+        pos[j] = p;
+        src_of[p] = j;
+    }
+    __syncthreads();
+    const double sigma1 = m > 0 ? norms[src_of[0]] : 0.0;
+    const double cutoff = sigma1 * (double)n * DBL_EPSILON;
+    for (int j = tid; j < m; j += NT) sigma[pos[j]] = norms[j];
+    for (int jj = warp; jj < m; jj += NW) {
+        const int src = src_of[jj];
+        const double s = norms[src];
+        double* u = Uout + (int64_t)jj * n;
+        const double* c = A + (int64_t)src * n;
+        if (s > cutoff) {
+            const double inv = 1.0 / s;
+            for (int i = lane; i < n; i += kWarp) u[i] = c[i] * inv;
+        } else {
+            for (int i = lane; i < n; i += kWarp) u[i] = 0.0;
+        }
+        if (Vout) {
+            const double* vs = Vacc + (int64_t)src * m;
+            double* vd = Vout + (int64_t)jj * m;
+            for (int i = lane; i < m; i += kWarp) vd[i] = vs[i];
+        }
+    }
+    __syncthreads();
+    __threadfence_block();
+    // deterministic completion of the deficient columns (rare; sequential over
+    // columns and axes, the CTA cooperates on each dot product)
+    int next_axis = 0;
+    for (int j = 0; j < m; ++j) {
+        if (norms[src_of[j]] > cutoff) continue;
+        double* uj = Uout + (int64_t)j * n;
+        for (; next_axis < n; ++next_axis) {
+            for (int i = tid; i < n; i += NT) uj[i] = (i == next_axis) ? 1.0 : 0.0;
+            __syncthreads();
+            for (int pass = 0; pass < 2; ++pass) {
+                for (int k = 0; k < m; ++k) {
+                    if (k == j) continue;
+                    const double* uk = Uout + (int64_t)k * n;
+                    double s = 0.0;
+                    for (int i = tid; i < n; i += NT) s += uk[i] * uj[i];
+                    s = warp_sum(s);
+                    if (lane == 0) red[warp] = s;
+                    __syncthreads();
+                    double dot = 0.0;
+                    for (int w = 0; w < NW; ++w) dot += red[w];
+                    for (int i = tid; i < n; i += NT) uj[i] -= dot * uk[i];
+                    __syncthreads();
+                }
+            }
+            double s = 0.0;
+            for (int i = tid; i < n; i += NT) s += uj[i] * uj[i];
+            s = warp_sum(s);
+            if (lane == 0) red[warp] = s;
+            __syncthreads();
+            double nrm = 0.0;
+            for (int w = 0; w < NW; ++w) nrm += red[w];
+            nrm = sqrt(nrm);
+            __syncthreads();
+            if (nrm > 0.5) {
+                for (int i = tid; i < n; i += NT) uj[i] /= nrm;
+                __syncthreads();
+                ++next_axis;
+                break;
+            }
+        }
+    }
+}
+
+// dst (cols x rows, ld cols) = src^T, src rows x cols with ld_src
+__global__ void transpose_kernel(const double* src, int64_t rows, int64_t cols, int64_t ld_src, double* dst) {
+    __shared__ double tile[32][33];
+    const int64_t bx = blockIdx.x * 32, by = blockIdx.y * 32;  // bx over cols, by over rows
+    for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+        const int64_t r = by + threadIdx.x, c = bx + k;
+        if (r < rows && c < cols) tile[k][threadIdx.x] = src[c * ld_src + r];
+    }
+    __syncthreads();
+    for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+        const int64_t c = bx + threadIdx.x, r = by + k;
+        if (r < rows && c < cols) dst[r * cols + c] = tile[threadIdx.x][k];
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K_TSMM — Y = reshape(X V[:, c0:c0+KC]).  One thread per row i; the V chunk
+// sits in shared memory as [j][c] so every FMA reads a broadcast; the KC
+// results of row i go to flat positions p = i + n*c, i.e. Y(p mod out_rows,
+// p div out_rows) (tsmm.hpp:14-19).  When out_rows divides n (every TT step)
+// the destination is column (i div out_rows) + n_next*c, row i mod out_rows,
+// so consecutive threads write consecutive addresses.
+// ---------------------------------------------------------------------------
+template <int KC>
+__global__ void __launch_bounds__(256) tsmm_kernel(const double* __restrict__ X, int64_t n, int m, int64_t ldx,
+                                                   const double* __restrict__ V, int64_t ldv, int k,
+                                                   double* __restrict__ Y, int64_t out_rows, int64_t ldy) {
+    extern __shared__ __align__(16) double Vs[];
+    const int c0 = blockIdx.y * KC;
+    const int kc = min(KC, k - c0);
+    for (int e = threadIdx.x; e < m * KC; e += blockDim.x) {
+        const int j = e / KC, c = e % KC;
+        Vs[e] = (c < kc) ? V[(int64_t)(c0 + c) * ldv + j] : 0.0;
+    }
+    __syncthreads();
+    const bool divisible = (n % out_rows) == 0;
+    const int64_t n_next = divisible ? n / out_rows : 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        double acc[KC];
+#pragma unroll
+        for (int c = 0; c < KC; ++c) acc[c] = 0.0;
+        const double* xi = X + i;
+#pragma unroll 4
+        for (int j = 0; j < m; ++j) {
+            const double x = ldg_stream(xi + (int64_t)j * ldx);
+            const double* vj = Vs + j * KC;
+#pragma unroll
+            for (int c = 0; c < KC; ++c) acc[c] = fma(vj[c], x, acc[c]);
+        }
+        if (divisible) {
+            const int64_t b = i / out_rows, ii = i - b * out_rows;
+#pragma unroll
+            for (int c = 0; c < KC; ++c)
+                if (c < kc) Y[(b + n_next * (c0 + c)) * ldy + ii] = acc[c];
+        } else {
+#pragma unroll
+            for (int c = 0; c < KC; ++c)
+                if (c < kc) {
+                    const int64_t p = i + n * (c0 + c);
+                    const int64_t col = p / out_rows;
+                    Y[col * ldy + (p - col * out_rows)] = acc[c];
+                }
+        }
+    }
+}
+
+// zero rows [out_rows, ldy) of every column of Y (the padded slots, storage.hpp:57)
+__global__ void zero_padding_kernel(double* Y, int64_t out_rows, int64_t ldy, int64_t cols) {
+    const int64_t pad = ldy - out_rows;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < pad * cols; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t c = e / pad;
+        Y[c * ldy + out_rows + (e - c * pad)] = 0.0;
+    }
+}
+
+}  // namespace ttsvd_b200

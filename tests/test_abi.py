@@ -1,0 +1,54 @@
+"""CPU checks of the drop-in boundary: the C-ABI library loads, exports every
+symbol include/ttsvd_cu.h declares, and fails cleanly (status code, message)
+without a GPU.  No compute calls here."""
+import ctypes as C
+import os
+
+import pytest
+
+
+def test_library_exports_every_header_symbol():
+    from paper_2102_00104_b200 import _lib
+    L = _lib.lib()
+    syms = _lib.header_symbols()
+    assert len(syms) >= 25
+    missing = [s for s in syms if not hasattr(L, s)]
+    assert not missing, missing
+    # and the ctypes signature table covers the header exactly
+    assert sorted(_lib._SIGS) == syms
+
+
+def test_no_gpu_is_a_clean_error():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    from paper_2102_00104_b200 import _lib
+    L = _lib.lib()
+    h = C.c_void_p()
+    rc = L.ttsvd_cu_ctx_create(0, None, C.byref(h))
+    assert rc == 8  # TTSVD_ERR_DEVICE
+    assert L.ttsvd_cu_last_error()
+
+
+def test_host_arithmetic_entries():
+    from paper_2102_00104_b200 import _lib
+    L = _lib.lib()
+    # shape.hpp:22-28 pins (test_storage.cpp:11-17)
+    for n, s in [(1, 64), (64, 64), (65, 192), (128, 192), (256, 320), (262144, 262208), (1 << 24, (1 << 24) + 64)]:
+        assert L.ttsvd_cu_padded_stride(n) == s
+    out = C.c_double()
+    assert L.ttsvd_cu_derive_delta(2.0, 0.1, 5, C.byref(out)) == 0 and abs(out.value - 0.1) < 1e-15
+    assert L.ttsvd_cu_derive_delta(1.0, 0.1, 1, C.byref(out)) == 6
+
+
+def test_c_header_compiles_standalone(tmp_path):
+    src = tmp_path / "t.c"
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    src.write_text('#include "ttsvd_cu.h"\nint main(void){return ttsvd_cu_padded_stride(1)==64?0:1;}\n')
+    import subprocess
+    lib = os.path.join(root, "paper_2102_00104_b200")
+    r = subprocess.run(["gcc", "-std=c99", "-Wall", "-Werror", f"-I{root}/include", str(src), "-o",
+                        str(tmp_path / "t"), f"-L{lib}", "-lttsvd_cu", f"-Wl,-rpath,{lib}"],
+                       capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    assert subprocess.run([str(tmp_path / "t")]).returncode == 0
