@@ -204,7 +204,7 @@ class Oracle:
         steps = (Step * max(d - 1, 1))()
         total = int(np.prod(dims))
         cap = max(1, min(total, 1 << 22))
-        sig_cap = sum(int(min(total // x, x)) for x in dims) + 16
+        sig_cap = 1 << 20
         while True:
             cores = np.zeros(cap)
             if self.kind == "restated":

@@ -59,7 +59,7 @@ struct ttsvd_cu_ctx {
     int64_t launches = 0;
     bool timing = false;
     // grow-only device workspaces
-    DevBuf ws_R, ws_R2, ws_A, ws_V, ws_sigma, ws_flags, ws_work[2], ws_X, ws_send, ws_recv;
+    DevBuf ws_R, ws_R2, ws_A, ws_V, ws_Vacc, ws_U, ws_sigma, ws_flags, ws_work[2], ws_X, ws_send, ws_recv;
     DevBuf host_stage;  // pinned
     cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
 };
@@ -169,7 +169,7 @@ int merge_tree(ttsvd_cu_ctx* ctx, double* parts, int64_t count, int m, double* R
     while (count > 1) {
         const int64_t next = (count + 1) / 2;
         double* dst = (next == 1) ? R_final : bufs[flip];
-        TsqrArgs a{src, count, (int64_t)m, dst, m, p.bt, p.ldb, 1, p.r_in_smem};
+        TsqrArgs a{src, count, (int64_t)m, dst, m, p.bt, p.ldb, 1, p.r_in_smem, nullptr};
         TT_TRY(launch_tsqr_kernel(ctx, a, (int)next, p.smem));
         src = dst;
         count = next;
@@ -187,7 +187,7 @@ int tsqr_device(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t ld
     G = std::min<int64_t>(G, 2 * (int64_t)ctx->num_sms);
     TT_TRY(ensure(ctx->ws_R, (size_t)G * m * m * 8));
     double* parts = as<double>(ctx->ws_R);
-    TsqrArgs a{X, n, ld, G == 1 ? R : parts, m, p.bt, p.ldb, 0, p.r_in_smem};
+    TsqrArgs a{X, n, ld, G == 1 ? R : parts, m, p.bt, p.ldb, 0, p.r_in_smem, nullptr};
     TT_TRY(launch_tsqr_kernel(ctx, a, (int)G, p.smem));
     if (G == 1) return TTSVD_OK;
     return merge_tree(ctx, parts, G, m, R);
@@ -212,7 +212,7 @@ int jacobi_device(ttsvd_cu_ctx* ctx, double* A, int n, int m, double* Vacc) {
     TT_CUDA(cudaMemsetAsync(flags, 0, 64 * sizeof(int), ctx->stream));
     JacobiArgs a{A, Vacc, n, m, flags, flags + 40, 30};
     const size_t smem = ((size_t)n * m + (Vacc ? (size_t)m * m : 0)) * 8;
-    if (smem <= 200 * 1024) {
+    if (smem <= 220 * 1024) {
         static bool attr = false;
         if (!attr) {
             TT_CUDA(cudaFuncSetAttribute(jacobi_smem_kernel<kJacobiSmemThreads>,
@@ -249,23 +249,35 @@ int finalize_device(ttsvd_cu_ctx* ctx, const double* A, int n, int m, const doub
     return check_launch(ctx, "jacobi_finalize_kernel");
 }
 
-// Right singular vectors of a work matrix given as the columns to
-// orthogonalise: A_src (n x m, ld) is copied/transposed into the workspace
-// first.  Output: sigma[m] and Vout (n x m, ld n) = normalised columns.
-int svd_columns(ttsvd_cu_ctx* ctx, const double* src, int64_t src_rows, int64_t src_cols, int64_t src_ld,
-                bool transpose, double* sigma, double* Vout, int* sweeps) {
-    const int64_t n = transpose ? src_cols : src_rows;
-    const int64_t m = transpose ? src_rows : src_cols;
+// sigma and right singular vectors of a work matrix.
+//   tall (small_svd of the TSQR factor, tt_svd.hpp:80-90): one-sided Jacobi on
+//     the columns of R with the rotations accumulated into V — the
+//     reference's algorithm, so V is orthonormal to working precision even
+//     for numerically zero sigma;
+//   wide (tt_svd.hpp:91-103): Jacobi on the columns of W^T, V := the
+//     normalised columns (the reference's U of jacobi_svd(W^T)) with its
+//     deterministic completion.
+// src is (src_rows x src_cols, ld); sigma gets nsig values, Vout is
+// (cols x nsig, ld cols).
+int svd_work(ttsvd_cu_ctx* ctx, const double* src, int64_t src_rows, int64_t src_cols, int64_t src_ld, bool wide,
+             double* sigma, double* Vout, int* sweeps) {
+    const int64_t n = wide ? src_cols : src_rows;   // column length of A
+    const int64_t m = wide ? src_rows : src_cols;   // columns of A
     TT_TRY(ensure(ctx->ws_A, (size_t)n * m * 8));
     double* A = as<double>(ctx->ws_A);
-    if (transpose) {
+    if (wide) {
         TT_TRY(transpose_device(ctx, src, src_rows, src_cols, src_ld, A));
-    } else {
-        TT_CUDA(cudaMemcpy2DAsync(A, n * 8, src, src_ld * 8, n * 8, m, cudaMemcpyDeviceToDevice, ctx->stream));
+        TT_TRY(jacobi_device(ctx, A, (int)n, (int)m, nullptr));
+        TT_TRY(jacobi_status(ctx, sweeps));
+        return finalize_device(ctx, A, (int)n, (int)m, nullptr, sigma, Vout, nullptr);
     }
-    TT_TRY(jacobi_device(ctx, A, (int)n, (int)m, nullptr));
+    TT_CUDA(cudaMemcpy2DAsync(A, n * 8, src, src_ld * 8, n * 8, m, cudaMemcpyDeviceToDevice, ctx->stream));
+    TT_TRY(ensure(ctx->ws_Vacc, (size_t)m * m * 8));
+    TT_TRY(ensure(ctx->ws_U, (size_t)n * m * 8));
+    double* Vacc = as<double>(ctx->ws_Vacc);
+    TT_TRY(jacobi_device(ctx, A, (int)n, (int)m, Vacc));
     TT_TRY(jacobi_status(ctx, sweeps));
-    return finalize_device(ctx, A, (int)n, (int)m, nullptr, sigma, Vout, nullptr);
+    return finalize_device(ctx, A, (int)n, (int)m, Vacc, sigma, as<double>(ctx->ws_U), Vout);
 }
 
 // ---------------------------------------------------------------- K_TSMM ----
@@ -397,13 +409,11 @@ int run_chain(ttsvd_cu_ctx* ctx, WorkView cur, const std::vector<int64_t>& dims,
             double* R = as<double>(ctx->ws_X);
             TT_TRY(tsqr_device(ctx, cur.data, cur.rows, (int)m, cur.ld, R));
             tm.mark(1);
-            // one-sided Jacobi on R^T: its orthogonalised columns are R's right
-            // singular vectors scaled by sigma (no rotation accumulation)
-            TT_TRY(svd_columns(ctx, R, m, m, m, true, d_sigma, d_V, &sweeps));
+            TT_TRY(svd_work(ctx, R, m, m, m, false, d_sigma, d_V, &sweeps));
         } else {
             tm.mark(1);
             // wide step (tt_svd.hpp:91-103): Jacobi on W^T, V := its U
-            TT_TRY(svd_columns(ctx, cur.data, cur.rows, cur.cols, cur.ld, true, d_sigma, d_V, &sweeps));
+            TT_TRY(svd_work(ctx, cur.data, cur.rows, cur.cols, cur.ld, true, d_sigma, d_V, &sweeps));
         }
         tm.mark(2);
         sig.resize(nsig);
@@ -507,7 +517,7 @@ int ttsvd_cu_ctx_destroy(ttsvd_cu_ctx* ctx) {
     if (!ctx) return TTSVD_OK;
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
-    for (DevBuf* b : {&ctx->ws_R, &ctx->ws_R2, &ctx->ws_A, &ctx->ws_V, &ctx->ws_sigma, &ctx->ws_flags, &ctx->ws_work[0],
+    for (DevBuf* b : {&ctx->ws_R, &ctx->ws_R2, &ctx->ws_A, &ctx->ws_V, &ctx->ws_Vacc, &ctx->ws_U, &ctx->ws_sigma, &ctx->ws_flags, &ctx->ws_work[0],
                       &ctx->ws_work[1], &ctx->ws_X, &ctx->ws_send, &ctx->ws_recv})
         if (b->p) cudaFree(b->p);
     if (ctx->host_stage.p) cudaFreeHost(ctx->host_stage.p);
@@ -552,17 +562,15 @@ int ttsvd_cu_reduce_block(ttsvd_cu_ctx* ctx, const double* M, int64_t rows, int6
     if (r_m != m) return fail(TTSVD_ERR_DIMENSION_MISMATCH, "reduce_block: R.m != M.cols");
     if (m < 1 || rows < 0 || !R_in || !R_out || (rows > 0 && (!M || ldm < rows)))
         return fail(TTSVD_ERR_INVALID, "reduce_block: bad arguments");
-    // stage [R_in, M] as two parts of a 2-part merge (M as an m-row block when
-    // rows <= m, else through the sweep path with R_in folded in afterwards)
+    // one job: the running R starts at R_in and the rows of M are folded in
+    // (tsqr.hpp:208-224 is a single reduce_into as well)
     if (rows == 0) {
         TT_CUDA(cudaMemcpyAsync(R_out, R_in, (size_t)m * m * 8, cudaMemcpyDeviceToDevice, ctx->stream));
         return TTSVD_OK;
     }
-    TT_TRY(ensure(ctx->ws_send, (size_t)2 * m * m * 8));
-    double* parts = as<double>(ctx->ws_send);
-    TT_CUDA(cudaMemcpyAsync(parts, R_in, (size_t)m * m * 8, cudaMemcpyDeviceToDevice, ctx->stream));
-    TT_TRY(tsqr_device(ctx, M, rows, (int)m, ldm, parts + m * m));
-    return merge_tree(ctx, parts, 2, (int)m, R_out);
+    TsqrPlan p = tsqr_plan((int)m);
+    TsqrArgs a{M, rows, ldm, R_out, (int)m, p.bt, p.ldb, 0, p.r_in_smem, R_in};
+    return launch_tsqr_kernel(ctx, a, 1, p.smem);
 }
 
 int ttsvd_cu_combine_factors(ttsvd_cu_ctx* ctx, const double* parts, int64_t P, int64_t m, double* R) {
@@ -580,7 +588,7 @@ int ttsvd_cu_small_svd(ttsvd_cu_ctx* ctx, const double* R, int64_t m, double* si
     if (m > 4096) return fail(TTSVD_ERR_DIMENSION_MISMATCH, "small_svd: m exceeds 4096");
     if (m < 1 || !R || !sigma || !V) return fail(TTSVD_ERR_INVALID, "small_svd: bad arguments");
     int sweeps = 0;
-    TT_TRY(svd_columns(ctx, R, m, m, m, true, sigma, V, &sweeps));
+    TT_TRY(svd_work(ctx, R, m, m, m, false, sigma, V, &sweeps));
     TT_CUDA(cudaStreamSynchronize(ctx->stream));
     return TTSVD_OK;
 }
@@ -755,7 +763,7 @@ int ttsvd_cu_tt_svd_distributed(ttsvd_cu_ctx* ctx, const double* const* slabs, i
         double* d_sigma = as<double>(ctx->ws_sigma);
         double* d_V = as<double>(ctx->ws_V);
         int sweeps = 0;
-        if ((rc = svd_columns(ctx, R, m, m, m, true, d_sigma, d_V, &sweeps)) != TTSVD_OK) break;
+        if ((rc = svd_work(ctx, R, m, m, m, false, d_sigma, d_V, &sweeps)) != TTSVD_OK) break;
         sig.resize(m);
         if ((rc = d2h(ctx, sig.data(), d_sigma, m)) != TTSVD_OK) break;
         const int64_t global_rows = cur[0].rows * P_total;
@@ -776,7 +784,7 @@ int ttsvd_cu_tt_svd_distributed(ttsvd_cu_ctx* ctx, const double* const* slabs, i
         st.nsig = nsig;
         st.rank = rnew;
         tt->steps.push_back(st);
-        tt->sigmas.push_back(sig);
+        tt->sigmas.emplace_back(sig.begin(), sig.begin() + nsig);
         for (int64_t p = 0; p < n_slabs && rc == TTSVD_OK; ++p) {
             const int64_t out_rows = i >= 1 ? cur[p].rows / ldims[i - 1] : 1;
             const int64_t out_cols = i >= 1 ? ldims[i - 1] * rnew : rnew;

@@ -67,7 +67,8 @@ __global__ void gen_uniform_kernel(uint64_t seed, int64_t total, int64_t rows, i
 // the tile's column j (R's rows above j are final, rows below are zero), the
 // reference's eps_fp trick (tsqr.hpp:120-142) keeps it branch-free:
 //     t = eps + ||u||^2, alpha = -sign(u0) sqrt(t + eps), t -= alpha u0,
-//     beta = 1/sqrt(t), v = beta (u - alpha e1), ||v||^2 = 2.
+//     beta = 1/sqrt(t), v = beta (u - alpha e1), ||v||^2 = 2;
+// a zero block column under a nonzero pivot leaves R's row untouched (H = I).
 // The trailing columns are updated by warps (one column per warp at a time,
 // lanes over rows, shuffle reduction).  Two modes:
 //   mode 0 (sweep):  job g = rows [g*n/G, (g+1)*n/G) of X, R starts at 0;
@@ -84,6 +85,7 @@ struct TsqrArgs {
     int ldb;           // tile leading dimension in shared memory
     int mode;
     int r_in_smem;
+    const double* R_init0;  // mode 0 only, grid 1: start from this R (reduce_block)
 };
 
 template <int NT>
@@ -105,6 +107,7 @@ __global__ void __launch_bounds__(NT) tsqr_tile_kernel(TsqrArgs a) {
         row1 = row0 + base + (job < rem ? 1 : 0);
         X = a.X;
         ld = a.ld;
+        R_init = a.R_init0;
     } else {
         const int64_t count = a.n;
         R_init = a.X + (2 * job) * (int64_t)m * m;
@@ -146,14 +149,24 @@ __global__ void __launch_bounds__(NT) tsqr_tile_kernel(TsqrArgs a) {
                 double tot = 0.0;
                 for (int w = 0; w < NW; ++w) tot += red[w];
                 const double u0 = R[j * m + j];
-                double t = eps + (u0 * u0 + tot);
-                double alpha = sqrt(t + eps);
-                alpha = (u0 > 0.0) ? -alpha : alpha;
-                t -= alpha * u0;
-                const double beta = 1.0 / sqrt(t);
-                red[NW + 0] = alpha;
-                red[NW + 1] = beta;
-                red[NW + 2] = (u0 - alpha) * beta;
+                if (tot == 0.0 && u0 != 0.0) {
+                    // nothing below a nonzero pivot: H = I (LAPACK dlarfg
+                    // convention), R(j,:) stays bitwise as it is.  An all-zero
+                    // u still takes the eps_fp path below, which yields the
+                    // reference's alpha = sqrt(2 DBL_MIN) (tsqr.hpp:120-126).
+                    red[NW + 0] = u0;
+                    red[NW + 1] = 0.0;
+                    red[NW + 2] = 0.0;
+                } else {
+                    double t = eps + (u0 * u0 + tot);
+                    double alpha = sqrt(t + eps);
+                    alpha = (u0 > 0.0) ? -alpha : alpha;
+                    t -= alpha * u0;
+                    const double beta = 1.0 / sqrt(t);
+                    red[NW + 0] = alpha;
+                    red[NW + 1] = beta;
+                    red[NW + 2] = (u0 - alpha) * beta;
+                }
             }
             __syncthreads();
             const double alpha = red[NW + 0], beta = red[NW + 1], v0 = red[NW + 2];
@@ -216,13 +229,47 @@ __device__ __forceinline__ void circle_pair(int r, int i, int mp, int& p, int& q
     }
 }
 
+// One rotation of columns (ap, aq) of length n (and optionally vp, vq of
+// length m).  Columns are pulled into registers in CH-wide chunks so that all
+// loads of a chunk are in flight together (the pair is latency-bound).
+template <int CH>
+__device__ __forceinline__ void rotate_cols(double* x, double* y, int n, int lane, double c, double s) {
+    for (int base = 0; base < n; base += CH * kWarp) {
+        double a[CH], b[CH];
+#pragma unroll
+        for (int t = 0; t < CH; ++t) {
+            const int i = base + t * kWarp + lane;
+            a[t] = i < n ? x[i] : 0.0;
+            b[t] = i < n ? y[i] : 0.0;
+        }
+#pragma unroll
+        for (int t = 0; t < CH; ++t) {
+            const int i = base + t * kWarp + lane;
+            if (i < n) {
+                x[i] = c * a[t] - s * b[t];
+                y[i] = s * a[t] + c * b[t];
+            }
+        }
+    }
+}
+
 __device__ __forceinline__ bool jacobi_pair(double* ap, double* aq, int n, double* vp, double* vq, int m, int lane) {
+    constexpr int CH = 8;
     double al = 0.0, be = 0.0, ga = 0.0;
-    for (int i = lane; i < n; i += kWarp) {
-        const double x = ap[i], y = aq[i];
-        al += x * x;
-        be += y * y;
-        ga += x * y;
+    for (int base = 0; base < n; base += CH * kWarp) {
+        double a[CH], b[CH];
+#pragma unroll
+        for (int t = 0; t < CH; ++t) {
+            const int i = base + t * kWarp + lane;
+            a[t] = i < n ? ap[i] : 0.0;
+            b[t] = i < n ? aq[i] : 0.0;
+        }
+#pragma unroll
+        for (int t = 0; t < CH; ++t) {
+            al += a[t] * a[t];
+            be += b[t] * b[t];
+            ga += a[t] * b[t];
+        }
     }
     al = warp_sum(al);
     be = warp_sum(be);
@@ -233,18 +280,8 @@ __device__ __forceinline__ bool jacobi_pair(double* ap, double* aq, int n, doubl
     const double t = ((zeta >= 0.0) ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
     const double c = 1.0 / sqrt(1.0 + t * t);
     const double s = c * t;
-    for (int i = lane; i < n; i += kWarp) {
-        const double x = ap[i], y = aq[i];
-        ap[i] = c * x - s * y;
-        aq[i] = s * x + c * y;
-    }
-    if (vp) {
-        for (int i = lane; i < m; i += kWarp) {
-            const double x = vp[i], y = vq[i];
-            vp[i] = c * x - s * y;
-            vq[i] = s * x + c * y;
-        }
-    }
+    rotate_cols<CH>(ap, aq, n, lane, c, s);
+    if (vp) rotate_cols<CH>(vp, vq, m, lane, c, s);
     return true;
 }
 
