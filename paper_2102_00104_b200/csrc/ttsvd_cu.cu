@@ -17,6 +17,7 @@
 
 #include "../../include/ttsvd_cu.h"
 #include "ttsvd_kernels.cuh"
+#include "tsqr_blk.cuh"
 
 using namespace ttsvd_b200;
 
@@ -59,7 +60,7 @@ struct ttsvd_cu_ctx {
     int64_t launches = 0;
     bool timing = false;
     // grow-only device workspaces
-    DevBuf ws_R, ws_R2, ws_A, ws_V, ws_Vacc, ws_U, ws_sigma, ws_flags, ws_work[2], ws_X, ws_send, ws_recv;
+    DevBuf ws_R, ws_R2, ws_P, ws_A, ws_V, ws_Vacc, ws_U, ws_sigma, ws_flags, ws_work[2], ws_X, ws_send, ws_recv;
     DevBuf host_stage;  // pinned
     cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
 };
@@ -154,12 +155,65 @@ int launch_tsqr_kernel(ttsvd_cu_ctx* ctx, const TsqrArgs& a, int grid, size_t sm
     return check_launch(ctx, "tsqr_tile_kernel");
 }
 
-// Fixed index-ordered merge tree over `count` parts (each m*m) in buf_a; the
+// ---- blocked DMMA path (m > 32) ----
+constexpr int kSmallM = 32;
+
+int launch_blk(ttsvd_cu_ctx* ctx, const BlkArgs& a, int grid) {
+    static bool attr_set = false;
+    if (!attr_set) {
+        TT_CUDA(cudaFuncSetAttribute(tsqr_blk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit));
+        attr_set = true;
+    }
+    tsqr_blk_kernel<<<grid, kBlkThreads, blk_smem_bytes(a.M), ctx->stream>>>(a);
+    return check_launch(ctx, "tsqr_blk_kernel");
+}
+
+int copy_leading(ttsvd_cu_ctx* ctx, const double* Rws, int M, int m, double* R) {
+    copy_leading_kernel<<<std::max(1, std::min(1024, (m * m + 255) / 256)), 256, 0, ctx->stream>>>(Rws, M, m, R);
+    return check_launch(ctx, "copy_leading_kernel");
+}
+
+// merge tree over `count` M x M workspace parts in `parts` (overwritten);
+// the final M x M factor lands in `out`.
+int merge_tree_blk(ttsvd_cu_ctx* ctx, double* parts, int64_t count, int m, int M, double* out) {
+    if (count == 1) {
+        TT_CUDA(cudaMemcpyAsync(out, parts, (size_t)M * M * 8, cudaMemcpyDeviceToDevice, ctx->stream));
+        return TTSVD_OK;
+    }
+    TT_TRY(ensure(ctx->ws_R2, (size_t)((count + 1) / 2) * M * M * 8));
+    double* src = parts;
+    double* bufs[2] = {as<double>(ctx->ws_R2), parts};
+    int flip = 0;
+    while (count > 1) {
+        const int64_t next = (count + 1) / 2;
+        double* dst = (next == 1) ? out : bufs[flip];
+        BlkArgs a{src, count, (int64_t)M, dst, nullptr, m, M, 1};
+        TT_TRY(launch_blk(ctx, a, (int)next));
+        src = dst;
+        count = next;
+        flip ^= 1;
+    }
+    return TTSVD_OK;
+}
+
+// Fixed index-ordered merge tree over `count` parts (each m x m, ld m); the
 // result lands in R_final.  Level l pairs (2i, 2i+1); an odd tail is carried.
 int merge_tree(ttsvd_cu_ctx* ctx, double* parts, int64_t count, int m, double* R_final) {
     if (count == 1) {
         TT_CUDA(cudaMemcpyAsync(R_final, parts, (size_t)m * m * 8, cudaMemcpyDeviceToDevice, ctx->stream));
         return TTSVD_OK;
+    }
+    if (m > kSmallM) {
+        const int M = (m + 31) / 32 * 32;
+        TT_TRY(ensure(ctx->ws_P, (size_t)(count + 1) * M * M * 8));
+        double* P = as<double>(ctx->ws_P);
+        TT_CUDA(cudaMemsetAsync(P, 0, (size_t)count * M * M * 8, ctx->stream));
+        for (int64_t q = 0; q < count; ++q)
+            TT_CUDA(cudaMemcpy2DAsync(P + q * M * M, (size_t)M * 8, parts + q * m * m, (size_t)m * 8, (size_t)m * 8, m,
+                                      cudaMemcpyDeviceToDevice, ctx->stream));
+        double* out = P + count * M * M;
+        TT_TRY(merge_tree_blk(ctx, P, count, m, M, out));
+        return copy_leading(ctx, out, M, m, R_final);
     }
     TT_TRY(ensure(ctx->ws_R2, (size_t)((count + 1) / 2) * m * m * 8));
     TsqrPlan p = tsqr_plan(m);
@@ -180,14 +234,41 @@ int merge_tree(ttsvd_cu_ctx* ctx, double* parts, int64_t count, int m, double* R
 
 // R (m x m) of X (n x m, ld) — n may be smaller than m (the structured kernel
 // does not need n >= m; gram_triangular's square padding is implicit).
-int tsqr_device(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t ld, double* R) {
+// R_init (m x m) optionally seeds a single job (reduce_block).
+int tsqr_device(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t ld, double* R,
+                const double* R_init = nullptr) {
+    if (m > kSmallM) {
+        const int M = (m + 31) / 32 * 32;
+        const int per_sm = blk_smem_bytes(M) * 2 <= (size_t)kSmemLimit ? 2 : 1;
+        int64_t G = std::max<int64_t>(1, n / (4 * (int64_t)M));
+        G = std::min<int64_t>(G, (int64_t)per_sm * ctx->num_sms);
+        if (R_init) G = 1;
+        TT_TRY(ensure(ctx->ws_R, (size_t)(G + 1) * M * M * 8));
+        double* parts = as<double>(ctx->ws_R);
+        double* Rinit_ws = nullptr;
+        if (R_init) {
+            Rinit_ws = parts + M * M;
+            TT_CUDA(cudaMemsetAsync(Rinit_ws, 0, (size_t)M * M * 8, ctx->stream));
+            TT_CUDA(cudaMemcpy2DAsync(Rinit_ws, (size_t)M * 8, R_init, (size_t)m * 8, (size_t)m * 8, m,
+                                      cudaMemcpyDeviceToDevice, ctx->stream));
+        }
+        BlkArgs a{X, n, ld, parts, Rinit_ws, m, M, 0};
+        TT_TRY(launch_blk(ctx, a, (int)G));
+        if (G > 1) {
+            TT_TRY(ensure(ctx->ws_P, (size_t)M * M * 8));
+            TT_TRY(merge_tree_blk(ctx, parts, G, m, M, as<double>(ctx->ws_P)));
+            return copy_leading(ctx, as<double>(ctx->ws_P), M, m, R);
+        }
+        return copy_leading(ctx, parts, M, m, R);
+    }
     TsqrPlan p = tsqr_plan(m);
     const int64_t min_rows = std::max<int64_t>(p.bt, 8 * (int64_t)m);
     int64_t G = std::max<int64_t>(1, n / min_rows);
     G = std::min<int64_t>(G, 2 * (int64_t)ctx->num_sms);
+    if (R_init) G = 1;
     TT_TRY(ensure(ctx->ws_R, (size_t)G * m * m * 8));
     double* parts = as<double>(ctx->ws_R);
-    TsqrArgs a{X, n, ld, G == 1 ? R : parts, m, p.bt, p.ldb, 0, p.r_in_smem, nullptr};
+    TsqrArgs a{X, n, ld, G == 1 ? R : parts, m, p.bt, p.ldb, 0, p.r_in_smem, R_init};
     TT_TRY(launch_tsqr_kernel(ctx, a, (int)G, p.smem));
     if (G == 1) return TTSVD_OK;
     return merge_tree(ctx, parts, G, m, R);
@@ -517,7 +598,7 @@ int ttsvd_cu_ctx_destroy(ttsvd_cu_ctx* ctx) {
     if (!ctx) return TTSVD_OK;
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
-    for (DevBuf* b : {&ctx->ws_R, &ctx->ws_R2, &ctx->ws_A, &ctx->ws_V, &ctx->ws_Vacc, &ctx->ws_U, &ctx->ws_sigma, &ctx->ws_flags, &ctx->ws_work[0],
+    for (DevBuf* b : {&ctx->ws_R, &ctx->ws_R2, &ctx->ws_P, &ctx->ws_A, &ctx->ws_V, &ctx->ws_Vacc, &ctx->ws_U, &ctx->ws_sigma, &ctx->ws_flags, &ctx->ws_work[0],
                       &ctx->ws_work[1], &ctx->ws_X, &ctx->ws_send, &ctx->ws_recv})
         if (b->p) cudaFree(b->p);
     if (ctx->host_stage.p) cudaFreeHost(ctx->host_stage.p);
@@ -568,9 +649,7 @@ int ttsvd_cu_reduce_block(ttsvd_cu_ctx* ctx, const double* M, int64_t rows, int6
         TT_CUDA(cudaMemcpyAsync(R_out, R_in, (size_t)m * m * 8, cudaMemcpyDeviceToDevice, ctx->stream));
         return TTSVD_OK;
     }
-    TsqrPlan p = tsqr_plan((int)m);
-    TsqrArgs a{M, rows, ldm, R_out, (int)m, p.bt, p.ldb, 0, p.r_in_smem, R_in};
-    return launch_tsqr_kernel(ctx, a, 1, p.smem);
+    return tsqr_device(ctx, M, rows, (int)m, ldm, R_out, R_in);
 }
 
 int ttsvd_cu_combine_factors(ttsvd_cu_ctx* ctx, const double* parts, int64_t P, int64_t m, double* R) {
