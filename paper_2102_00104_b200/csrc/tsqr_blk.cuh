@@ -15,8 +15,11 @@
 //   3. trailing update of every 8-column group c (all warps, DMMA):
 //        W = R(p, c) + V^T B(:, c);  W = T^T W;  R(p, c) -= W;  B(:, c) -= V W.
 //
-// R (M x M, ld M, M = m rounded up to 32) lives in the job's global workspace
-// (L2 resident); the tile and V live in shared memory.  In merge mode the
+// R lives in the job's global workspace in a packed panel-major layout (row
+// panel p = 32 rows x (M - 32p) columns, column-major, ld 32): only the upper
+// triangle is stored, every DMMA fragment of R is a contiguous 2 KiB run, and
+// 296 CTAs x M(M+32)/2 doubles stay L2 resident at M = 256.  The tile and V
+// live in shared memory.  In merge mode the
 // incoming part is upper triangular, so panels left of the tile's first row
 // are structurally zero and skipped.
 #pragma once
@@ -32,11 +35,11 @@ constexpr int kBlkThreads = 128;
 constexpr int kTld = 33;        // smem ld of S and T
 
 struct BlkArgs {
-    const double* X;        // mode 0: matrix (n x m, ld); mode 1: parts (count x M x M)
+    const double* X;        // mode 0: matrix (n x m, ld); mode 1: parts (count x blk_rsize(M))
     int64_t n;              // mode 0: rows; mode 1: number of parts at this level
     int64_t ld;
-    double* Rws;            // per-job running R / output (M x M, ld M)
-    const double* R_init0;  // mode 0 only: starting R (M x M, ld M) or nullptr
+    double* Rws;            // per-job running R / output (packed panel layout, blk_rsize(M))
+    const double* R_init0;  // mode 0 only: starting R (packed panel layout) or nullptr
     int m;                  // logical columns
     int M;                  // padded columns (multiple of 32)
     int mode;
@@ -47,6 +50,12 @@ __device__ __forceinline__ void dmma884(double (&d)[2], double a, double b) {
                  : "+d"(d[0]), "+d"(d[1])
                  : "d"(a), "d"(b));
 }
+
+// offset of row panel p in the packed layout, and the packed size
+__host__ __device__ __forceinline__ int64_t blk_roff(int p, int M) {
+    return 32 * ((int64_t)p * M - 32 * (int64_t)p * (p - 1) / 2);
+}
+__host__ __device__ __forceinline__ int64_t blk_rsize(int M) { return blk_roff(M / 32, M); }
 
 inline size_t blk_smem_bytes(int M) {
     return ((size_t)M * kBlkLdb + 3 * 32 * kTld + 64 + (kBlkThreads / 32) * 32 * 9) * sizeof(double);
@@ -68,7 +77,8 @@ __global__ void __launch_bounds__(kBlkThreads, 2) tsqr_blk_kernel(BlkArgs a) {
     const double* X;
     int64_t row0, row1, ld;
     const double* R_init = nullptr;
-    double* R = a.Rws + job * (int64_t)M * M;
+    const int64_t RS = blk_rsize(M);
+    double* R = a.Rws + job * RS;
     if (a.mode == 0) {
         const int64_t G = gridDim.x;
         const int64_t base = a.n / G, rem = a.n % G;
@@ -79,9 +89,9 @@ __global__ void __launch_bounds__(kBlkThreads, 2) tsqr_blk_kernel(BlkArgs a) {
         R_init = a.R_init0;
     } else {
         const int64_t count = a.n;
-        R_init = a.X + (2 * job) * (int64_t)M * M;
+        R_init = a.X + (2 * job) * RS;
         if (2 * job + 1 < count) {
-            X = a.X + (2 * job + 1) * (int64_t)M * M;
+            X = a.X + (2 * job + 1) * RS;
             row0 = 0;
             row1 = M;
         } else {
@@ -90,15 +100,25 @@ __global__ void __launch_bounds__(kBlkThreads, 2) tsqr_blk_kernel(BlkArgs a) {
         }
         ld = M;
     }
-    for (int64_t e = tid; e < (int64_t)M * M; e += kBlkThreads) R[e] = R_init ? R_init[e] : 0.0;
+    for (int64_t e = tid; e < RS; e += kBlkThreads) R[e] = R_init ? R_init[e] : 0.0;
     __syncthreads();
 
     const int npan = M / 32;
     for (int64_t r0 = row0; r0 < row1; r0 += kBlkRows) {
         const int rows = (int)((row1 - r0) < kBlkRows ? (row1 - r0) : kBlkRows);
-        for (int e = tid; e < M * kBlkRows; e += kBlkThreads) {
-            const int c = e >> 5, i = e & 31;
-            Bt[c * kBlkLdb + i] = (i < rows && c < m) ? X[(int64_t)c * ld + r0 + i] : 0.0;
+        if (a.mode == 0) {
+            for (int e = tid; e < M * kBlkRows; e += kBlkThreads) {
+                const int c = e >> 5, i = e & 31;
+                Bt[c * kBlkLdb + i] = (i < rows && c < m) ? X[(int64_t)c * ld + r0 + i] : 0.0;
+            }
+        } else {
+            // row panel t of a packed triangular part: columns < 32t are zero
+            const int t = (int)(r0 / 32);
+            const double* src = X + blk_roff(t, M) - (int64_t)32 * 32 * t;
+            for (int e = tid; e < M * kBlkRows; e += kBlkThreads) {
+                const int c = e >> 5, i = e & 31;
+                Bt[c * kBlkLdb + i] = (c >= 32 * t) ? src[e] : 0.0;
+            }
         }
         __syncthreads();
         const int p_first = a.mode == 1 ? (int)(r0 / 32) : 0;  // structural zeros of a triangular part
@@ -113,7 +133,8 @@ __global__ void __launch_bounds__(kBlkThreads, 2) tsqr_blk_kernel(BlkArgs a) {
                 double x[32];
 #pragma unroll
                 for (int r = 0; r < 32; ++r) x[r] = Bt[(c0 + lane) * kBlkLdb + r];
-                for (int i = 0; i < 32; ++i) Rp[i * kTld + lane] = R[(int64_t)(c0 + lane) * M + c0 + i];
+                const double* Rpan = R + blk_roff(p, M);  // row panel p, column c0 + k at k*32
+                for (int e = lane; e < 32 * 32; e += 32) Rp[(e & 31) * kTld + (e >> 5)] = Rpan[e];
                 __syncwarp();
                 for (int jj = 0; jj < 32; ++jj) {
                     // pivot column -> shared memory, read back as broadcasts
@@ -173,44 +194,74 @@ __global__ void __launch_bounds__(kBlkThreads, 2) tsqr_blk_kernel(BlkArgs a) {
                 }
 #pragma unroll
                 for (int r = 0; r < 32; ++r) Bt[(c0 + lane) * kBlkLdb + r] = x[r];
-                for (int i = 0; i < 32; ++i) R[(int64_t)(c0 + lane) * M + c0 + i] = Rp[i * kTld + lane];
+                for (int e = lane; e < 32 * 32; e += 32) R[blk_roff(p, M) + e] = Rp[(e & 31) * kTld + (e >> 5)];
             }
             __syncthreads();
             if (c0 + 32 >= M) continue;  // no trailing columns: T is not needed
-            // ---- 2. S = strict upper part of V^T V, then T = (diag(1/tau) + S)^{-1} ----
-            for (int e = tid; e < 32 * 32; e += kBlkThreads) {
-                const int i = e >> 5, j = e & 31;
-                if (i < j) {
-                    const double* vi = Bt + (c0 + i) * kBlkLdb;
-                    const double* vj = Bt + (c0 + j) * kBlkLdb;
-                    double s = 0.0;
-#pragma unroll 8
-                    for (int r = 0; r < 32; ++r) s += vi[r] * vj[r];
-                    Sm[i * kTld + j] = s;
+            // ---- 2. S = V^T V (DMMA, warp w -> reflector columns 8w..8w+7 of 32),
+            //         then T = (diag(1/tau) + striu(S))^{-1} blockwise ----
+            const int lr = lane >> 2, lc = lane & 3;
+            for (int nt = warp; nt < 4; nt += kBlkThreads / 32) {
+                double sacc[4][2];
+#pragma unroll
+                for (int mt = 0; mt < 4; ++mt) sacc[mt][0] = sacc[mt][1] = 0.0;
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk) {
+                    const double b = Bt[(c0 + 8 * nt + lr) * kBlkLdb + 4 * kk + lc];
+#pragma unroll
+                    for (int mt = 0; mt < 4; ++mt) dmma884(sacc[mt], Bt[(c0 + 8 * mt + lr) * kBlkLdb + 4 * kk + lc], b);
                 }
+#pragma unroll
+                for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+                    for (int e = 0; e < 2; ++e) Sm[(8 * mt + lr) * kTld + 8 * nt + 2 * lc + e] = sacc[mt][e];
             }
             __syncthreads();
+            // T = U^{-1}, U = diag(1/tau) + striu(S), by 8x8 diagonal blocks
+            // (lane 8b+j back-substitutes column j of block b) and two levels
+            // of the block identity [[A, B], [0, C]]^{-1} = [[A^-1, -A^-1 B C^-1], [0, C^-1]].
             if (warp == 0) {
-                const int j = lane;  // lane j back-substitutes column j of T
-                for (int i = 31; i > j; --i) Tm[i * kTld + j] = 0.0;
-                Tm[j * kTld + j] = tau[j];
+                const int b0 = 8 * (lane >> 3), j = lane & 7;
+                for (int i = 0; i < 32; ++i) Tm[i * kTld + b0 + j] = 0.0;
+                Tm[(b0 + j) * kTld + b0 + j] = tau[b0 + j];
                 for (int i = j - 1; i >= 0; --i) {
                     double acc = 0.0;
-                    for (int l = i + 1; l <= j; ++l) acc += Sm[i * kTld + l] * Tm[l * kTld + j];
-                    Tm[i * kTld + j] = -tau[i] * acc;
+                    for (int l = i + 1; l <= j; ++l) acc += Sm[(b0 + i) * kTld + b0 + l] * Tm[(b0 + l) * kTld + b0 + j];
+                    Tm[(b0 + i) * kTld + b0 + j] = -tau[b0 + i] * acc;
                 }
             }
             __syncthreads();
+            for (int lev = 8; lev <= 16; lev *= 2) {
+                // blocks [o, o+lev) x [o+lev, o+2lev), o = 0 (and 16 when lev = 8)
+                double* Xs = Wsc;  // scratch (>= 16 x 16 used as lev x lev, ld 17)
+                const int nblk = 32 / (2 * lev);
+                for (int e = tid; e < nblk * lev * lev; e += kBlkThreads) {
+                    const int q = e / (lev * lev), i = (e / lev) % lev, j = e % lev;
+                    const int o = q * 2 * lev;
+                    double acc = 0.0;  // X = S[o.., o+lev..] T[o+lev.., o+lev..]
+                    for (int l = 0; l <= j; ++l) acc += Sm[(o + i) * kTld + o + lev + l] * Tm[(o + lev + l) * kTld + o + lev + j];
+                    Xs[q * 17 * 17 + i * 17 + j] = acc;
+                }
+                __syncthreads();
+                for (int e = tid; e < nblk * lev * lev; e += kBlkThreads) {
+                    const int q = e / (lev * lev), i = (e / lev) % lev, j = e % lev;
+                    const int o = q * 2 * lev;
+                    double acc = 0.0;  // T[o+i, o+lev+j] = -(T_A X)(i, j)
+                    for (int l = i; l < lev; ++l) acc += Tm[(o + i) * kTld + o + l] * Xs[q * 17 * 17 + l * 17 + j];
+                    Tm[(o + i) * kTld + o + lev + j] = -acc;
+                }
+                __syncthreads();
+            }
             // ---- 3. trailing update over 8-column groups (DMMA m8n8k4) ----
             double* Ws = Wsc + warp * 32 * 9;
-            const int lr = lane >> 2, lc = lane & 3;
+            double* Rrow = R + blk_roff(p, M);
             for (int g = c0 + 32 + 8 * warp; g < M; g += 8 * (kBlkThreads / 32)) {
                 double acc[4][2], rsav[4][2];
 #pragma unroll
                 for (int mt = 0; mt < 4; ++mt)
 #pragma unroll
                     for (int e = 0; e < 2; ++e) {
-                        rsav[mt][e] = R[(int64_t)(g + 2 * lc + e) * M + c0 + 8 * mt + lr];
+                        rsav[mt][e] = Rrow[(g + 2 * lc + e - c0) * 32 + 8 * mt + lr];
                         acc[mt][e] = rsav[mt][e];
                     }
                 // W = R(p, c) + V^T B(:, c):  A = V^T (refl x row), B = tile (row x col)
@@ -240,7 +291,7 @@ __global__ void __launch_bounds__(kBlkThreads, 2) tsqr_blk_kernel(BlkArgs a) {
                 for (int mt = 0; mt < 4; ++mt)
 #pragma unroll
                     for (int e = 0; e < 2; ++e) {
-                        R[(int64_t)(g + 2 * lc + e) * M + c0 + 8 * mt + lr] = rsav[mt][e] - w2[mt][e];
+                        Rrow[(g + 2 * lc + e - c0) * 32 + 8 * mt + lr] = rsav[mt][e] - w2[mt][e];
                         Ws[(8 * mt + lr) * 9 + 2 * lc + e] = w2[mt][e];
                     }
                 __syncwarp();
@@ -267,11 +318,26 @@ __global__ void __launch_bounds__(kBlkThreads, 2) tsqr_blk_kernel(BlkArgs a) {
     }
 }
 
-// leading m x m block of an M x M workspace factor -> R (ld m)
+// packed panel-major M x M factor -> leading m x m block, column-major ld m
 __global__ void copy_leading_kernel(const double* Rws, int M, int m, double* R) {
     for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < m * m; e += gridDim.x * blockDim.x) {
         const int j = e / m, i = e - j * m;
-        R[e] = Rws[(int64_t)j * M + i];
+        const int p = i >> 5;
+        R[e] = (i <= j) ? Rws[blk_roff(p, M) + (int64_t)(j - 32 * p) * 32 + (i & 31)] : 0.0;
+    }
+}
+
+// P parts of m x m (ld m, upper triangular) -> packed panel-major M x M parts
+__global__ void pack_parts_kernel(const double* parts, int64_t P, int m, int M, double* out) {
+    const int64_t RS = blk_rsize(M);
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < P * RS; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t q = e / RS;
+        int64_t o = e - q * RS;
+        int p = 0;
+        while (p + 1 < M / 32 && blk_roff(p + 1, M) <= o) ++p;
+        o -= blk_roff(p, M);
+        const int c = 32 * p + (int)(o >> 5), row = 32 * p + (int)(o & 31);
+        out[e] = (row < m && c < m && row <= c) ? parts[q * (int64_t)m * m + (int64_t)c * m + row] : 0.0;
     }
 }
 

@@ -173,14 +173,15 @@ int copy_leading(ttsvd_cu_ctx* ctx, const double* Rws, int M, int m, double* R) 
     return check_launch(ctx, "copy_leading_kernel");
 }
 
-// merge tree over `count` M x M workspace parts in `parts` (overwritten);
-// the final M x M factor lands in `out`.
+// merge tree over `count` packed workspace parts in `parts` (overwritten);
+// the final packed factor lands in `out`.
 int merge_tree_blk(ttsvd_cu_ctx* ctx, double* parts, int64_t count, int m, int M, double* out) {
+    const int64_t RS = blk_rsize(M);
     if (count == 1) {
-        TT_CUDA(cudaMemcpyAsync(out, parts, (size_t)M * M * 8, cudaMemcpyDeviceToDevice, ctx->stream));
+        TT_CUDA(cudaMemcpyAsync(out, parts, (size_t)RS * 8, cudaMemcpyDeviceToDevice, ctx->stream));
         return TTSVD_OK;
     }
-    TT_TRY(ensure(ctx->ws_R2, (size_t)((count + 1) / 2) * M * M * 8));
+    TT_TRY(ensure(ctx->ws_R2, (size_t)((count + 1) / 2) * RS * 8));
     double* src = parts;
     double* bufs[2] = {as<double>(ctx->ws_R2), parts};
     int flip = 0;
@@ -196,6 +197,13 @@ int merge_tree_blk(ttsvd_cu_ctx* ctx, double* parts, int64_t count, int m, int M
     return TTSVD_OK;
 }
 
+int pack_parts(ttsvd_cu_ctx* ctx, const double* parts, int64_t P, int m, int M, double* out) {
+    const int64_t total = P * blk_rsize(M);
+    pack_parts_kernel<<<(unsigned)std::min<int64_t>((total + 255) / 256, 4096), 256, 0, ctx->stream>>>(parts, P, m, M,
+                                                                                                   out);
+    return check_launch(ctx, "pack_parts_kernel");
+}
+
 // Fixed index-ordered merge tree over `count` parts (each m x m, ld m); the
 // result lands in R_final.  Level l pairs (2i, 2i+1); an odd tail is carried.
 int merge_tree(ttsvd_cu_ctx* ctx, double* parts, int64_t count, int m, double* R_final) {
@@ -205,13 +213,11 @@ int merge_tree(ttsvd_cu_ctx* ctx, double* parts, int64_t count, int m, double* R
     }
     if (m > kSmallM) {
         const int M = (m + 31) / 32 * 32;
-        TT_TRY(ensure(ctx->ws_P, (size_t)(count + 1) * M * M * 8));
+        const int64_t RS = blk_rsize(M);
+        TT_TRY(ensure(ctx->ws_P, (size_t)(count + 1) * RS * 8));
         double* P = as<double>(ctx->ws_P);
-        TT_CUDA(cudaMemsetAsync(P, 0, (size_t)count * M * M * 8, ctx->stream));
-        for (int64_t q = 0; q < count; ++q)
-            TT_CUDA(cudaMemcpy2DAsync(P + q * M * M, (size_t)M * 8, parts + q * m * m, (size_t)m * 8, (size_t)m * 8, m,
-                                      cudaMemcpyDeviceToDevice, ctx->stream));
-        double* out = P + count * M * M;
+        TT_TRY(pack_parts(ctx, parts, count, m, M, P));
+        double* out = P + count * RS;
         TT_TRY(merge_tree_blk(ctx, P, count, m, M, out));
         return copy_leading(ctx, out, M, m, R_final);
     }
@@ -239,23 +245,22 @@ int tsqr_device(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t ld
                 const double* R_init = nullptr) {
     if (m > kSmallM) {
         const int M = (m + 31) / 32 * 32;
+        const int64_t RS = blk_rsize(M);
         const int per_sm = blk_smem_bytes(M) * 2 <= (size_t)kSmemLimit ? 2 : 1;
         int64_t G = std::max<int64_t>(1, n / (4 * (int64_t)M));
         G = std::min<int64_t>(G, (int64_t)per_sm * ctx->num_sms);
         if (R_init) G = 1;
-        TT_TRY(ensure(ctx->ws_R, (size_t)(G + 1) * M * M * 8));
+        TT_TRY(ensure(ctx->ws_R, (size_t)(G + 1) * RS * 8));
         double* parts = as<double>(ctx->ws_R);
         double* Rinit_ws = nullptr;
         if (R_init) {
-            Rinit_ws = parts + M * M;
-            TT_CUDA(cudaMemsetAsync(Rinit_ws, 0, (size_t)M * M * 8, ctx->stream));
-            TT_CUDA(cudaMemcpy2DAsync(Rinit_ws, (size_t)M * 8, R_init, (size_t)m * 8, (size_t)m * 8, m,
-                                      cudaMemcpyDeviceToDevice, ctx->stream));
+            Rinit_ws = parts + RS;
+            TT_TRY(pack_parts(ctx, R_init, 1, m, M, Rinit_ws));
         }
         BlkArgs a{X, n, ld, parts, Rinit_ws, m, M, 0};
         TT_TRY(launch_blk(ctx, a, (int)G));
         if (G > 1) {
-            TT_TRY(ensure(ctx->ws_P, (size_t)M * M * 8));
+            TT_TRY(ensure(ctx->ws_P, (size_t)RS * 8));
             TT_TRY(merge_tree_blk(ctx, parts, G, m, M, as<double>(ctx->ws_P)));
             return copy_leading(ctx, as<double>(ctx->ws_P), M, m, R);
         }
