@@ -43,6 +43,7 @@ struct BlkArgs {
     int m;                  // logical columns
     int M;                  // padded columns (multiple of 32)
     int mode;
+    long long* prof;        // optional per-CTA phase cycle counters (8 per CTA), diagnostics
 };
 
 __device__ __forceinline__ void dmma884(double (&d)[2], double a, double b) {
@@ -103,6 +104,14 @@ __global__ void __launch_bounds__(kBlkThreads, 2) tsqr_blk_kernel(BlkArgs a) {
     for (int64_t e = tid; e < RS; e += kBlkThreads) R[e] = R_init ? R_init[e] : 0.0;
     __syncthreads();
 
+    long long t_prev = 0, t_acc[6] = {0, 0, 0, 0, 0, 0};
+#define TT_PROF(ph)                                  \
+    if (a.prof && tid == 0) {                        \
+        const long long t_now = clock64();           \
+        if (t_prev) t_acc[ph] += t_now - t_prev;     \
+        t_prev = t_now;                              \
+    }
+    TT_PROF(5);
     const int npan = M / 32;
     for (int64_t r0 = row0; r0 < row1; r0 += kBlkRows) {
         const int rows = (int)((row1 - r0) < kBlkRows ? (row1 - r0) : kBlkRows);
@@ -121,6 +130,7 @@ __global__ void __launch_bounds__(kBlkThreads, 2) tsqr_blk_kernel(BlkArgs a) {
             }
         }
         __syncthreads();
+        TT_PROF(0);
         const int p_first = a.mode == 1 ? (int)(r0 / 32) : 0;  // structural zeros of a triangular part
         for (int p = p_first; p < npan; ++p) {
             const int c0 = p * 32;
@@ -132,71 +142,82 @@ __global__ void __launch_bounds__(kBlkThreads, 2) tsqr_blk_kernel(BlkArgs a) {
             if (warp == 0) {
                 double x[32];
 #pragma unroll
-                for (int r = 0; r < 32; ++r) x[r] = Bt[(c0 + lane) * kBlkLdb + r];
-                const double* Rpan = R + blk_roff(p, M);  // row panel p, column c0 + k at k*32
-                for (int e = lane; e < 32 * 32; e += 32) Rp[(e & 31) * kTld + (e >> 5)] = Rpan[e];
+                for (int r = 0; r < 32; r += 2) {
+                    const double2 t = *reinterpret_cast<const double2*>(Bt + (c0 + lane) * kBlkLdb + r);
+                    x[r] = t.x;
+                    x[r + 1] = t.y;
+                }
+                {
+                    const double* Rpan = R + blk_roff(p, M);  // row panel p: column c0 + k at k*32
+                    double tmp[32];
+#pragma unroll
+                    for (int q = 0; q < 32; ++q) tmp[q] = Rpan[q * 32 + lane];  // (row lane, col c0+q)
+#pragma unroll
+                    for (int q = 0; q < 32; ++q) Rp[lane * kTld + q] = tmp[q];
+                }
                 __syncwarp();
                 for (int jj = 0; jj < 32; ++jj) {
-                    // pivot column -> shared memory, read back as broadcasts
-                    if (lane == jj) {
+                    double u[32];
 #pragma unroll
-                        for (int r = 0; r < 32; r += 2)
-                            *reinterpret_cast<double2*>(ucol + r) = make_double2(x[r], x[r + 1]);
-                    }
-                    __syncwarp();
-                    double s0 = 0.0, s1 = 0.0, d0 = 0.0, d1 = 0.0;
+                    for (int r = 0; r < 32; ++r) u[r] = __shfl_sync(0xffffffffu, x[r], jj);
+                    double sa[8], da[8];
 #pragma unroll
-                    for (int r = 0; r < 32; r += 2) {
-                        const double2 uu = *reinterpret_cast<const double2*>(ucol + r);
-                        s0 += uu.x * uu.x;
-                        s1 += uu.y * uu.y;
-                        d0 += uu.x * x[r];
-                        d1 += uu.y * x[r + 1];
+                    for (int q = 0; q < 8; ++q) {
+                        sa[q] = u[q] * u[q];
+                        da[q] = u[q] * x[q];
                     }
-                    const double s = s0 + s1;
+#pragma unroll
+                    for (int r = 8; r < 32; ++r) {
+                        sa[r & 7] += u[r] * u[r];
+                        da[r & 7] += u[r] * x[r];
+                    }
+                    const double s = ((sa[0] + sa[1]) + (sa[2] + sa[3])) + ((sa[4] + sa[5]) + (sa[6] + sa[7]));
+                    const double d = ((da[0] + da[1]) + (da[2] + da[3])) + ((da[4] + da[5]) + (da[6] + da[7]));
                     const double u0 = Rp[jj * kTld + jj];
-                    double alpha, tj, scale;
-                    if (s == 0.0 && u0 != 0.0) {
+                    const double nrm2 = u0 * u0 + s;
+                    // alpha = -sign(u0) ||u||, tau = (alpha - u0)/alpha = 1 + |u0|/||u||,
+                    // scale = 1/(u0 - alpha) = sign(u0)/(|u0| + ||u||)   (sign(0) = -1)
+                    const double inv = rsqrt(nrm2);
+                    const double nr = nrm2 * inv;
+                    const double au = fabs(u0);
+                    const double sg = (u0 > 0.0) ? 1.0 : -1.0;
+                    double alpha = -sg * nr;
+                    double tj = 1.0 + au * inv;
+                    double scale = sg * __drcp_rn(au + nr);
+                    if (s == 0.0 && u0 != 0.0) {  // H = I
                         alpha = u0;
                         tj = 0.0;
                         scale = 0.0;
-                    } else {
-                        const double nrm2 = u0 * u0 + s;
-                        if (nrm2 == 0.0) {
-                            alpha = sqrt(2.0 * DBL_MIN);
-                            tj = 2.0;
-                            scale = 0.0;
-                        } else {
-                            const double nr = sqrt(nrm2);
-                            alpha = (u0 > 0.0) ? -nr : nr;
-                            tj = (alpha - u0) / alpha;
-                            scale = 1.0 / (u0 - alpha);
-                        }
+                    }
+                    if (nrm2 == 0.0) {  // all-zero u: the reference's eps_fp result
+                        alpha = sqrt(2.0 * DBL_MIN);
+                        tj = 2.0;
+                        scale = 0.0;
                     }
                     const double rjk = Rp[jj * kTld + lane];
-                    const double g = tj * (rjk + scale * (d0 + d1));
-                    const double gs = g * scale;
-                    if (lane > jj) {
+                    const double g = tj * (rjk + scale * d);
+                    const bool piv = lane == jj;
+                    const double f = (lane > jj) ? g * scale : 0.0;
 #pragma unroll
-                        for (int r = 0; r < 32; r += 2) {
-                            const double2 uu = *reinterpret_cast<const double2*>(ucol + r);
-                            x[r] -= gs * uu.x;
-                            x[r + 1] -= gs * uu.y;
-                        }
-                        Rp[jj * kTld + lane] = rjk - g;
-                    } else if (lane == jj) {
-#pragma unroll
-                        for (int r = 0; r < 32; ++r) x[r] *= scale;  // v_j
+                    for (int r = 0; r < 32; ++r) x[r] = piv ? scale * u[r] : fma(-f, u[r], x[r]);
+                    if (lane > jj) Rp[jj * kTld + lane] = rjk - g;
+                    if (piv) {
                         Rp[jj * kTld + jj] = alpha;
                         tau[jj] = tj;
                     }
                     __syncwarp();
                 }
 #pragma unroll
-                for (int r = 0; r < 32; ++r) Bt[(c0 + lane) * kBlkLdb + r] = x[r];
-                for (int e = lane; e < 32 * 32; e += 32) R[blk_roff(p, M) + e] = Rp[(e & 31) * kTld + (e >> 5)];
+                for (int r = 0; r < 32; r += 2)
+                    *reinterpret_cast<double2*>(Bt + (c0 + lane) * kBlkLdb + r) = make_double2(x[r], x[r + 1]);
+                {
+                    double* Rpan = R + blk_roff(p, M);
+#pragma unroll
+                    for (int q = 0; q < 32; ++q) Rpan[q * 32 + lane] = Rp[lane * kTld + q];
+                }
             }
             __syncthreads();
+            TT_PROF(1);
             if (c0 + 32 >= M) continue;  // no trailing columns: T is not needed
             // ---- 2. S = V^T V (DMMA, warp w -> reflector columns 8w..8w+7 of 32),
             //         then T = (diag(1/tau) + striu(S))^{-1} blockwise ----
@@ -217,6 +238,7 @@ __global__ void __launch_bounds__(kBlkThreads, 2) tsqr_blk_kernel(BlkArgs a) {
                     for (int e = 0; e < 2; ++e) Sm[(8 * mt + lr) * kTld + 8 * nt + 2 * lc + e] = sacc[mt][e];
             }
             __syncthreads();
+            TT_PROF(2);
             // T = U^{-1}, U = diag(1/tau) + striu(S), by 8x8 diagonal blocks
             // (lane 8b+j back-substitutes column j of block b) and two levels
             // of the block identity [[A, B], [0, C]]^{-1} = [[A^-1, -A^-1 B C^-1], [0, C^-1]].
@@ -231,6 +253,7 @@ __global__ void __launch_bounds__(kBlkThreads, 2) tsqr_blk_kernel(BlkArgs a) {
                 }
             }
             __syncthreads();
+            TT_PROF(3);
             for (int lev = 8; lev <= 16; lev *= 2) {
                 // blocks [o, o+lev) x [o+lev, o+2lev), o = 0 (and 16 when lev = 8)
                 double* Xs = Wsc;  // scratch (>= 16 x 16 used as lev x lev, ld 17)
@@ -251,6 +274,7 @@ __global__ void __launch_bounds__(kBlkThreads, 2) tsqr_blk_kernel(BlkArgs a) {
                     Tm[(o + i) * kTld + o + lev + j] = -acc;
                 }
                 __syncthreads();
+                TT_PROF(3);
             }
             // ---- 3. trailing update over 8-column groups (DMMA m8n8k4) ----
             double* Ws = Wsc + warp * 32 * 9;
@@ -314,8 +338,12 @@ __global__ void __launch_bounds__(kBlkThreads, 2) tsqr_blk_kernel(BlkArgs a) {
                 __syncwarp();
             }
             __syncthreads();
+            TT_PROF(4);
         }
     }
+    if (a.prof && tid == 0)
+        for (int q = 0; q < 6; ++q) a.prof[blockIdx.x * 8 + q] = t_acc[q];
+#undef TT_PROF
 }
 
 // packed panel-major M x M factor -> leading m x m block, column-major ld m

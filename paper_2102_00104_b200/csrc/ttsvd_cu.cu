@@ -12,6 +12,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include <string>
 #include <vector>
 
@@ -188,7 +189,7 @@ int merge_tree_blk(ttsvd_cu_ctx* ctx, double* parts, int64_t count, int m, int M
     while (count > 1) {
         const int64_t next = (count + 1) / 2;
         double* dst = (next == 1) ? out : bufs[flip];
-        BlkArgs a{src, count, (int64_t)M, dst, nullptr, m, M, 1};
+        BlkArgs a{src, count, (int64_t)M, dst, nullptr, m, M, 1, nullptr};
         TT_TRY(launch_blk(ctx, a, (int)next));
         src = dst;
         count = next;
@@ -257,8 +258,24 @@ int tsqr_device(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t ld
             Rinit_ws = parts + RS;
             TT_TRY(pack_parts(ctx, R_init, 1, m, M, Rinit_ws));
         }
-        BlkArgs a{X, n, ld, parts, Rinit_ws, m, M, 0};
+        BlkArgs a{X, n, ld, parts, Rinit_ws, m, M, 0, nullptr};
+        static const bool prof = std::getenv("TTSVD_PROF_BLK") != nullptr;
+        long long* dprof = nullptr;
+        if (prof) TT_CUDA(cudaMalloc(&dprof, (size_t)G * 8 * sizeof(long long)));
+        a.prof = dprof;
         TT_TRY(launch_blk(ctx, a, (int)G));
+        if (prof) {
+            std::vector<long long> hp((size_t)G * 8);
+            TT_CUDA(cudaMemcpy(hp.data(), dprof, hp.size() * 8, cudaMemcpyDeviceToHost));
+            cudaFree(dprof);
+            double ph[6] = {0, 0, 0, 0, 0, 0};
+            for (int64_t g = 0; g < G; ++g)
+                for (int q = 0; q < 6; ++q) ph[q] += (double)hp[g * 8 + q] / G;
+            const double tiles = (double)n / G / 32.0;
+            std::fprintf(stderr, "[blk prof] n=%lld m=%d G=%lld tiles/CTA=%.1f  Mcyc/CTA: load %.2f panel %.2f S %.2f T %.2f trail %.2f | per tile kcyc: %.1f %.1f %.1f %.1f %.1f\n",
+                         (long long)n, m, (long long)G, tiles, ph[0] / 1e6, ph[1] / 1e6, ph[2] / 1e6, ph[3] / 1e6, ph[4] / 1e6,
+                         ph[0] / tiles / 1e3, ph[1] / tiles / 1e3, ph[2] / tiles / 1e3, ph[3] / tiles / 1e3, ph[4] / tiles / 1e3);
+        }
         if (G > 1) {
             TT_TRY(ensure(ctx->ws_P, (size_t)RS * 8));
             TT_TRY(merge_tree_blk(ctx, parts, G, m, M, as<double>(ctx->ws_P)));
@@ -324,6 +341,8 @@ int jacobi_status(ttsvd_cu_ctx* ctx, int* sweeps) {
     TT_CUDA(cudaMemcpyAsync(&h, as<int>(ctx->ws_flags) + 40, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
     TT_CUDA(cudaStreamSynchronize(ctx->stream));
     *sweeps = h;
+    static const bool dbg = std::getenv("TTSVD_DEBUG_SVD") != nullptr;
+    if (dbg) std::fprintf(stderr, "[jacobi] sweeps %d\n", h);
     if (h < 0) return fail(TTSVD_ERR_CONVERGENCE, "jacobi_svd: no convergence in 30 sweeps");
     return TTSVD_OK;
 }
