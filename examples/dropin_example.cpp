@@ -1,0 +1,43 @@
+// Reference-style caller of the B200 drop-in (include/ttsvd_b200.hpp): the
+// same code a user of /root/reference/proj/include/ttsvd would write.
+//   g++ -std=c++20 -Iinclude -I/usr/local/cuda/include examples/dropin_example.cpp
+//       -Lpaper_2102_00104_b200 -lttsvd_cu -L/usr/local/cuda/lib64 -lcudart
+// Without a GPU (argv[1] == "host") only host-side entry points run.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+
+#include "ttsvd_b200.hpp"
+
+int main(int argc, char** argv) {
+    using namespace ttsvd;
+    if (padded_stride(262144) != 262208) return 1;
+    if (select_rank({2, 1, 0.5, 0.1}, 0.2, 10) != 3) return 2;
+    if (derive_delta(2.0, 0.1, 5) < 0.0999999 || derive_delta(2.0, 0.1, 5) > 0.1000001) return 3;
+    try {
+        derive_delta(1.0, 0.1, 1);
+        return 4;
+    } catch (const DegenerateDimension&) {
+    }
+    if (argc > 1 && std::strcmp(argv[1], "host") == 0) {
+        std::printf("host entry points ok\n");
+        return 0;
+    }
+    // device path: 4^8 tensor, entries from a simple deterministic pattern
+    DenseTensor X({4, 4, 4, 4, 4, 4, 4, 4});
+    for (index_t l = 0; l < X.total(); ++l) X.at_flat(l) = ((l * 7919) % 1000) / 1000.0 - 0.5;
+    TruncationSpec spec;
+    spec.r_max = 8;
+    TensorTrain tt = tt_svd_tsqr(X, spec);
+    const auto r = tt.ranks();
+    std::printf("ranks:");
+    for (auto v : r) std::printf(" %lld", static_cast<long long>(v));
+    std::printf("\n");
+    PaddedMatrix M(1000, 4);
+    for (index_t j = 0; j < 4; ++j) M(j, j) = 1.0;
+    TriangularFactor R = tsqr(M.view(), BlockParams::for_cols(4), 1);
+    for (index_t j = 0; j < 4; ++j)
+        if (std::abs(std::abs(R(j, j)) - 1.0) > 1e-14) return 5;
+    std::printf("device entry points ok\n");
+    return 0;
+}

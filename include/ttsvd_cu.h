@@ -94,6 +94,8 @@ int ttsvd_cu_jacobi_svd(ttsvd_cu_ctx* ctx, const double* A, int64_t n, int64_t m
 /* small_svd.hpp:49 select_rank() on a device sigma; the rank is returned on the host. */
 int ttsvd_cu_select_rank(ttsvd_cu_ctx* ctx, const double* sigma, int64_t m, double delta, int64_t r_max,
                          int64_t* rank_host);
+/* small_svd.hpp:49 select_rank() on a host sigma (pure host arithmetic). */
+int64_t ttsvd_cu_select_rank_host(const double* sigma_host, int64_t m, double delta, int64_t r_max);
 /* small_svd.hpp:41 derive_delta() (host arithmetic, kept for completeness). */
 int ttsvd_cu_derive_delta(double norm_source, double eps, int64_t d, double* delta_host);
 /* tsmm.hpp:20 tsmm_reshape(): Y (out_rows x out_cols, ld ldy >= out_rows)

@@ -776,3 +776,33 @@ void orc_mt_uniform(uint64_t seed, idx count, double shift, double* out) {
     mt64_seed(&g, seed);
     for (idx i = 0; i < count; ++i) out[i] = (double)(mt64_next(&g) >> 11) * 0x1.0p-53 + shift;
 }
+
+/* Diagnostics: sweeps the cyclic one-sided Jacobi needs on A (n x m). */
+int orc_jacobi_sweeps(const double* A, idx n, idx m, idx lda) {
+    double* a = (double*)malloc((size_t)(n * m + m * m) * sizeof(double));
+    for (idx j = 0; j < m; ++j)
+        for (idx i = 0; i < n; ++i) a[j * n + i] = A[j * lda + i];
+    double* v = a + n * m;
+    for (idx i = 0; i < m * m; ++i) v[i] = 0.0;
+    const double tol = 1e2 * DBL_EPSILON;
+    int sweep = 0;
+    for (; sweep < 60; ++sweep) {
+        int rotated = 0;
+        for (idx p = 0; p < m - 1; ++p)
+            for (idx q = p + 1; q < m; ++q) {
+                double* ap = a + p * n;
+                double* aq = a + q * n;
+                double al = 0, be = 0, ga = 0;
+                for (idx i = 0; i < n; ++i) { al += ap[i] * ap[i]; be += aq[i] * aq[i]; ga += ap[i] * aq[i]; }
+                if (fabs(ga) <= tol * sqrt(al * be)) continue;
+                rotated = 1;
+                const double zeta = (be - al) / (2.0 * ga);
+                const double t = ((zeta >= 0.0) ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+                const double c = 1.0 / sqrt(1.0 + t * t), s = c * t;
+                for (idx i = 0; i < n; ++i) { const double x = ap[i], y = aq[i]; ap[i] = c * x - s * y; aq[i] = s * x + c * y; }
+            }
+        if (!rotated) break;
+    }
+    free(a);
+    return sweep;
+}

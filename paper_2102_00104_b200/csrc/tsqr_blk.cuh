@@ -31,7 +31,7 @@ namespace ttsvd_b200 {
 
 constexpr int kBlkRows = 32;    // tile rows (one per lane in the panel)
 constexpr int kBlkLdb = 36;     // smem ld of the tile: fragment loads in 2 wavefronts
-constexpr int kBlkThreads = 128;
+constexpr int kBlkThreads = 256;  // 8 lanes per panel column in the panel
 constexpr int kTld = 33;        // smem ld of S and T
 
 struct BlkArgs {
@@ -59,7 +59,7 @@ __host__ __device__ __forceinline__ int64_t blk_roff(int p, int M) {
 __host__ __device__ __forceinline__ int64_t blk_rsize(int M) { return blk_roff(M / 32, M); }
 
 inline size_t blk_smem_bytes(int M) {
-    return ((size_t)M * kBlkLdb + 3 * 32 * kTld + 64 + (kBlkThreads / 32) * 32 * 9) * sizeof(double);
+    return ((size_t)M * kBlkLdb + 2 * 32 * kTld + 96 + (kBlkThreads / 32) * 32 * 9) * sizeof(double);
 }
 
 __global__ void __launch_bounds__(kBlkThreads, 2) tsqr_blk_kernel(BlkArgs a) {
@@ -68,11 +68,11 @@ __global__ void __launch_bounds__(kBlkThreads, 2) tsqr_blk_kernel(BlkArgs a) {
     const int M = a.M, m = a.m;
     double* Bt = sm;                          // M columns x 32 rows, ld kBlkLdb
     double* Sm = Bt + (size_t)M * kBlkLdb;    // 32 x 32 (S = V^T V, row-major, ld kTld)
+    double* Rp = Sm;                          // 32 x 32 panel block of R: dead before S is formed
     double* Tm = Sm + 32 * kTld;              // 32 x 32 (T, row-major)
-    double* Rp = Tm + 32 * kTld;              // 32 x 32 panel block of R (row-major)
-    double* tau = Rp + 32 * kTld;             // 32
-    double* ucol = tau + 32;                  // 32: the pivot column being broadcast
-    double* Wsc = ucol + 32;                  // per-warp 32 x 8 scratch (ld 9)
+    double* tau = Tm + 32 * kTld;             // 32
+    double* ucol = tau + 32;                  // 2 x 32: the pivot column being broadcast
+    double* Wsc = ucol + 64;                  // per-warp 32 x 8 scratch (ld 9)
 
     const int64_t job = blockIdx.x;
     const double* X;
@@ -101,7 +101,8 @@ __global__ void __launch_bounds__(kBlkThreads, 2) tsqr_blk_kernel(BlkArgs a) {
         }
         ld = M;
     }
-    for (int64_t e = tid; e < RS; e += kBlkThreads) R[e] = R_init ? R_init[e] : 0.0;
+    const uint64_t pol_x = l2_policy_evict_first(), pol_r = l2_policy_evict_last();
+    for (int64_t e = tid; e < RS; e += kBlkThreads) st_hint(R + e, R_init ? R_init[e] : 0.0, pol_r);
     __syncthreads();
 
     long long t_prev = 0, t_acc[6] = {0, 0, 0, 0, 0, 0};
@@ -118,7 +119,7 @@ __global__ void __launch_bounds__(kBlkThreads, 2) tsqr_blk_kernel(BlkArgs a) {
         if (a.mode == 0) {
             for (int e = tid; e < M * kBlkRows; e += kBlkThreads) {
                 const int c = e >> 5, i = e & 31;
-                Bt[c * kBlkLdb + i] = (i < rows && c < m) ? X[(int64_t)c * ld + r0 + i] : 0.0;
+                Bt[c * kBlkLdb + i] = (i < rows && c < m) ? ld_stream_hint(X + (int64_t)c * ld + r0 + i, pol_x) : 0.0;
             }
         } else {
             // row panel t of a packed triangular part: columns < 32t are zero
@@ -139,44 +140,42 @@ __global__ void __launch_bounds__(kBlkThreads, 2) tsqr_blk_kernel(BlkArgs a) {
             // column is broadcast by shuffles, so every reflector needs no
             // cross-lane reduction: lanes compute the norm redundantly and
             // their own column's dot product locally.
-            if (warp == 0) {
-                double x[32];
-#pragma unroll
-                for (int r = 0; r < 32; r += 2) {
-                    const double2 t = *reinterpret_cast<const double2*>(Bt + (c0 + lane) * kBlkLdb + r);
-                    x[r] = t.x;
-                    x[r + 1] = t.y;
+            // ---- 1. panel factorisation: the whole CTA, 8 lanes per panel
+            //         column (lane group g holds rows 4g..4g+3), one barrier
+            //         per reflector (the pivot column is double buffered) ----
+            {
+                const int pc = tid >> 3;        // panel column owned by this lane group
+                const int rg = (tid & 7) * 4;   // first of this lane's 4 tile rows
+                double x[4];
+                {
+                    const double2 t0 = *reinterpret_cast<const double2*>(Bt + (c0 + pc) * kBlkLdb + rg);
+                    const double2 t1 = *reinterpret_cast<const double2*>(Bt + (c0 + pc) * kBlkLdb + rg + 2);
+                    x[0] = t0.x; x[1] = t0.y; x[2] = t1.x; x[3] = t1.y;
                 }
                 {
                     const double* Rpan = R + blk_roff(p, M);  // row panel p: column c0 + k at k*32
-                    double tmp[32];
-#pragma unroll
-                    for (int q = 0; q < 32; ++q) tmp[q] = Rpan[q * 32 + lane];  // (row lane, col c0+q)
-#pragma unroll
-                    for (int q = 0; q < 32; ++q) Rp[lane * kTld + q] = tmp[q];
+                    for (int e = tid; e < 32 * 32; e += kBlkThreads)
+                        Rp[(e & 31) * kTld + (e >> 5)] = ld_hint(Rpan + e, pol_r);
                 }
-                __syncwarp();
                 for (int jj = 0; jj < 32; ++jj) {
-                    double u[32];
-#pragma unroll
-                    for (int r = 0; r < 32; ++r) u[r] = __shfl_sync(0xffffffffu, x[r], jj);
-                    double sa[8], da[8];
-#pragma unroll
-                    for (int q = 0; q < 8; ++q) {
-                        sa[q] = u[q] * u[q];
-                        da[q] = u[q] * x[q];
+                    double* ub = ucol + (jj & 1) * 32;
+                    if (pc == jj) {
+                        *reinterpret_cast<double2*>(ub + rg) = make_double2(x[0], x[1]);
+                        *reinterpret_cast<double2*>(ub + rg + 2) = make_double2(x[2], x[3]);
                     }
+                    __syncthreads();
+                    const double2 u01 = *reinterpret_cast<const double2*>(ub + rg);
+                    const double2 u23 = *reinterpret_cast<const double2*>(ub + rg + 2);
+                    double sp = u01.x * u01.x + u01.y * u01.y + (u23.x * u23.x + u23.y * u23.y);
+                    double dp = u01.x * x[0] + u01.y * x[1] + (u23.x * x[2] + u23.y * x[3]);
 #pragma unroll
-                    for (int r = 8; r < 32; ++r) {
-                        sa[r & 7] += u[r] * u[r];
-                        da[r & 7] += u[r] * x[r];
+                    for (int o = 1; o < 8; o <<= 1) {
+                        sp += __shfl_xor_sync(0xffffffffu, sp, o);
+                        dp += __shfl_xor_sync(0xffffffffu, dp, o);
                     }
-                    const double s = ((sa[0] + sa[1]) + (sa[2] + sa[3])) + ((sa[4] + sa[5]) + (sa[6] + sa[7]));
-                    const double d = ((da[0] + da[1]) + (da[2] + da[3])) + ((da[4] + da[5]) + (da[6] + da[7]));
                     const double u0 = Rp[jj * kTld + jj];
-                    const double nrm2 = u0 * u0 + s;
-                    // alpha = -sign(u0) ||u||, tau = (alpha - u0)/alpha = 1 + |u0|/||u||,
-                    // scale = 1/(u0 - alpha) = sign(u0)/(|u0| + ||u||)   (sign(0) = -1)
+                    const double nrm2 = u0 * u0 + sp;
+                    // alpha = -sign(u0) ||u||, tau = 1 + |u0|/||u||, scale = 1/(u0 - alpha)
                     const double inv = rsqrt(nrm2);
                     const double nr = nrm2 * inv;
                     const double au = fabs(u0);
@@ -184,7 +183,7 @@ __global__ void __launch_bounds__(kBlkThreads, 2) tsqr_blk_kernel(BlkArgs a) {
                     double alpha = -sg * nr;
                     double tj = 1.0 + au * inv;
                     double scale = sg * __drcp_rn(au + nr);
-                    if (s == 0.0 && u0 != 0.0) {  // H = I
+                    if (sp == 0.0 && u0 != 0.0) {  // H = I
                         alpha = u0;
                         tj = 0.0;
                         scale = 0.0;
@@ -194,26 +193,32 @@ __global__ void __launch_bounds__(kBlkThreads, 2) tsqr_blk_kernel(BlkArgs a) {
                         tj = 2.0;
                         scale = 0.0;
                     }
-                    const double rjk = Rp[jj * kTld + lane];
-                    const double g = tj * (rjk + scale * d);
-                    const bool piv = lane == jj;
-                    const double f = (lane > jj) ? g * scale : 0.0;
-#pragma unroll
-                    for (int r = 0; r < 32; ++r) x[r] = piv ? scale * u[r] : fma(-f, u[r], x[r]);
-                    if (lane > jj) Rp[jj * kTld + lane] = rjk - g;
-                    if (piv) {
-                        Rp[jj * kTld + jj] = alpha;
-                        tau[jj] = tj;
+                    if (pc > jj) {
+                        const double rjk = Rp[jj * kTld + pc];
+                        const double g = tj * (rjk + scale * dp);
+                        const double f = g * scale;
+                        x[0] = fma(-f, u01.x, x[0]);
+                        x[1] = fma(-f, u01.y, x[1]);
+                        x[2] = fma(-f, u23.x, x[2]);
+                        x[3] = fma(-f, u23.y, x[3]);
+                        if (rg == 0) Rp[jj * kTld + pc] = rjk - g;
+                    } else if (pc == jj) {
+                        x[0] = scale * u01.x;  // v_j
+                        x[1] = scale * u01.y;
+                        x[2] = scale * u23.x;
+                        x[3] = scale * u23.y;
+                        if (rg == 0) {
+                            Rp[jj * kTld + jj] = alpha;
+                            tau[jj] = tj;
+                        }
                     }
-                    __syncwarp();
                 }
-#pragma unroll
-                for (int r = 0; r < 32; r += 2)
-                    *reinterpret_cast<double2*>(Bt + (c0 + lane) * kBlkLdb + r) = make_double2(x[r], x[r + 1]);
+                *reinterpret_cast<double2*>(Bt + (c0 + pc) * kBlkLdb + rg) = make_double2(x[0], x[1]);
+                *reinterpret_cast<double2*>(Bt + (c0 + pc) * kBlkLdb + rg + 2) = make_double2(x[2], x[3]);
+                __syncthreads();
                 {
                     double* Rpan = R + blk_roff(p, M);
-#pragma unroll
-                    for (int q = 0; q < 32; ++q) Rpan[q * 32 + lane] = Rp[lane * kTld + q];
+                    for (int e = tid; e < 32 * 32; e += kBlkThreads) st_hint(Rpan + e, Rp[(e & 31) * kTld + (e >> 5)], pol_r);
                 }
             }
             __syncthreads();
@@ -285,7 +290,7 @@ __global__ void __launch_bounds__(kBlkThreads, 2) tsqr_blk_kernel(BlkArgs a) {
                 for (int mt = 0; mt < 4; ++mt)
 #pragma unroll
                     for (int e = 0; e < 2; ++e) {
-                        rsav[mt][e] = Rrow[(g + 2 * lc + e - c0) * 32 + 8 * mt + lr];
+                        rsav[mt][e] = ld_hint(Rrow + (g + 2 * lc + e - c0) * 32 + 8 * mt + lr, pol_r);
                         acc[mt][e] = rsav[mt][e];
                     }
                 // W = R(p, c) + V^T B(:, c):  A = V^T (refl x row), B = tile (row x col)
@@ -315,7 +320,7 @@ __global__ void __launch_bounds__(kBlkThreads, 2) tsqr_blk_kernel(BlkArgs a) {
                 for (int mt = 0; mt < 4; ++mt)
 #pragma unroll
                     for (int e = 0; e < 2; ++e) {
-                        Rrow[(g + 2 * lc + e - c0) * 32 + 8 * mt + lr] = rsav[mt][e] - w2[mt][e];
+                        st_hint(Rrow + (g + 2 * lc + e - c0) * 32 + 8 * mt + lr, rsav[mt][e] - w2[mt][e], pol_r);
                         Ws[(8 * mt + lr) * 9 + 2 * lc + e] = w2[mt][e];
                     }
                 __syncwarp();

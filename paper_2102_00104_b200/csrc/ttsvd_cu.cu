@@ -247,7 +247,10 @@ int tsqr_device(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t ld
     if (m > kSmallM) {
         const int M = (m + 31) / 32 * 32;
         const int64_t RS = blk_rsize(M);
-        const int per_sm = blk_smem_bytes(M) * 2 <= (size_t)kSmemLimit ? 2 : 1;
+        int per_sm = 1;
+        TT_CUDA(cudaFuncSetAttribute(tsqr_blk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit));
+        TT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tsqr_blk_kernel, kBlkThreads, blk_smem_bytes(M)));
+        per_sm = std::max(1, per_sm);
         int64_t G = std::max<int64_t>(1, n / (4 * (int64_t)M));
         G = std::min<int64_t>(G, (int64_t)per_sm * ctx->num_sms);
         if (R_init) G = 1;
@@ -355,28 +358,37 @@ int finalize_device(ttsvd_cu_ctx* ctx, const double* A, int n, int m, const doub
 }
 
 // sigma and right singular vectors of a work matrix.
-//   tall (small_svd of the TSQR factor, tt_svd.hpp:80-90): one-sided Jacobi on
-//     the columns of R with the rotations accumulated into V — the
-//     reference's algorithm, so V is orthonormal to working precision even
-//     for numerically zero sigma;
-//   wide (tt_svd.hpp:91-103): Jacobi on the columns of W^T, V := the
-//     normalised columns (the reference's U of jacobi_svd(W^T)) with its
-//     deterministic completion.
+//   accumulate == true (the small_svd / jacobi_svd API, small_svd.hpp:72-114):
+//     one-sided Jacobi on the columns of R with the rotations accumulated
+//     into V — the reference's algorithm, V orthonormal to working precision
+//     even for sigma ~ 0;
+//   accumulate == false (the TT-SVD driver): one-sided Jacobi on the columns
+//     of R^T (tall step) or W^T (wide step, tt_svd.hpp:91-103); the
+//     orthogonalised columns are sigma_j v_j, so V := their normalisation
+//     (with the reference's deterministic completion for sigma <= n eps
+//     sigma_1).  No rotation accumulation, and Jacobi on the transposed
+//     triangular factor converges in ~40% fewer sweeps (Drmac's observation;
+//     15 -> 9 sweeps on config-2-like factors, tools/ measurements).  The
+//     driver only consumes the leading r columns, with sigma_r above the
+//     numerical-zero level (choose_rank), where this V is accurate.
 // src is (src_rows x src_cols, ld); sigma gets nsig values, Vout is
 // (cols x nsig, ld cols).
-int svd_work(ttsvd_cu_ctx* ctx, const double* src, int64_t src_rows, int64_t src_cols, int64_t src_ld, bool wide,
-             double* sigma, double* Vout, int* sweeps) {
-    const int64_t n = wide ? src_cols : src_rows;   // column length of A
-    const int64_t m = wide ? src_rows : src_cols;   // columns of A
+int svd_work(ttsvd_cu_ctx* ctx, const double* src, int64_t src_rows, int64_t src_cols, int64_t src_ld, bool transpose,
+             bool accumulate, double* sigma, double* Vout, int* sweeps) {
+    const int64_t n = transpose ? src_cols : src_rows;   // column length of A
+    const int64_t m = transpose ? src_rows : src_cols;   // columns of A
     TT_TRY(ensure(ctx->ws_A, (size_t)n * m * 8));
     double* A = as<double>(ctx->ws_A);
-    if (wide) {
+    if (transpose) {
         TT_TRY(transpose_device(ctx, src, src_rows, src_cols, src_ld, A));
+    } else {
+        TT_CUDA(cudaMemcpy2DAsync(A, n * 8, src, src_ld * 8, n * 8, m, cudaMemcpyDeviceToDevice, ctx->stream));
+    }
+    if (!accumulate) {
         TT_TRY(jacobi_device(ctx, A, (int)n, (int)m, nullptr));
         TT_TRY(jacobi_status(ctx, sweeps));
         return finalize_device(ctx, A, (int)n, (int)m, nullptr, sigma, Vout, nullptr);
     }
-    TT_CUDA(cudaMemcpy2DAsync(A, n * 8, src, src_ld * 8, n * 8, m, cudaMemcpyDeviceToDevice, ctx->stream));
     TT_TRY(ensure(ctx->ws_Vacc, (size_t)m * m * 8));
     TT_TRY(ensure(ctx->ws_U, (size_t)n * m * 8));
     double* Vacc = as<double>(ctx->ws_Vacc);
@@ -514,11 +526,11 @@ int run_chain(ttsvd_cu_ctx* ctx, WorkView cur, const std::vector<int64_t>& dims,
             double* R = as<double>(ctx->ws_X);
             TT_TRY(tsqr_device(ctx, cur.data, cur.rows, (int)m, cur.ld, R));
             tm.mark(1);
-            TT_TRY(svd_work(ctx, R, m, m, m, false, d_sigma, d_V, &sweeps));
+            TT_TRY(svd_work(ctx, R, m, m, m, true, false, d_sigma, d_V, &sweeps));
         } else {
             tm.mark(1);
             // wide step (tt_svd.hpp:91-103): Jacobi on W^T, V := its U
-            TT_TRY(svd_work(ctx, cur.data, cur.rows, cur.cols, cur.ld, true, d_sigma, d_V, &sweeps));
+            TT_TRY(svd_work(ctx, cur.data, cur.rows, cur.cols, cur.ld, true, false, d_sigma, d_V, &sweeps));
         }
         tm.mark(2);
         sig.resize(nsig);
@@ -691,7 +703,7 @@ int ttsvd_cu_small_svd(ttsvd_cu_ctx* ctx, const double* R, int64_t m, double* si
     if (m > 4096) return fail(TTSVD_ERR_DIMENSION_MISMATCH, "small_svd: m exceeds 4096");
     if (m < 1 || !R || !sigma || !V) return fail(TTSVD_ERR_INVALID, "small_svd: bad arguments");
     int sweeps = 0;
-    TT_TRY(svd_work(ctx, R, m, m, m, false, sigma, V, &sweeps));
+    TT_TRY(svd_work(ctx, R, m, m, m, false, true, sigma, V, &sweeps));
     TT_CUDA(cudaStreamSynchronize(ctx->stream));
     return TTSVD_OK;
 }
@@ -727,6 +739,11 @@ int ttsvd_cu_select_rank(ttsvd_cu_ctx* ctx, const double* sigma, int64_t m, doub
     if (m > 0) TT_TRY(d2h(ctx, s.data(), sigma, (size_t)m));
     *rank_host = select_rank_h(s.data(), m, delta, r_max);
     return TTSVD_OK;
+}
+
+int64_t ttsvd_cu_select_rank_host(const double* sigma, int64_t m, double delta, int64_t r_max) {
+    if (!sigma || m < 0) return -1;
+    return select_rank_h(sigma, m, delta, r_max);
 }
 
 int ttsvd_cu_derive_delta(double norm_source, double eps, int64_t d, double* delta_host) {
@@ -866,7 +883,7 @@ int ttsvd_cu_tt_svd_distributed(ttsvd_cu_ctx* ctx, const double* const* slabs, i
         double* d_sigma = as<double>(ctx->ws_sigma);
         double* d_V = as<double>(ctx->ws_V);
         int sweeps = 0;
-        if ((rc = svd_work(ctx, R, m, m, m, false, d_sigma, d_V, &sweeps)) != TTSVD_OK) break;
+        if ((rc = svd_work(ctx, R, m, m, m, true, false, d_sigma, d_V, &sweeps)) != TTSVD_OK) break;
         sig.resize(m);
         if ((rc = d2h(ctx, sig.data(), d_sigma, m)) != TTSVD_OK) break;
         const int64_t global_rows = cur[0].rows * P_total;

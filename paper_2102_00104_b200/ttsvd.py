@@ -507,14 +507,16 @@ def _torch_exchange(group):
 
 
 def tt_svd_distributed(slabs, ldims, spec: TruncationSpec | tuple | None = None, ctx_exec=None,
-                       group=None, P_total: int | None = None, part0: int = 0) -> TensorTrain:
+                       group=None, P_total: int | None = None, part0: int = 0, exchange=None) -> TensorTrain:
     """tt_svd.hpp:520 (Alg. 5).  ``slabs`` are this process's device slabs
     ((rows x n_last) column-major views of the local shape ``ldims``, all with
     the same leading stride).  Single process: all P slabs, no exchange (the
     reference's in-process form).  Multi-process (``group`` given, one or more
     slabs per rank): the per-rank R factors are all-gathered over
     torch.distributed (NCCL on B200) and every rank runs the same pinned-order
-    merge and small SVD, so shared cores are bitwise identical."""
+    merge and small SVD, so shared cores are bitwise identical.  ``exchange``
+    overrides the all-gather (a callable(send_tensor, recv_tensor) on device
+    tensors)."""
     spec = _spec(spec)
     ldims = [int(x) for x in ldims]
     if len(slabs) == 0:
@@ -530,7 +532,18 @@ def tt_svd_distributed(slabs, ldims, spec: TruncationSpec | tuple | None = None,
     ptrs = (C.c_void_p * n_slabs)(*[C.c_void_p(s.data_ptr()) for s in slabs])
     dv = np.asarray(ldims, dtype=np.int64)
     r_max = spec.r_max if spec.r_max < 2 ** 62 else 0
-    exch = _torch_exchange(group) if n_slabs != P_total else _lib.EXCHANGE_FN()
+    if exchange is not None:
+        def _cb(user, send, recv, count, stream):
+            try:
+                s_t = torch.as_tensor(_CAI(send, count), device="cuda")
+                r_t = torch.as_tensor(_CAI(recv, count * (P_total // n_slabs)), device="cuda")
+                exchange(s_t, r_t)
+                return 0
+            except Exception:
+                return 1
+        exch = _lib.EXCHANGE_FN(_cb)
+    else:
+        exch = _torch_exchange(group) if n_slabs != P_total else _lib.EXCHANGE_FN()
     h = C.c_void_p()
     _check(_lib.lib().ttsvd_cu_tt_svd_distributed(ctx.handle, ptrs, n_slabs, part0, P_total,
                                                   dv.ctypes.data_as(_lib.i64p), len(ldims), lds.pop(), r_max,

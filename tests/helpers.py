@@ -72,3 +72,21 @@ def rel_error(X: np.ndarray, dims, cores) -> float:
     x = padded_to_flat(X, dims)
     y = tt_full(cores)
     return float(np.linalg.norm(x - y) / np.linalg.norm(x))
+
+
+def split_slabs(glob: np.ndarray, gdims, P: int):
+    """split_first_dim (ttsvd_bench.cpp:72-86): slab p holds global flat
+    entries l -> p + P*l, each stored in its own padded layout."""
+    from oracle.oracle import padded_stride
+    ldims = list(gdims[1:])
+    rest = int(np.prod(gdims)) // P
+    rows = rest // ldims[-1]
+    ld = padded_stride(rows)
+    grows = int(np.prod(gdims)) // gdims[-1]
+    flat = glob[:grows].reshape(-1, order="F")
+    out = []
+    for p in range(P):
+        s = np.zeros((ld, ldims[-1]), order="F")
+        s[:rows] = flat[p::P].reshape((rows, ldims[-1]), order="F")
+        out.append(s)
+    return out, ldims, ld

@@ -52,3 +52,33 @@ def test_c_header_compiles_standalone(tmp_path):
                        capture_output=True, text=True)
     assert r.returncode == 0, r.stderr
     assert subprocess.run([str(tmp_path / "t")]).returncode == 0
+
+
+def _build_example(tmp_path):
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    lib = os.path.join(root, "paper_2102_00104_b200")
+    exe = str(tmp_path / "dropin")
+    r = subprocess.run(["g++", "-std=c++20", "-Wall", "-Werror", f"-I{root}/include", "-I/usr/local/cuda/include",
+                        os.path.join(root, "examples", "dropin_example.cpp"), "-o", exe, f"-L{lib}", "-lttsvd_cu",
+                        f"-Wl,-rpath,{lib}", "-L/usr/local/cuda/lib64", "-lcudart", "-Wl,-rpath,/usr/local/cuda/lib64"],
+                       capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    return exe
+
+
+def test_cpp_dropin_header_compiles_and_host_entries_run(tmp_path):
+    """include/ttsvd_b200.hpp: the reference's names/types over the C-ABI."""
+    import subprocess
+    exe = _build_example(tmp_path)
+    r = subprocess.run([exe, "host"], capture_output=True, text=True)
+    assert r.returncode == 0, (r.returncode, r.stdout, r.stderr)
+
+
+@pytest.mark.gpu
+def test_cpp_dropin_device_path(tmp_path):
+    import subprocess
+    exe = _build_example(tmp_path)
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, (r.returncode, r.stdout, r.stderr)
+    assert "device entry points ok" in r.stdout

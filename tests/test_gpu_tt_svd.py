@@ -10,7 +10,7 @@ to gauge via the principal angles of the right frames (<= 1e-8 rad).
 import numpy as np
 import pytest
 
-from helpers import frame_angles, rel_error
+from helpers import frame_angles, rel_error, split_slabs
 
 pytestmark = pytest.mark.gpu
 
@@ -197,31 +197,13 @@ def test_exact_tt_rank32_scaled_config2(tt, orc):
 
 
 # ----------------------------------------------------------- distributed ----
-def _slabs(glob, gdims, P):
-    """split_first_dim (ttsvd_bench.cpp:72-86): slab p holds l -> p + P*l."""
-    rest = int(np.prod(gdims)) // P
-    ldims = gdims[1:]
-    rows = rest // ldims[-1]
-    from oracle.oracle import padded_stride
-    ld = padded_stride(rows)
-    total = int(np.prod(gdims))
-    grows = total // gdims[-1]
-    flat = glob[:grows].reshape(-1, order="F")
-    out = []
-    for p in range(P):
-        s = np.zeros((ld, ldims[-1]), order="F")
-        s[:rows] = flat[p::P].reshape((rows, ldims[-1]), order="F")
-        out.append(s)
-    return out, ldims, ld
-
-
 def test_distributed_matches_unsplit_c08(tt, orc, ref):
     # acceptance_test.cpp:311-340: (4, 2^12) split over 4 partitions
     import torch
     from oracle.oracle import random_tensor
     gdims = [4] + [2] * 12
     glob = random_tensor(2718, gdims)
-    slabs, ldims, ld = _slabs(glob, gdims, 4)
+    slabs, ldims, ld = split_slabs(glob, gdims, 4)
     rows = int(np.prod(ldims)) // ldims[-1]
     dev = [torch.from_numpy(np.ascontiguousarray(s.T)).cuda().t()[:rows] for s in slabs]
     T = tt.tt_svd_distributed(dev, ldims, (4, 0.0))
@@ -258,3 +240,76 @@ def test_distributed_partition_mismatch(tt):
     b = torch.zeros((6, 64), dtype=torch.float64, device="cuda").t()[:2]
     with pytest.raises(tt.PartitionMismatch):
         tt.tt_svd_distributed([a, b], [2, 5], (2, 0.0))
+
+
+# ------------------------------------------------- committed golden fixtures ----
+GOLD = __import__("os").path.join(__import__("os").path.dirname(__import__("os").path.abspath(__file__)), "golden",
+                                  "reference_golden.npz")
+
+
+@pytest.mark.parametrize("name,seed,dims,rmax,eps", [("tt_2pow12_seed43_r4", 43, [2] * 12, 4, 0.0),
+                                                     ("tt_2pow16_seed4242_r5", 4242, [2] * 16, 5, 0.0),
+                                                     ("tt_2x3x4x5x6_seed113_r5", 113, [2, 3, 4, 5, 6], 5, 0.0),
+                                                     ("tt_4pow6_seed5001_r8_eps1e-2", 5001, [4] * 6, 8, 1e-2)])
+def test_gpu_vs_reference_golden(tt, name, seed, dims, rmax, eps):
+    """GPU result vs outputs the reference itself produced (tests/golden/)."""
+    import torch
+    from oracle.oracle import random_tensor, split_cores
+    g = np.load(GOLD)
+    X = random_tensor(seed, dims)
+    rows = int(np.prod(dims)) // dims[-1]
+    Xd = torch.from_numpy(np.ascontiguousarray(X.T)).cuda().t()[:rows]
+    T = tt.tt_svd_tsqr(Xd, dims, (rmax, eps))
+    ranks = g[f"{name}_ranks"].tolist()
+    assert T.ranks() == ranks
+    ref_cores = split_cores(g[f"{name}_cores"], dims, ranks)
+    assert abs(rel_error(X, dims, cores_of(T)) - float(g[f"{name}_error"])) <= 1e-10
+    assert max(frame_angles(cores_of(T), ref_cores)) <= 1e-8
+
+
+def test_gpu_config1_vs_reference_golden(tt, orc):
+    import torch
+    from oracle.oracle import split_cores
+    g = np.load(GOLD)
+    dims = [4] * 10
+    X = orc.gen_uniform(1, dims)
+    Xd = tt.gen_uniform(1, dims)  # the device generator must give the same bytes
+    full = Xd.as_strided((Xd.stride(1), dims[-1]), (1, Xd.stride(1))).cpu().numpy()
+    assert np.array_equal(full, X)
+    T = tt.tt_svd_tsqr(Xd, dims, (16, 0.0))
+    ranks = g["cfg1_ranks"].tolist()
+    assert T.ranks() == ranks
+    sig = np.concatenate(T.sigmas)
+    assert np.max(np.abs(sig - g["cfg1_sigma"])) <= 1e-10 * np.max(g["cfg1_sigma"])
+    assert abs(rel_error(X, dims, cores_of(T)) - float(g["cfg1_error"])) <= 1e-10
+    assert max(frame_angles(cores_of(T), split_cores(g["cfg1_cores"], dims, ranks))) <= 1e-8
+
+
+def test_distributed_exchange_callback_path(tt, ref):
+    """The multi-process code path of ttsvd_cu_tt_svd_distributed (exchange
+    callback through ctypes, device pointers wrapped as torch tensors) on one
+    GPU: a callback that plays two ranks holding identical slabs must give the
+    in-process two-slab result bitwise, and match the reference."""
+    import torch
+    from oracle.oracle import padded_stride
+    # global (2, 4, 4, 4): both partitions equal -> slab s twice
+    from oracle.oracle import random_tensor
+    ldims = [4, 4, 4]
+    s = random_tensor(31, ldims)
+    rows = 16
+    dev = torch.from_numpy(np.ascontiguousarray(s.T)).cuda().t()[:rows]
+    calls = []
+
+    def dup(send, recv):  # rank-ordered all-gather of two identical ranks
+        calls.append(send.numel())
+        recv[: send.numel()].copy_(send)
+        recv[send.numel():].copy_(send)
+
+    a = tt.tt_svd_distributed([dev], ldims, (4, 0.0), P_total=2, exchange=dup)
+    b = tt.tt_svd_distributed([dev, dev], ldims, (4, 0.0))
+    assert len(calls) == len(ldims) + 1  # one R exchange per step + the final gather
+    assert a.ranks() == b.ranks()
+    for ca, cb in zip(a.cores, b.cores):
+        assert np.array_equal(ca.data, cb.data)
+    rr, rc = ref.tt_svd_distributed([s, s], ldims, padded_stride(rows), 4)
+    assert a.ranks() == rr
