@@ -61,7 +61,7 @@ struct ttsvd_cu_ctx {
     int64_t launches = 0;
     bool timing = false;
     // grow-only device workspaces
-    DevBuf ws_R, ws_R2, ws_P, ws_A, ws_V, ws_Vacc, ws_U, ws_sigma, ws_flags, ws_work[2], ws_X, ws_send, ws_recv;
+    DevBuf ws_R, ws_R2, ws_P, ws_Scr, ws_A, ws_V, ws_Vacc, ws_U, ws_sigma, ws_flags, ws_work[2], ws_X, ws_send, ws_recv;
     DevBuf host_stage;  // pinned
     cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
 };
@@ -247,6 +247,44 @@ int tsqr_device(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t ld
     if (m > kSmallM) {
         const int M = (m + 31) / 32 * 32;
         const int64_t RS = blk_rsize(M);
+        // tall tiles: one CTA per SM, >= 4 tiles of 128 rows per CTA
+        if (!R_init && n >= (int64_t)4 * kTallRows * 2) {
+            int64_t Gt = std::min<int64_t>(ctx->num_sms, std::max<int64_t>(1, n / (4 * (int64_t)M)));
+            Gt = std::min<int64_t>(Gt, std::max<int64_t>(1, n / (4 * (int64_t)kTallRows)));
+            TT_TRY(ensure(ctx->ws_R, (size_t)Gt * RS * 8));
+            TT_TRY(ensure(ctx->ws_Scr, (size_t)Gt * kTallRows * M * 8));
+            double* parts = as<double>(ctx->ws_R);
+            static bool tattr = false;
+            if (!tattr) {
+                TT_CUDA(cudaFuncSetAttribute(tsqr_tall_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)tall_smem_bytes()));
+                tattr = true;
+            }
+            static const bool prof = std::getenv("TTSVD_PROF_BLK") != nullptr;
+            long long* dprof = nullptr;
+            if (prof) TT_CUDA(cudaMalloc(&dprof, (size_t)Gt * 8 * sizeof(long long)));
+            TallArgs ta{X, n, ld, parts, as<double>(ctx->ws_Scr), m, M, dprof};
+            tsqr_tall_kernel<<<(unsigned)Gt, kTallThreads, tall_smem_bytes(), ctx->stream>>>(ta);
+            TT_TRY(check_launch(ctx, "tsqr_tall_kernel"));
+            if (prof) {
+                std::vector<long long> hp((size_t)Gt * 8);
+                TT_CUDA(cudaMemcpy(hp.data(), dprof, hp.size() * 8, cudaMemcpyDeviceToHost));
+                cudaFree(dprof);
+                double ph[6] = {0, 0, 0, 0, 0, 0};
+                for (int64_t g = 0; g < Gt; ++g)
+                    for (int q = 0; q < 6; ++q) ph[q] += (double)hp[g * 8 + q] / Gt;
+                const double tiles = (double)n / Gt / kTallRows;
+                std::fprintf(stderr, "[tall prof] n=%lld m=%d G=%lld tiles/CTA=%.1f per tile kcyc: load %.1f panel %.1f S %.1f T %.1f trail %.1f\n",
+                             (long long)n, m, (long long)Gt, tiles, ph[0] / tiles / 1e3, ph[1] / tiles / 1e3,
+                             ph[2] / tiles / 1e3, ph[3] / tiles / 1e3, ph[4] / tiles / 1e3);
+            }
+            if (Gt > 1) {
+                TT_TRY(ensure(ctx->ws_P, (size_t)RS * 8));
+                TT_TRY(merge_tree_blk(ctx, parts, Gt, m, M, as<double>(ctx->ws_P)));
+                return copy_leading(ctx, as<double>(ctx->ws_P), M, m, R);
+            }
+            return copy_leading(ctx, parts, M, m, R);
+        }
         int per_sm = 1;
         TT_CUDA(cudaFuncSetAttribute(tsqr_blk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit));
         TT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tsqr_blk_kernel, kBlkThreads, blk_smem_bytes(M)));
@@ -634,7 +672,7 @@ int ttsvd_cu_ctx_destroy(ttsvd_cu_ctx* ctx) {
     if (!ctx) return TTSVD_OK;
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
-    for (DevBuf* b : {&ctx->ws_R, &ctx->ws_R2, &ctx->ws_P, &ctx->ws_A, &ctx->ws_V, &ctx->ws_Vacc, &ctx->ws_U, &ctx->ws_sigma, &ctx->ws_flags, &ctx->ws_work[0],
+    for (DevBuf* b : {&ctx->ws_R, &ctx->ws_R2, &ctx->ws_P, &ctx->ws_Scr, &ctx->ws_A, &ctx->ws_V, &ctx->ws_Vacc, &ctx->ws_U, &ctx->ws_sigma, &ctx->ws_flags, &ctx->ws_work[0],
                       &ctx->ws_work[1], &ctx->ws_X, &ctx->ws_send, &ctx->ws_recv})
         if (b->p) cudaFree(b->p);
     if (ctx->host_stage.p) cudaFreeHost(ctx->host_stage.p);
