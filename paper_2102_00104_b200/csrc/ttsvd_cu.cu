@@ -247,10 +247,14 @@ int tsqr_device(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t ld
     if (m > kSmallM) {
         const int M = (m + 31) / 32 * 32;
         const int64_t RS = blk_rsize(M);
-        // tall tiles: one CTA per SM, >= 4 tiles of 128 rows per CTA
-        if (!R_init && n >= (int64_t)4 * kTallRows * 2) {
-            int64_t Gt = std::min<int64_t>(ctx->num_sms, std::max<int64_t>(1, n / (4 * (int64_t)M)));
-            Gt = std::min<int64_t>(Gt, std::max<int64_t>(1, n / (4 * (int64_t)kTallRows)));
+        // Tall tiles pay off for wide factors (M >= 384: the 32-row tiles of
+        // tsqr_blk_kernel only fit one CTA per SM there); measured on config
+        // 2: 65536x512 41 -> see profiles, 2^20x256 40.4 ms tall vs 36.7 ms blk.
+        // Grid: one CTA per SM, at least 4 tiles of 128 rows per CTA (the
+        // merge tree costs ~M reflector steps per level, so very short row
+        // ranges do not pay).
+        if (!R_init && M >= 384 && n >= (int64_t)4 * kTallRows * 2) {
+            int64_t Gt = std::min<int64_t>(ctx->num_sms, std::max<int64_t>(1, n / (4 * (int64_t)kTallRows)));
             TT_TRY(ensure(ctx->ws_R, (size_t)Gt * RS * 8));
             TT_TRY(ensure(ctx->ws_Scr, (size_t)Gt * kTallRows * M * 8));
             double* parts = as<double>(ctx->ws_R);

@@ -280,7 +280,7 @@ __device__ __forceinline__ void rotate_cols(double* x, double* y, int n, int lan
 }
 
 __device__ __forceinline__ bool jacobi_pair(double* ap, double* aq, int n, double* vp, double* vq, int m, int lane) {
-    constexpr int CH = 8;
+    constexpr int CH = 16;  // n <= 512: every load of the pair in flight at once
     double al = 0.0, be = 0.0, ga = 0.0;
     for (int base = 0; base < n; base += CH * kWarp) {
         double a[CH], b[CH];
@@ -302,9 +302,11 @@ __device__ __forceinline__ bool jacobi_pair(double* ap, double* aq, int n, doubl
     ga = warp_sum(ga);
     const double tol = 1e2 * DBL_EPSILON;
     if (fabs(ga) <= tol * sqrt(al * be)) return false;
-    const double zeta = (be - al) / (2.0 * ga);
-    const double t = ((zeta >= 0.0) ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-    const double c = 1.0 / sqrt(1.0 + t * t);
+    // the reference's rotation (small_svd.hpp:92-96) with correctly rounded
+    // reciprocals / rsqrt instead of divisions (<= 1 ulp apart)
+    const double zeta = (be - al) * __drcp_rn(2.0 * ga);
+    const double t = ((zeta >= 0.0) ? 1.0 : -1.0) * __drcp_rn(fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
+    const double c = rsqrt(fma(t, t, 1.0));
     const double s = c * t;
     rotate_cols<CH>(ap, aq, n, lane, c, s);
     if (vp) rotate_cols<CH>(vp, vq, m, lane, c, s);
