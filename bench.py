@@ -245,6 +245,13 @@ def run_ours(args, rank: int, world: int):
         pk = fp64_peak(dev)
         achieved = flops / (tsqr_ms[dom] * 1e-3) / 1e12
         mp = peaks()
+        traffic = None
+        try:  # DRAM bytes of the same kernel from the committed ncu --set full capture
+            tr = json.load(open(os.path.join(ROOT, "profiles", "r01_traffic.json")))
+            traffic = {"bytes_per_launch": tr["dram_bytes_per_launch"], "kernel": tr["kernel"], "source": tr["source"],
+                       "algorithmic_bytes": 8.0 * n * m}
+        except Exception:
+            pass
         out = {
             "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": max(args.warmup, 3), "ms_per_step": round(ms, 4), "higher_is_better": True,
@@ -261,7 +268,7 @@ def run_ours(args, rank: int, world: int):
                           "step_shapes": [[s.rows, s.cols, s.rank] for s in phase[0]]},
             "roofline": {"kernel": f"K_TSQR step {dom + 1} ({n} x {m}, incl. merge tree)", "bound": "fp64",
                          "achieved": round(achieved, 3), "peak": round(pk["peak_tflops"], 3), "unit": "TFLOP/s",
-                         "frac": round(achieved / pk["peak_tflops"], 4), "traffic": None,
+                         "frac": round(achieved / pk["peak_tflops"], 4), "traffic": traffic,
                          "algorithmic": f"2*n*m^2 = {flops:.4g} flop per launch group",
                          "peak_source": "measured this run (DFMA/DMMA loop probe); MEASURED_PEAKS.json has no fp64",
                          "probe": pk, "hbm_peak_gbs": mp.get("hbm_gbs")},
