@@ -1,0 +1,319 @@
+// K_TSQR for short-fat work matrices (n / m <= 256, m > 32): one cooperative
+// grid factorises the whole n x M matrix with blocked Householder QR (R only)
+// instead of per-CTA flat trees + a merge tree.  For n / m ~ 8..128 the merge
+// tree of the per-CTA path costs log2(G) sequential M-column structured QRs
+// on single CTAs (config 2 step 3: ~26 of 31.6 ms); here every panel is
+// shared by the whole GPU.
+//
+//   CTA c owns rows [c n/G, (c+1) n/G) for the whole factorisation.
+//   Panel p (32 columns): the CTA's rows of the panel sit in shared memory;
+//   reflector j needs the squared norm of column j below the pivot and the
+//   dots with the panel columns right of it — per-CTA partials, one grid
+//   barrier, then every CTA sums the partials in the same fixed order (so all
+//   CTAs compute identical alpha/tau/gamma, deterministically) and updates
+//   its rows.  LAPACK dlarfg normalisation; a zero column under a nonzero
+//   pivot is H = I; an all-zero u gives alpha = sqrt(2 DBL_MIN) (tsqr.hpp:120).
+//   Then T = (diag(1/tau) + striu(Y^T Y))^{-1}, W = Y^T A(:, trail) by split-K
+//   DMMA over the CTAs' rows, W' = T^T W reduced column-chunk-wise, and every
+//   CTA updates its rows A -= Y W' on DMMA.
+//   A is a private copy of the work matrix (the TSMM still needs the original).
+#pragma once
+
+#include <cooperative_groups.h>
+#include <cfloat>
+#include <cstdint>
+
+namespace ttsvd_b200 {
+
+constexpr int kGqrThreads = 256;
+constexpr int kGqrMaxRows = 512;  // rows per CTA (panel rows in shared memory)
+
+struct GqrArgs {
+    double* A;       // n x M, ld lda (column-major), factorised in place
+    int64_t n, lda;
+    int m, M;
+    double* part;    // reduction partials: 2 x G x 33 (reflectors), G x 32 x 32 (S), G x 32 x M (W)
+    double* piv;     // 2 x 32: the pivot row of the current reflector
+    double* Wfin;    // 32 x M: W' = T^T W of the current panel
+};
+
+__host__ __device__ inline int gqr_ldy(int rows) { return ((((rows + 3) & ~3) + 7) & ~7) + 4; }
+
+inline size_t gqr_smem_bytes(int rows_max) {
+    const int ldy = gqr_ldy(rows_max);
+    return ((size_t)32 * ldy + 2 * 32 * 33 + 32 + 8 * 33 + (kGqrThreads / 32) * 32 * 9) * sizeof(double);
+}
+
+__global__ void __launch_bounds__(kGqrThreads, 1) gqr_kernel(GqrArgs a) {
+    namespace cg = cooperative_groups;
+    cg::grid_group grid = cg::this_grid();
+    extern __shared__ __align__(16) double sm[];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int G = gridDim.x, c = blockIdx.x;
+    const int64_t n = a.n, lda = a.lda;
+    const int M = a.M;
+    const int64_t base = n / G, rem = n % G;
+    const int64_t r0 = c * base + (c < rem ? c : rem);
+    const int rows = (int)(base + (c < rem ? 1 : 0));
+    const int rows4 = (rows + 3) & ~3;      // K extent for DMMA (zero padded)
+    const int ldy = gqr_ldy(rows);           // smem ld of the panel rows
+    double* Ys = sm;                         // 32 columns x ldy
+    double* Sm = Ys + 32 * ldy;              // 32 x 33
+    double* Tm = Sm + 32 * 33;               // 32 x 33
+    double* tau = Tm + 32 * 33;              // 32
+    double* red = tau + 32;                  // 8 warps x 33
+    double* Wsc = red + 8 * 33;              // per-warp 32 x 8 (ld 9)
+    double* part = a.part;
+    double* A = a.A;
+    const int lr = lane >> 2, lc = lane & 3;
+
+    for (int p = 0; p < M / 32; ++p) {
+        const int64_t c0 = 32 * (int64_t)p;
+        // ---- stage my rows of the panel ----
+        for (int e = tid; e < 32 * ldy; e += kGqrThreads) {
+            const int k = e / ldy, i = e - k * ldy;
+            Ys[e] = i < rows ? A[(c0 + k) * lda + r0 + i] : 0.0;
+        }
+        __syncthreads();
+        // ---- 32 reflectors, one grid barrier each ----
+        for (int jj = 0; jj < 32; ++jj) {
+            const int64_t j = c0 + jj;
+            const int buf = jj & 1;
+            // partials over my rows below the pivot: v[0] = sum x_j^2, v[k] = sum x_j x_k (k > jj)
+            double v[32];
+#pragma unroll
+            for (int k = 0; k < 32; ++k) v[k] = 0.0;
+            for (int i = tid; i < rows; i += kGqrThreads) {
+                const int64_t gi = r0 + i;
+                if (gi <= j) {
+                    if (gi == j)  // pivot row -> broadcast slot
+                        for (int k = jj; k < 32; ++k) a.piv[buf * 32 + k] = Ys[k * ldy + i];
+                    continue;
+                }
+                const double xj = Ys[jj * ldy + i];
+                v[0] = fma(xj, xj, v[0]);
+#pragma unroll
+                for (int k = 1; k < 32; ++k)
+                    if (k > jj) v[k] = fma(xj, Ys[k * ldy + i], v[k]);
+            }
+            // block reduction of the 32 values: warp butterfly, then warps via smem
+#pragma unroll
+            for (int k = 0; k < 32; ++k) v[k] = warp_sum(v[k]);
+            if (lane == 0)
+#pragma unroll
+                for (int k = 0; k < 32; ++k) red[warp * 33 + k] = v[k];
+            __syncthreads();
+            if (tid < 32) {
+                double t = 0.0;
+                for (int w = 0; w < kGqrThreads / 32; ++w) t += red[w * 33 + tid];
+                part[((int64_t)buf * G + c) * 33 + tid] = t;
+            }
+            __threadfence();
+            grid.sync();
+            // totals in a fixed order (identical on every CTA)
+            if (tid < 32) {
+                double t = 0.0;
+                for (int q = 0; q < G; ++q) t += part[((int64_t)buf * G + q) * 33 + tid];
+                red[tid] = t;
+                red[33 + tid] = a.piv[buf * 32 + tid];
+            }
+            __syncthreads();
+            const double sp = red[0];
+            const double u0 = red[33 + jj];
+            const double nrm2 = u0 * u0 + sp;
+            const double inv = rsqrt(nrm2);
+            const double nr = nrm2 * inv;
+            const double au = fabs(u0);
+            const double sg = (u0 > 0.0) ? 1.0 : -1.0;
+            double alpha = -sg * nr, tj = 1.0 + au * inv, scale = sg * __drcp_rn(au + nr);
+            if (sp == 0.0 && u0 != 0.0) {
+                alpha = u0;
+                tj = 0.0;
+                scale = 0.0;
+            }
+            if (nrm2 == 0.0) {
+                alpha = sqrt(2.0 * DBL_MIN);
+                tj = 2.0;
+                scale = 0.0;
+            }
+            // gamma_k = tau (A(j,k) + scale d_k): column k > jj
+            double gam[32];
+#pragma unroll
+            for (int k = 0; k < 32; ++k) gam[k] = (k > jj) ? tj * (red[33 + k] + scale * red[k]) : 0.0;
+            for (int i = tid; i < rows; i += kGqrThreads) {
+                const int64_t gi = r0 + i;
+                if (gi < j) continue;
+                if (gi == j) {
+#pragma unroll
+                    for (int k = 0; k < 32; ++k)
+                        if (k > jj) Ys[k * ldy + i] -= gam[k];
+                    Ys[jj * ldy + i] = alpha;
+                    continue;
+                }
+                const double xj = Ys[jj * ldy + i];
+                const double f = xj * scale;
+#pragma unroll
+                for (int k = 0; k < 32; ++k)
+                    if (k > jj) Ys[k * ldy + i] = fma(-gam[k], f, Ys[k * ldy + i]);
+                Ys[jj * ldy + i] = f;  // v
+            }
+            if (tid == 0) tau[jj] = tj;
+            __syncthreads();
+        }
+        // ---- write back the panel (R rows and v), then the structured Y in smem ----
+        for (int e = tid; e < 32 * ldy; e += kGqrThreads) {
+            const int k = e / ldy, i = e - k * ldy;
+            if (i < rows) {
+                A[(c0 + k) * lda + r0 + i] = Ys[e];
+                const int64_t gi = r0 + i;
+                Ys[e] = gi > c0 + k ? Ys[e] : (gi == c0 + k ? 1.0 : 0.0);
+            }
+        }
+        __syncthreads();
+        if (c0 + 32 >= M) break;
+        // ---- S = Y^T Y partial (DMMA over my rows), reduce, T ----
+        if (warp < 4) {
+            const int nt = warp;
+            double sacc[4][2];
+#pragma unroll
+            for (int mt = 0; mt < 4; ++mt) sacc[mt][0] = sacc[mt][1] = 0.0;
+            for (int kk = 0; kk < rows4 / 4; ++kk) {
+                const double b = Ys[(8 * nt + lr) * ldy + 4 * kk + lc];
+#pragma unroll
+                for (int mt = 0; mt < 4; ++mt) dmma884(sacc[mt], Ys[(8 * mt + lr) * ldy + 4 * kk + lc], b);
+            }
+            double* ps = part + (int64_t)2 * G * 33 + (int64_t)c * 1024;
+#pragma unroll
+            for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+                for (int e = 0; e < 2; ++e) ps[(8 * mt + lr) * 32 + 8 * nt + 2 * lc + e] = sacc[mt][e];
+        }
+        __threadfence();
+        grid.sync();
+        for (int e = tid; e < 1024; e += kGqrThreads) {
+            double t = 0.0;
+            for (int q = 0; q < G; ++q) t += part[(int64_t)2 * G * 33 + (int64_t)q * 1024 + e];
+            Sm[(e >> 5) * 33 + (e & 31)] = t;
+        }
+        __syncthreads();
+        if (warp == 0) {
+            const int b0 = 8 * (lane >> 3), jx = lane & 7;
+            for (int i = 0; i < 32; ++i) Tm[i * 33 + b0 + jx] = 0.0;
+            Tm[(b0 + jx) * 33 + b0 + jx] = tau[b0 + jx];
+            for (int i = jx - 1; i >= 0; --i) {
+                double acc = 0.0;
+                for (int l = i + 1; l <= jx; ++l) acc += Sm[(b0 + i) * 33 + b0 + l] * Tm[(b0 + l) * 33 + b0 + jx];
+                Tm[(b0 + i) * 33 + b0 + jx] = -tau[b0 + i] * acc;
+            }
+        }
+        __syncthreads();
+        for (int lev = 8; lev <= 16; lev *= 2) {
+            double* Xs = Wsc;
+            const int nblk = 32 / (2 * lev);
+            for (int e = tid; e < nblk * lev * lev; e += kGqrThreads) {
+                const int q = e / (lev * lev), i = (e / lev) % lev, jx = e % lev;
+                const int o = q * 2 * lev;
+                double acc = 0.0;
+                for (int l = 0; l <= jx; ++l) acc += Sm[(o + i) * 33 + o + lev + l] * Tm[(o + lev + l) * 33 + o + lev + jx];
+                Xs[q * 17 * 17 + i * 17 + jx] = acc;
+            }
+            __syncthreads();
+            for (int e = tid; e < nblk * lev * lev; e += kGqrThreads) {
+                const int q = e / (lev * lev), i = (e / lev) % lev, jx = e % lev;
+                const int o = q * 2 * lev;
+                double acc = 0.0;
+                for (int l = i; l < lev; ++l) acc += Tm[(o + i) * 33 + o + l] * Xs[q * 17 * 17 + l * 17 + jx];
+                Tm[(o + i) * 33 + o + lev + jx] = -acc;
+            }
+            __syncthreads();
+        }
+        // ---- W partial = Y_c^T A(rows_c, trail): DMMA, K = my rows ----
+        const int64_t t0 = c0 + 32;
+        const int ngr = (int)((M - t0) / 8);
+        double* pw = part + (int64_t)2 * G * 33 + (int64_t)G * 1024;  // G x 32 x M (cols t0..M used)
+        for (int gq = warp; gq < ngr; gq += kGqrThreads / 32) {
+            const int64_t g = t0 + 8 * gq;
+            double acc[4][2];
+#pragma unroll
+            for (int mt = 0; mt < 4; ++mt) acc[mt][0] = acc[mt][1] = 0.0;
+            const double* colp = A + (g + lr) * lda + r0;
+            for (int kk = 0; kk < rows4 / 4; ++kk) {
+                const int row = 4 * kk + lc;
+                const double b = row < rows ? colp[row] : 0.0;
+#pragma unroll
+                for (int mt = 0; mt < 4; ++mt) dmma884(acc[mt], Ys[(8 * mt + lr) * ldy + 4 * kk + lc], b);
+            }
+#pragma unroll
+            for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+                for (int e = 0; e < 2; ++e) pw[((int64_t)c * 32 + 8 * mt + lr) * M + g + 2 * lc + e] = acc[mt][e];
+        }
+        __threadfence();
+        grid.sync();
+        // ---- reduce W over the CTAs (column chunks), W' = T^T W -> Wfin ----
+        {
+            const int64_t ncols = M - t0;
+            const int64_t chunk = (ncols + G - 1) / G;
+            const int64_t ca = t0 + c * chunk, cb = (ca + chunk < M) ? ca + chunk : M;
+            for (int64_t col = ca + warp; col < cb; col += kGqrThreads / 32) {
+                // lane k: W(k, col) summed over CTAs in order
+                double w = 0.0;
+                for (int q = 0; q < G; ++q) w += pw[((int64_t)q * 32 + lane) * M + col];
+                // W'(i, col) = sum_k T(k, i) W(k, col)
+                double wp = 0.0;
+                for (int k = 0; k < 32; ++k) wp = fma(Tm[k * 33 + lane], __shfl_sync(0xffffffffu, w, k), wp);
+                a.Wfin[(int64_t)lane * M + col] = wp;
+            }
+        }
+        __threadfence();
+        grid.sync();
+        // ---- A(rows_c, trail) -= Y_c W': DMMA per 8-column group, 64-row chunks ----
+        for (int gq = warp; gq < ngr; gq += kGqrThreads / 32) {
+            const int64_t g = t0 + 8 * gq;
+            double* Ws = Wsc + warp * 32 * 9;
+            for (int e = lane; e < 256; e += 32) Ws[(e >> 3) * 9 + (e & 7)] = a.Wfin[(int64_t)(e >> 3) * M + g + (e & 7)];
+            __syncwarp();
+            double wf[8];
+#pragma unroll
+            for (int kk = 0; kk < 8; ++kk) wf[kk] = Ws[(4 * kk + lc) * 9 + lr];
+            for (int rb = 0; rb < rows4; rb += 64) {
+                double cbv[8][2];
+#pragma unroll
+                for (int mt = 0; mt < 8; ++mt)
+#pragma unroll
+                    for (int e = 0; e < 2; ++e) {
+                        const int row = rb + 8 * mt + lr;
+                        cbv[mt][e] = row < rows ? A[(g + 2 * lc + e) * lda + r0 + row] : 0.0;
+                    }
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk)
+#pragma unroll
+                    for (int mt = 0; mt < 8; ++mt) {
+                        const int row = rb + 8 * mt + lr;
+                        const double y = row < ldy ? Ys[(4 * kk + lc) * ldy + row] : 0.0;
+                        dmma884(cbv[mt], -y, wf[kk]);
+                    }
+#pragma unroll
+                for (int mt = 0; mt < 8; ++mt)
+#pragma unroll
+                    for (int e = 0; e < 2; ++e) {
+                        const int row = rb + 8 * mt + lr;
+                        if (row < rows) A[(g + 2 * lc + e) * lda + r0 + row] = cbv[mt][e];
+                    }
+            }
+            __syncwarp();
+        }
+        __threadfence();
+        grid.sync();
+    }
+}
+
+// upper triangle of A(0:m, 0:m) (ld lda) -> R (m x m, ld m)
+__global__ void gqr_extract_kernel(const double* A, int64_t lda, int m, double* R) {
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < m * m; e += gridDim.x * blockDim.x) {
+        const int j = e / m, i = e - j * m;
+        R[e] = i <= j ? A[(int64_t)j * lda + i] : 0.0;
+    }
+}
+
+}  // namespace ttsvd_b200

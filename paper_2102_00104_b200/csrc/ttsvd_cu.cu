@@ -19,6 +19,7 @@
 #include "../../include/ttsvd_cu.h"
 #include "ttsvd_kernels.cuh"
 #include "tsqr_blk.cuh"
+#include "gqr.cuh"
 
 using namespace ttsvd_b200;
 
@@ -61,7 +62,7 @@ struct ttsvd_cu_ctx {
     int64_t launches = 0;
     bool timing = false;
     // grow-only device workspaces
-    DevBuf ws_R, ws_R2, ws_P, ws_Scr, ws_A, ws_V, ws_Vacc, ws_U, ws_sigma, ws_flags, ws_work[2], ws_X, ws_send, ws_recv;
+    DevBuf ws_R, ws_R2, ws_P, ws_Scr, ws_G, ws_Gp, ws_A, ws_V, ws_Vacc, ws_U, ws_sigma, ws_flags, ws_work[2], ws_X, ws_send, ws_recv;
     DevBuf host_stage;  // pinned
     cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
 };
@@ -247,6 +248,38 @@ int tsqr_device(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t ld
     if (m > kSmallM) {
         const int M = (m + 31) / 32 * 32;
         const int64_t RS = blk_rsize(M);
+        // Short-fat (n <= 256 M, n <= 512 rows per SM): one cooperative grid
+        // factorises the whole matrix (gqr.cuh), no merge tree.
+        if (!R_init && n >= M && n <= (int64_t)256 * M && n <= (int64_t)kGqrMaxRows * ctx->num_sms) {
+            int64_t Gq = std::max<int64_t>(1, std::min<int64_t>(ctx->num_sms, n / 128));
+            while ((n + Gq - 1) / Gq > kGqrMaxRows) ++Gq;
+            const int rows_max = (int)((n + Gq - 1) / Gq);
+            const size_t smem = gqr_smem_bytes(rows_max);
+            static bool gattr = false;
+            if (!gattr) {
+                TT_CUDA(cudaFuncSetAttribute(gqr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit));
+                gattr = true;
+            }
+            int per_sm = 0;
+            TT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gqr_kernel, kGqrThreads, smem));
+            if (per_sm >= 1 && Gq <= (int64_t)per_sm * ctx->num_sms) {
+                TT_TRY(ensure(ctx->ws_G, (size_t)n * M * 8));
+                const size_t np = (size_t)2 * Gq * 33 + (size_t)Gq * 1024 + (size_t)Gq * 32 * M;
+                TT_TRY(ensure(ctx->ws_Gp, (np + 64 + (size_t)32 * M) * 8));
+                double* Aw = as<double>(ctx->ws_G);
+                TT_CUDA(cudaMemcpy2DAsync(Aw, (size_t)n * 8, X, (size_t)ld * 8, (size_t)n * 8, m, cudaMemcpyDeviceToDevice,
+                                          ctx->stream));
+                if (M > m) TT_CUDA(cudaMemsetAsync(Aw + (size_t)n * m, 0, (size_t)n * (M - m) * 8, ctx->stream));
+                double* pp = as<double>(ctx->ws_Gp);
+                GqrArgs ga{Aw, n, n, m, M, pp, pp + np, pp + np + 64};
+                void* args[] = {&ga};
+                TT_CUDA(cudaLaunchCooperativeKernel((const void*)gqr_kernel, dim3((unsigned)Gq), dim3(kGqrThreads), args,
+                                                    smem, ctx->stream));
+                TT_TRY(check_launch(ctx, "gqr_kernel"));
+                gqr_extract_kernel<<<std::max(1, std::min(1024, (m * m + 255) / 256)), 256, 0, ctx->stream>>>(Aw, n, m, R);
+                return check_launch(ctx, "gqr_extract_kernel");
+            }
+        }
         // Tall tiles pay off for wide factors (M >= 384: the 32-row tiles of
         // tsqr_blk_kernel only fit one CTA per SM there); measured on config
         // 2: 65536x512 41 -> see profiles, 2^20x256 40.4 ms tall vs 36.7 ms blk.
@@ -676,7 +709,7 @@ int ttsvd_cu_ctx_destroy(ttsvd_cu_ctx* ctx) {
     if (!ctx) return TTSVD_OK;
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
-    for (DevBuf* b : {&ctx->ws_R, &ctx->ws_R2, &ctx->ws_P, &ctx->ws_Scr, &ctx->ws_A, &ctx->ws_V, &ctx->ws_Vacc, &ctx->ws_U, &ctx->ws_sigma, &ctx->ws_flags, &ctx->ws_work[0],
+    for (DevBuf* b : {&ctx->ws_R, &ctx->ws_R2, &ctx->ws_P, &ctx->ws_Scr, &ctx->ws_G, &ctx->ws_Gp, &ctx->ws_A, &ctx->ws_V, &ctx->ws_Vacc, &ctx->ws_U, &ctx->ws_sigma, &ctx->ws_flags, &ctx->ws_work[0],
                       &ctx->ws_work[1], &ctx->ws_X, &ctx->ws_send, &ctx->ws_recv})
         if (b->p) cudaFree(b->p);
     if (ctx->host_stage.p) cudaFreeHost(ctx->host_stage.p);
