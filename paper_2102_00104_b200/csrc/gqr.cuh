@@ -308,6 +308,20 @@ __global__ void __launch_bounds__(kGqrThreads, 1) gqr_kernel(GqrArgs a) {
     }
 }
 
+// count packed panel-major factors (blk_rsize(M) each) -> the dense stacked
+// matrix S (count*M x M, ld count*M): rows [q M, (q+1) M) hold factor q
+// (zeros below its diagonal)
+__global__ void stack_packed_kernel(const double* parts, int64_t count, int M, double* S) {
+    const int64_t RS = blk_rsize(M), ld = count * M;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < ld * M; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t col = e / ld, row = e - col * ld;
+        const int64_t q = row / M;
+        const int i = (int)(row - q * M), j = (int)col;
+        const int p = i >> 5;
+        S[e] = (i <= j) ? parts[q * RS + blk_roff(p, M) + (int64_t)(j - 32 * p) * 32 + (i & 31)] : 0.0;
+    }
+}
+
 // upper triangle of A(0:m, 0:m) (ld lda) -> R (m x m, ld m)
 __global__ void gqr_extract_kernel(const double* A, int64_t lda, int m, double* R) {
     for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < m * m; e += gridDim.x * blockDim.x) {

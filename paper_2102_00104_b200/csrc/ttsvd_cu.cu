@@ -206,6 +206,8 @@ int pack_parts(ttsvd_cu_ctx* ctx, const double* parts, int64_t P, int m, int M, 
     return check_launch(ctx, "pack_parts_kernel");
 }
 
+int gqr_device(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t ld, double* R);
+
 // Fixed index-ordered merge tree over `count` parts (each m x m, ld m); the
 // result lands in R_final.  Level l pairs (2i, 2i+1); an odd tail is carried.
 int merge_tree(ttsvd_cu_ctx* ctx, double* parts, int64_t count, int m, double* R_final) {
@@ -216,6 +218,18 @@ int merge_tree(ttsvd_cu_ctx* ctx, double* parts, int64_t count, int m, double* R
     if (m > kSmallM) {
         const int M = (m + 31) / 32 * 32;
         const int64_t RS = blk_rsize(M);
+        if (count >= 4 && count * m >= M && count * m <= (int64_t)kGqrMaxRows * ctx->num_sms) {
+            // one cooperative QR of the stacked factors (rows q*m .. q*m+m-1 = part q)
+            const int64_t ns = count * m;
+            TT_TRY(ensure(ctx->ws_G, (size_t)ns * M * 8));
+            double* Aw = as<double>(ctx->ws_G);
+            if (M > m) TT_CUDA(cudaMemsetAsync(Aw + (size_t)ns * m, 0, (size_t)ns * (M - m) * 8, ctx->stream));
+            for (int64_t q = 0; q < count; ++q)
+                TT_CUDA(cudaMemcpy2DAsync(Aw + q * m, (size_t)ns * 8, parts + q * m * m, (size_t)m * 8, (size_t)m * 8, m,
+                                          cudaMemcpyDeviceToDevice, ctx->stream));
+            const int rc = gqr_device(ctx, Aw, ns, m, ns, R_final);
+            if (rc != -1) return rc;
+        }
         TT_TRY(ensure(ctx->ws_P, (size_t)(count + 1) * RS * 8));
         double* P = as<double>(ctx->ws_P);
         TT_TRY(pack_parts(ctx, parts, count, m, M, P));
@@ -240,6 +254,56 @@ int merge_tree(ttsvd_cu_ctx* ctx, double* parts, int64_t count, int m, double* R
     return TTSVD_OK;
 }
 
+// Cooperative whole-grid blocked QR (gqr.cuh) of X (n x m, ld): R (m x m).
+// Returns -1 when the shape does not fit one co-resident grid.
+int gqr_device(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t ld, double* R) {
+    const int M = (m + 31) / 32 * 32;
+    if (n < M || n > (int64_t)kGqrMaxRows * ctx->num_sms) return -1;
+    int64_t Gq = std::max<int64_t>(1, std::min<int64_t>(ctx->num_sms, n / 128));
+    while ((n + Gq - 1) / Gq > kGqrMaxRows) ++Gq;
+    const int rows_max = (int)((n + Gq - 1) / Gq);
+    const size_t smem = gqr_smem_bytes(rows_max);
+    static bool gattr = false;
+    if (!gattr) {
+        TT_CUDA(cudaFuncSetAttribute(gqr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit));
+        gattr = true;
+    }
+    int per_sm = 0;
+    TT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gqr_kernel, kGqrThreads, smem));
+    if (per_sm < 1 || Gq > (int64_t)per_sm * ctx->num_sms) return -1;
+    TT_TRY(ensure(ctx->ws_G, (size_t)n * M * 8));
+    const size_t np = (size_t)2 * Gq * 33 + (size_t)Gq * 1024 + (size_t)Gq * 32 * M;
+    TT_TRY(ensure(ctx->ws_Gp, (np + 64 + (size_t)32 * M) * 8));
+    double* Aw = as<double>(ctx->ws_G);
+    if (X != Aw) {
+        TT_CUDA(cudaMemcpy2DAsync(Aw, (size_t)n * 8, X, (size_t)ld * 8, (size_t)n * 8, m, cudaMemcpyDeviceToDevice,
+                                  ctx->stream));
+        if (M > m) TT_CUDA(cudaMemsetAsync(Aw + (size_t)n * m, 0, (size_t)n * (M - m) * 8, ctx->stream));
+    }
+    double* pp = as<double>(ctx->ws_Gp);
+    GqrArgs ga{Aw, n, n, m, M, pp, pp + np, pp + np + 64};
+    void* args[] = {&ga};
+    TT_CUDA(cudaLaunchCooperativeKernel((const void*)gqr_kernel, dim3((unsigned)Gq), dim3(kGqrThreads), args, smem,
+                                        ctx->stream));
+    TT_TRY(check_launch(ctx, "gqr_kernel"));
+    gqr_extract_kernel<<<std::max(1, std::min(1024, (m * m + 255) / 256)), 256, 0, ctx->stream>>>(Aw, n, m, R);
+    return check_launch(ctx, "gqr_extract_kernel");
+}
+
+// Merge of `count` packed factors by one cooperative QR of their stack
+// (replaces log2(count) levels of single-CTA merges).  -1 if it does not fit.
+int merge_stack_gqr(ttsvd_cu_ctx* ctx, const double* parts, int64_t count, int m, int M, double* R) {
+    const int64_t n = count * M;
+    if (count < 4 || n > (int64_t)kGqrMaxRows * ctx->num_sms) return -1;
+    TT_TRY(ensure(ctx->ws_G, (size_t)n * M * 8));
+    double* Aw = as<double>(ctx->ws_G);
+    const int64_t tot = n * M;
+    stack_packed_kernel<<<(unsigned)std::min<int64_t>((tot + 255) / 256, 8192), 256, 0, ctx->stream>>>(parts, count, M,
+                                                                                                    Aw);
+    TT_TRY(check_launch(ctx, "stack_packed_kernel"));
+    return gqr_device(ctx, Aw, n, m, n, R);
+}
+
 // R (m x m) of X (n x m, ld) — n may be smaller than m (the structured kernel
 // does not need n >= m; gram_triangular's square padding is implicit).
 // R_init (m x m) optionally seeds a single job (reduce_block).
@@ -250,35 +314,9 @@ int tsqr_device(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t ld
         const int64_t RS = blk_rsize(M);
         // Short-fat (n <= 256 M, n <= 512 rows per SM): one cooperative grid
         // factorises the whole matrix (gqr.cuh), no merge tree.
-        if (!R_init && n >= M && n <= (int64_t)256 * M && n <= (int64_t)kGqrMaxRows * ctx->num_sms) {
-            int64_t Gq = std::max<int64_t>(1, std::min<int64_t>(ctx->num_sms, n / 128));
-            while ((n + Gq - 1) / Gq > kGqrMaxRows) ++Gq;
-            const int rows_max = (int)((n + Gq - 1) / Gq);
-            const size_t smem = gqr_smem_bytes(rows_max);
-            static bool gattr = false;
-            if (!gattr) {
-                TT_CUDA(cudaFuncSetAttribute(gqr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit));
-                gattr = true;
-            }
-            int per_sm = 0;
-            TT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gqr_kernel, kGqrThreads, smem));
-            if (per_sm >= 1 && Gq <= (int64_t)per_sm * ctx->num_sms) {
-                TT_TRY(ensure(ctx->ws_G, (size_t)n * M * 8));
-                const size_t np = (size_t)2 * Gq * 33 + (size_t)Gq * 1024 + (size_t)Gq * 32 * M;
-                TT_TRY(ensure(ctx->ws_Gp, (np + 64 + (size_t)32 * M) * 8));
-                double* Aw = as<double>(ctx->ws_G);
-                TT_CUDA(cudaMemcpy2DAsync(Aw, (size_t)n * 8, X, (size_t)ld * 8, (size_t)n * 8, m, cudaMemcpyDeviceToDevice,
-                                          ctx->stream));
-                if (M > m) TT_CUDA(cudaMemsetAsync(Aw + (size_t)n * m, 0, (size_t)n * (M - m) * 8, ctx->stream));
-                double* pp = as<double>(ctx->ws_Gp);
-                GqrArgs ga{Aw, n, n, m, M, pp, pp + np, pp + np + 64};
-                void* args[] = {&ga};
-                TT_CUDA(cudaLaunchCooperativeKernel((const void*)gqr_kernel, dim3((unsigned)Gq), dim3(kGqrThreads), args,
-                                                    smem, ctx->stream));
-                TT_TRY(check_launch(ctx, "gqr_kernel"));
-                gqr_extract_kernel<<<std::max(1, std::min(1024, (m * m + 255) / 256)), 256, 0, ctx->stream>>>(Aw, n, m, R);
-                return check_launch(ctx, "gqr_extract_kernel");
-            }
+        if (!R_init && n >= M && n <= (int64_t)256 * M) {
+            const int rc = gqr_device(ctx, X, n, m, ld, R);
+            if (rc != -1) return rc;
         }
         // Tall tiles pay off for wide factors (M >= 384: the 32-row tiles of
         // tsqr_blk_kernel only fit one CTA per SM there); measured on config
@@ -316,6 +354,8 @@ int tsqr_device(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t ld
                              ph[2] / tiles / 1e3, ph[3] / tiles / 1e3, ph[4] / tiles / 1e3);
             }
             if (Gt > 1) {
+                const int rc = merge_stack_gqr(ctx, parts, Gt, m, M, R);
+                if (rc != -1) return rc;
                 TT_TRY(ensure(ctx->ws_P, (size_t)RS * 8));
                 TT_TRY(merge_tree_blk(ctx, parts, Gt, m, M, as<double>(ctx->ws_P)));
                 return copy_leading(ctx, as<double>(ctx->ws_P), M, m, R);
@@ -355,6 +395,8 @@ int tsqr_device(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t ld
                          ph[0] / tiles / 1e3, ph[1] / tiles / 1e3, ph[2] / tiles / 1e3, ph[3] / tiles / 1e3, ph[4] / tiles / 1e3);
         }
         if (G > 1) {
+            const int rc = merge_stack_gqr(ctx, parts, G, m, M, R);
+            if (rc != -1) return rc;
             TT_TRY(ensure(ctx->ws_P, (size_t)RS * 8));
             TT_TRY(merge_tree_blk(ctx, parts, G, m, M, as<double>(ctx->ws_P)));
             return copy_leading(ctx, as<double>(ctx->ws_P), M, m, R);
