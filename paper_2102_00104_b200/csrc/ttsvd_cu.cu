@@ -20,6 +20,7 @@
 #include "ttsvd_kernels.cuh"
 #include "tsqr_blk.cuh"
 #include "gqr.cuh"
+#include "jacobi_blk.cuh"
 
 using namespace ttsvd_b200;
 
@@ -429,13 +430,62 @@ constexpr int kJacobiSmemThreads = 512;
 
 // One-sided Jacobi on A (n x m, ld n, device, overwritten).  With Vacc the
 // rotations are accumulated.  Returns sweeps used via *sweeps.
+// Cluster-resident block Jacobi (no accumulation, jacobi_blk.cuh).
+int jacobi_bj(ttsvd_cu_ctx* ctx, double* A, int n, int m, int* status, bool* launched) {
+    *launched = false;
+    const int n8 = (n + 7) / 8 * 8;
+    const int ldc = bj_ldc(n8);
+    const int nblk = (m + 3) / 4;
+    const int C = (nblk + 2 * kBjSlots - 1) / (2 * kBjSlots);
+    const size_t smem = bj_smem_bytes(ldc);
+    static int static_smem = -1;
+    if (static_smem < 0) {
+        cudaFuncAttributes fa;
+        TT_CUDA(cudaFuncGetAttributes(&fa, jacobi_bj_kernel));
+        static_smem = (int)fa.sharedSizeBytes;
+        TT_CUDA(cudaFuncSetAttribute(jacobi_bj_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        TT_CUDA(cudaFuncSetAttribute(jacobi_bj_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     kSmemLimit - static_smem));
+    }
+    if (C > 16 || smem > (size_t)(kSmemLimit - static_smem)) return TTSVD_OK;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(C);
+    cfg.blockDim = dim3(kBjThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = ctx->stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = C;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int ncl = 0;
+    if (cudaOccupancyMaxActiveClusters(&ncl, jacobi_bj_kernel, &cfg) != cudaSuccess || ncl < 1) {
+        (void)cudaGetLastError();
+        return TTSVD_OK;
+    }
+    BjArgs ba{A, n, m, n8, ldc, C, status, 30};
+    TT_CUDA(cudaLaunchKernelEx(&cfg, jacobi_bj_kernel, ba));
+    TT_TRY(check_launch(ctx, "jacobi_bj_kernel"));
+    *launched = true;
+    return TTSVD_OK;
+}
+
 int jacobi_device(ttsvd_cu_ctx* ctx, double* A, int n, int m, double* Vacc) {
     TT_TRY(ensure(ctx->ws_flags, 64 * sizeof(int)));
     int* flags = as<int>(ctx->ws_flags);
     TT_CUDA(cudaMemsetAsync(flags, 0, 64 * sizeof(int), ctx->stream));
     JacobiArgs a{A, Vacc, n, m, flags, flags + 40, 30};
     const size_t smem = ((size_t)n * m + (Vacc ? (size_t)m * m : 0)) * 8;
-    if (smem <= 220 * 1024) {
+    static const char* jsel = std::getenv("TTSVD_JACOBI");  // diagnostics: "smem", "bj", "coop"
+    const std::string sel = jsel ? jsel : "";
+    if (!Vacc && m >= 96 && (sel.empty() || sel == "bj")) {
+        bool launched = false;
+        TT_TRY(jacobi_bj(ctx, A, n, m, flags + 40, &launched));
+        if (launched) return TTSVD_OK;
+    }
+    if (smem <= 220 * 1024 && (sel.empty() || sel == "smem" || sel == "bj")) {
         static bool attr = false;
         if (!attr) {
             TT_CUDA(cudaFuncSetAttribute(jacobi_smem_kernel<kJacobiSmemThreads>,
@@ -444,7 +494,9 @@ int jacobi_device(ttsvd_cu_ctx* ctx, double* A, int n, int m, double* Vacc) {
         }
         jacobi_smem_kernel<kJacobiSmemThreads><<<1, kJacobiSmemThreads, smem, ctx->stream>>>(a);
         TT_TRY(check_launch(ctx, "jacobi_smem_kernel"));
-    } else {
+        return TTSVD_OK;
+    }
+    {
         const int warps_per = kJacobiThreads / 32;
         int grid = (m / 2 + warps_per - 1) / warps_per;
         grid = std::max(1, std::min(grid, ctx->coop_max_blocks));
