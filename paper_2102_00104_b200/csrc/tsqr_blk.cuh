@@ -44,6 +44,7 @@ struct BlkArgs {
     int M;                  // padded columns (multiple of 32)
     int mode;
     long long* prof;        // optional per-CTA phase cycle counters (8 per CTA), diagnostics
+    int dbg = 0;            // diagnostics only (timing experiments): bit 0 skip trailing, bit 1 skip phase A
 };
 
 __device__ __forceinline__ void dmma884(double (&d)[2], double a, double b) {

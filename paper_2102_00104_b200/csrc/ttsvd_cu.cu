@@ -21,6 +21,7 @@
 #include "tsqr_blk.cuh"
 #include "gqr.cuh"
 #include "jacobi_blk.cuh"
+#include "tsqr_la.cuh"
 
 using namespace ttsvd_b200;
 
@@ -161,14 +162,36 @@ int launch_tsqr_kernel(ttsvd_cu_ctx* ctx, const TsqrArgs& a, int grid, size_t sm
 // ---- blocked DMMA path (m > 32) ----
 constexpr int kSmallM = 32;
 
+bool use_old_blk() {
+    static const char* t = std::getenv("TTSVD_TSQR");  // diagnostics: "blk" = the non-look-ahead kernel
+    return t && std::string(t) == "blk";
+}
+
+int set_la_attr() {
+    static int done = 0;
+    if (!done) {
+        cudaFuncAttributes fa;
+        TT_CUDA(cudaFuncGetAttributes(&fa, tsqr_la_kernel));
+        TT_CUDA(cudaFuncSetAttribute(tsqr_la_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     kSmemLimit - (int)fa.sharedSizeBytes));
+        done = 1;
+    }
+    return TTSVD_OK;
+}
+
 int launch_blk(ttsvd_cu_ctx* ctx, const BlkArgs& a, int grid) {
     static bool attr_set = false;
     if (!attr_set) {
         TT_CUDA(cudaFuncSetAttribute(tsqr_blk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit));
+        TT_TRY(set_la_attr());
         attr_set = true;
     }
-    tsqr_blk_kernel<<<grid, kBlkThreads, blk_smem_bytes(a.M), ctx->stream>>>(a);
-    return check_launch(ctx, "tsqr_blk_kernel");
+    if (use_old_blk()) {
+        tsqr_blk_kernel<<<grid, kBlkThreads, blk_smem_bytes(a.M), ctx->stream>>>(a);
+        return check_launch(ctx, "tsqr_blk_kernel");
+    }
+    tsqr_la_kernel<<<grid, kLaThreads, la_smem_bytes(a.M), ctx->stream>>>(a);
+    return check_launch(ctx, "tsqr_la_kernel");
 }
 
 int copy_leading(ttsvd_cu_ctx* ctx, const double* Rws, int M, int m, double* R) {
@@ -325,7 +348,9 @@ int tsqr_device(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t ld
         // Grid: one CTA per SM, at least 4 tiles of 128 rows per CTA (the
         // merge tree costs ~M reflector steps per level, so very short row
         // ranges do not pay).
-        if (!R_init && M >= 384 && n >= (int64_t)4 * kTallRows * 2) {
+        static const char* tsel = std::getenv("TTSVD_TSQR");  // diagnostics: "tall", "blk"
+        const bool want_tall = tsel ? std::string(tsel) == "tall" : false;
+        if (!R_init && want_tall && n >= (int64_t)4 * kTallRows * 2) {
             int64_t Gt = std::min<int64_t>(ctx->num_sms, std::max<int64_t>(1, n / (4 * (int64_t)kTallRows)));
             TT_TRY(ensure(ctx->ws_R, (size_t)Gt * RS * 8));
             TT_TRY(ensure(ctx->ws_Scr, (size_t)Gt * kTallRows * M * 8));
@@ -365,7 +390,11 @@ int tsqr_device(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t ld
         }
         int per_sm = 1;
         TT_CUDA(cudaFuncSetAttribute(tsqr_blk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit));
-        TT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tsqr_blk_kernel, kBlkThreads, blk_smem_bytes(M)));
+        TT_TRY(set_la_attr());
+        if (use_old_blk())
+            TT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tsqr_blk_kernel, kBlkThreads, blk_smem_bytes(M)));
+        else
+            TT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tsqr_la_kernel, kLaThreads, la_smem_bytes(M)));
         per_sm = std::max(1, per_sm);
         int64_t G = std::max<int64_t>(1, n / (4 * (int64_t)M));
         G = std::min<int64_t>(G, (int64_t)per_sm * ctx->num_sms);
@@ -378,6 +407,8 @@ int tsqr_device(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t ld
             TT_TRY(pack_parts(ctx, R_init, 1, m, M, Rinit_ws));
         }
         BlkArgs a{X, n, ld, parts, Rinit_ws, m, M, 0, nullptr};
+        static const char* dbg = std::getenv("TTSVD_BLK_DBG");  // diagnostics only: wrong results by design
+        a.dbg = dbg ? std::atoi(dbg) : 0;
         static const bool prof = std::getenv("TTSVD_PROF_BLK") != nullptr;
         long long* dprof = nullptr;
         if (prof) TT_CUDA(cudaMalloc(&dprof, (size_t)G * 8 * sizeof(long long)));
@@ -387,13 +418,13 @@ int tsqr_device(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t ld
             std::vector<long long> hp((size_t)G * 8);
             TT_CUDA(cudaMemcpy(hp.data(), dprof, hp.size() * 8, cudaMemcpyDeviceToHost));
             cudaFree(dprof);
-            double ph[6] = {0, 0, 0, 0, 0, 0};
+            double ph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
             for (int64_t g = 0; g < G; ++g)
-                for (int q = 0; q < 6; ++q) ph[q] += (double)hp[g * 8 + q] / G;
+                for (int q = 0; q < 8; ++q) ph[q] += (double)hp[g * 8 + q] / G;
             const double tiles = (double)n / G / 32.0;
-            std::fprintf(stderr, "[blk prof] n=%lld m=%d G=%lld tiles/CTA=%.1f  Mcyc/CTA: load %.2f panel %.2f S %.2f T %.2f trail %.2f | per tile kcyc: %.1f %.1f %.1f %.1f %.1f\n",
-                         (long long)n, m, (long long)G, tiles, ph[0] / 1e6, ph[1] / 1e6, ph[2] / 1e6, ph[3] / 1e6, ph[4] / 1e6,
-                         ph[0] / tiles / 1e3, ph[1] / tiles / 1e3, ph[2] / tiles / 1e3, ph[3] / tiles / 1e3, ph[4] / tiles / 1e3);
+            std::fprintf(stderr, "[blk prof] n=%lld m=%d G=%lld tiles/CTA=%.1f per tile kcyc (la: load, wait-A, panel, T, end-sync, start, prologue panel, prologue T): %.1f %.1f %.1f %.1f %.1f %.1f %.1f %.1f\n",
+                         (long long)n, m, (long long)G, tiles, ph[0] / tiles / 1e3, ph[1] / tiles / 1e3, ph[2] / tiles / 1e3,
+                         ph[3] / tiles / 1e3, ph[4] / tiles / 1e3, ph[5] / tiles / 1e3, ph[6] / tiles / 1e3, ph[7] / tiles / 1e3);
         }
         if (G > 1) {
             const int rc = merge_stack_gqr(ctx, parts, G, m, M, R);
