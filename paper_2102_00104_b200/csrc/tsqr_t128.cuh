@@ -1,0 +1,324 @@
+// K_TSQR (m > 32), 128-row tiles, one CTA (16 warps) per SM.
+//
+// Same job structure and packed R workspace as tsqr_la_kernel, but each tile
+// [R; B] has 128 rows, so the serial reflector chain of a panel is paid once
+// per 128 rows instead of once per 32:
+//   * warps 0..3 (one per SM sub-partition) factor the panel together: warp k
+//     keeps tile rows 32k..32k+31 of the 32 panel columns in registers (lane =
+//     column); per reflector the four partial dot products meet through
+//     shared memory and one 128-thread named barrier; every panel warp then
+//     derives the same reflector (LAPACK dlarfg normalisation and the
+//     reference's zero rules, tsqr.hpp:120-160) and updates its rows;
+//   * warps 4..7 first apply panel p's block reflector to panel p+1's columns
+//     ("phase A", DMMA, result straight into the next panel buffer), then all
+//     twelve update warps apply it to the remaining columns while warps 0..3
+//     factor panel p+1;
+//   * the tile's trailing columns live in a per-CTA scratch in global memory
+//     (L2 resident, 128 x M doubles); panel 0 and the first trailing update of
+//     a tile read the input directly.
+// T of the compact WY form is built from S = V^T V, which falls out of the
+// panel's dot products (see la_panel).
+#pragma once
+
+#include <cfloat>
+#include <cstdint>
+
+namespace ttsvd_b200 {
+
+constexpr int kT2Rows = 128;
+constexpr int kT2Threads = 512;
+constexpr int kT2Pld = 132;  // smem ld of a panel buffer (128 rows + 4)
+
+struct T2Args {
+    const double* X;
+    int64_t n, ld;
+    double* Rws;  // per-CTA packed R (blk_rsize(M))
+    double* Scr;  // per-CTA tile scratch (kT2Rows x M, ld kT2Rows)
+    int m, M;
+};
+
+inline size_t t2_smem_bytes() {
+    return ((size_t)2 * 32 * kT2Pld + 32 * kLaRld + 32 * kTld + 2 * 32 * kLaTld + 32 + 4 * 32 + 2 * 4 * 32) *
+           sizeof(double);
+}
+
+__device__ __forceinline__ void t2_bar_panel() { asm volatile("bar.sync 2, 128;" ::: "memory"); }
+
+// panel warps 0..3: factor the 128 x 32 panel in P (ld kT2Pld) against the
+// diagonal R block Rp; leaves V in P, the new block in Rp, tau, striu(S) in Sm.
+__device__ __forceinline__ void t2_panel(double* P, double* Rp, double* tau, double* pvall, double* dpart, double* Sm,
+                                         int warp, int lane) {
+    double* pv = pvall + 32 * warp;
+    double x[32];
+#pragma unroll
+    for (int i = 0; i < 32; i += 2) {
+        const double2 t = *reinterpret_cast<const double2*>(P + lane * kT2Pld + 32 * warp + i);
+        x[i] = t.x;
+        x[i + 1] = t.y;
+    }
+    const unsigned s_pv = (unsigned)__cvta_generic_to_shared(pv);
+    const unsigned s_rcol = (unsigned)__cvta_generic_to_shared(Rp + lane * kLaRld);
+    const unsigned s_scol = (unsigned)__cvta_generic_to_shared(Sm + lane * kTld);
+    const unsigned s_dp = (unsigned)__cvta_generic_to_shared(dpart);
+    const unsigned s_rp = (unsigned)__cvta_generic_to_shared(Rp);
+    const unsigned s_tau = (unsigned)__cvta_generic_to_shared(tau);
+    const bool w0 = (warp == 0);
+    double my_scale = 1.0;
+    // warp 0 writes row j of the R block one reflector late (the other panel
+    // warps may still be reading it)
+    double pend_r = 0.0, pend_alpha = 0.0, pend_tau = 0.0;
+    bool pend_upd = false;
+    int pend_j = -1;
+#pragma unroll 1
+    for (int j = 0; j < 32; ++j) {
+        const int par = j & 1;
+        const bool piv = (lane == j);
+#pragma unroll
+        for (int i = 0; i < 32; i += 2) sts2_if(piv, s_pv + 8 * i, x[i], x[i + 1]);
+        __syncwarp();
+        double a[8];
+#pragma unroll
+        for (int i = 0; i < 32; i += 2) {
+            const double2 p0 = lds2(s_pv + 8 * i);
+            if (i < 16) {
+                a[i / 2] = p0.x * x[i];
+                a[i / 2] = fma(p0.y, x[i + 1], a[i / 2]);
+            } else {
+                a[(i - 16) / 2] = fma(p0.x, x[i], a[(i - 16) / 2]);
+                a[(i - 16) / 2] = fma(p0.y, x[i + 1], a[(i - 16) / 2]);
+            }
+        }
+        const double dk = ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
+        sts1_if(true, s_dp + 8 * (par * 128 + warp * 32 + lane), dk);
+        t2_bar_panel();
+        if (w0 && pend_j >= 0) {  // everyone is past reflector j-1: publish its R row
+            sts1_if(pend_upd, s_rcol + 8 * pend_j, pend_r);
+            sts1_if(lane == pend_j, s_rp + 8 * pend_j * (kLaRld + 1), pend_alpha);
+            sts1_if(lane == pend_j, s_tau + 8 * pend_j, pend_tau);
+        }
+        const double d = (lds1(s_dp + 8 * (par * 128 + lane)) + lds1(s_dp + 8 * (par * 128 + 32 + lane))) +
+                         (lds1(s_dp + 8 * (par * 128 + 64 + lane)) + lds1(s_dp + 8 * (par * 128 + 96 + lane)));
+        const double sp = (lds1(s_dp + 8 * (par * 128 + j)) + lds1(s_dp + 8 * (par * 128 + 32 + j))) +
+                          (lds1(s_dp + 8 * (par * 128 + 64 + j)) + lds1(s_dp + 8 * (par * 128 + 96 + j)));
+        const double u0 = lds1(s_rp + 8 * j * (kLaRld + 1));
+        const double rjc = lds1(s_rcol + 8 * j);
+        const double nrm2 = u0 * u0 + sp;
+        const double inv = rsqrt(nrm2);
+        const double nr = nrm2 * inv;
+        const double au = fabs(u0);
+        const double sg = (u0 > 0.0) ? 1.0 : -1.0;
+        double alpha = -sg * nr;
+        double tj = 1.0 + au * inv;
+        double scale = sg * __drcp_rn(au + nr);
+        if (sp == 0.0 && u0 != 0.0) {  // H = I
+            alpha = u0;
+            tj = 0.0;
+            scale = 0.0;
+        }
+        if (nrm2 == 0.0) {  // all-zero u
+            alpha = sqrt(2.0 * DBL_MIN);
+            tj = 2.0;
+            scale = 0.0;
+        }
+        const bool upd = lane > j;
+        const double g = tj * (rjc + scale * d);
+        const double f = upd ? g * scale : 0.0;
+        my_scale = piv ? scale : my_scale;
+        if (w0) {
+            sts1_if(lane < j, s_scol + 8 * j, my_scale * scale * d);  // S(c, j) = v_c . v_j
+            pend_r = rjc - g;
+            pend_upd = upd;
+            pend_alpha = alpha;
+            pend_tau = tj;
+            pend_j = j;
+        }
+#pragma unroll
+        for (int i = 0; i < 32; i += 2) {
+            const double2 p0 = lds2(s_pv + 8 * i);
+            x[i] = fma(-f, p0.x, x[i]);
+            x[i + 1] = fma(-f, p0.y, x[i + 1]);
+        }
+        __syncwarp();
+    }
+    t2_bar_panel();
+    if (w0) {
+        sts1_if(pend_upd, s_rcol + 8 * pend_j, pend_r);
+        sts1_if(lane == pend_j, s_rp + 8 * pend_j * (kLaRld + 1), pend_alpha);
+        sts1_if(lane == pend_j, s_tau + 8 * pend_j, pend_tau);
+    }
+#pragma unroll
+    for (int i = 0; i < 32; i += 2)
+        *reinterpret_cast<double2*>(P + lane * kT2Pld + 32 * warp + i) = make_double2(my_scale * x[i], my_scale * x[i + 1]);
+    t2_bar_panel();
+}
+
+// one warp: apply panel p's block reflector (V: 128 x 32 in smem, ld kT2Pld;
+// T) to tile columns g..g+7 (source: input X or the scratch; destination:
+// scratch or a panel buffer) and to R(p, g..g+7).
+//   W^T = R(p, c)^T + B(:, c)^T V;  W'^T = W^T T;  R(p, c) -= W';  B(:, c) -= V W'.
+template <bool SRC_X, bool DST_SMEM>
+__device__ __forceinline__ void t2_group(const double* src, int64_t lds, int rows, int mcols, double* dst, int64_t ldd,
+                                         const double* V, const double* Tm, double* Rrow, int c0, int g, int gd,
+                                         int lane, uint64_t pol_x, uint64_t pol_r) {
+    const int r = lane >> 2, q = lane & 3;
+    double* Rc = Rrow + (int64_t)(g + r - c0) * 32;
+    double acc[4][2], rsav[4][2];
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt) {
+        rsav[nt][0] = ld_hint(Rc + 8 * nt + 2 * q, pol_r);
+        rsav[nt][1] = ld_hint(Rc + 8 * nt + 2 * q + 1, pol_r);
+        acc[nt][0] = rsav[nt][0];
+        acc[nt][1] = rsav[nt][1];
+    }
+    const double* scol = src + (int64_t)(g + r) * lds;
+#pragma unroll
+    for (int kc = 0; kc < 32; kc += 8) {
+        double av[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int row = 4 * (kc + u) + q;
+            if (SRC_X) av[u] = (row < rows && g + r < mcols) ? ld_hint(scol + row, pol_x) : 0.0;
+            else av[u] = __ldcg(scol + row);
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+#pragma unroll
+            for (int nt = 0; nt < 4; ++nt)
+                dmma884(acc[nt], av[u], V[(8 * nt + r) * kT2Pld + 4 * (kc + u) + q]);
+    }
+    double w2[4][2];
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt) w2[nt][0] = w2[nt][1] = 0.0;
+#pragma unroll
+    for (int kk = 0; kk < 8; ++kk) {
+        const int sl = r * 4 + 2 * (kk & 1) + (q >> 1);
+        const double s0 = __shfl_sync(kFull, acc[kk >> 1][0], sl);
+        const double s1 = __shfl_sync(kFull, acc[kk >> 1][1], sl);
+        const double av = (q & 1) ? s1 : s0;
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt) dmma884(w2[nt], av, Tm[(4 * kk + q) * kLaTld + 8 * nt + r]);
+    }
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt) {
+        st_hint(Rc + 8 * nt + 2 * q, rsav[nt][0] - w2[nt][0], pol_r);
+        st_hint(Rc + 8 * nt + 2 * q + 1, rsav[nt][1] - w2[nt][1], pol_r);
+    }
+    double bv[8];
+#pragma unroll
+    for (int kk = 0; kk < 8; ++kk) {
+        const int sl = r * 4 + 2 * (kk & 1) + (q >> 1);
+        const double s0 = __shfl_sync(kFull, w2[kk >> 1][0], sl);
+        const double s1 = __shfl_sync(kFull, w2[kk >> 1][1], sl);
+        bv[kk] = (q & 1) ? s1 : s0;  // W'[4kk + q][r]
+    }
+    const double* s0c = src + (int64_t)(g + 2 * q) * lds;
+#pragma unroll 2
+    for (int mc = 0; mc < 16; mc += 4) {
+        double cb[4][2];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int row = 8 * (mc + u) + r;
+                if (SRC_X)
+                    cb[u][e] = (row < rows && g + 2 * q + e < mcols) ? ld_stream_hint(s0c + e * lds + row, pol_x) : 0.0;
+                else cb[u][e] = __ldcg(s0c + e * lds + row);
+            }
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk)
+#pragma unroll
+            for (int u = 0; u < 4; ++u) dmma884(cb[u], -V[(4 * kk + q) * kT2Pld + 8 * (mc + u) + r], bv[kk]);
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int row = 8 * (mc + u) + r;
+                if (DST_SMEM) dst[(int64_t)(gd + 2 * q + e) * ldd + row] = cb[u][e];
+                else __stcg(dst + (int64_t)(gd + 2 * q + e) * ldd + row, cb[u][e]);
+            }
+    }
+}
+
+__global__ void __launch_bounds__(kT2Threads, 1) tsqr_t128_kernel(T2Args a) {
+    extern __shared__ __align__(16) double sm[];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int M = a.M, m = a.m;
+    double* Pb = sm;                           // 2 panel buffers, 32 columns x 128 rows (ld kT2Pld)
+    double* Rp = Pb + 2 * 32 * kT2Pld;         // diagonal R block (ld kLaRld)
+    double* Sm = Rp + 32 * kLaRld;             // striu(V^T V) (ld kTld)
+    double* Tm0 = Sm + 32 * kTld;              // 2 x T (ld kLaTld)
+    double* tau = Tm0 + 2 * 32 * kLaTld;       // 32
+    double* pvall = tau + 32;                  // 4 x 32 pivot parts
+    double* dpart = pvall + 4 * 32;            // 2 x 4 x 32 partial dots
+
+    const int64_t job = blockIdx.x, G = gridDim.x;
+    const int64_t base = a.n / G, rem = a.n % G;
+    const int64_t row0 = job * base + (job < rem ? job : rem);
+    const int64_t row1 = row0 + base + (job < rem ? 1 : 0);
+    const int64_t RS = blk_rsize(M);
+    double* R = a.Rws + job * RS;
+    double* Scr = a.Scr + job * (int64_t)kT2Rows * M;
+    const uint64_t pol_x = l2_policy_evict_first(), pol_r = l2_policy_evict_last();
+    for (int64_t e = tid; e < RS; e += kT2Threads) st_hint(R + e, 0.0, pol_r);
+    __syncthreads();
+    const int npan = M / 32;
+    const bool panel_warp = warp < 4;
+    const int uw = warp - 4;  // update warp index 0..11
+    for (int64_t r0 = row0; r0 < row1; r0 += kT2Rows) {
+        const int rows = (int)((row1 - r0) < kT2Rows ? (row1 - r0) : kT2Rows);
+        const double* Xt = a.X + r0;  // column c at Xt + c * ld
+        // panel 0 of the tile straight from the input
+        if (warp == 0) la_fetch_rdiag(Rp, R, lane);
+        for (int e = tid; e < 32 * kT2Rows; e += kT2Threads) {
+            const int c = e >> 7, i = e & 127;
+            Pb[c * kT2Pld + i] = (i < rows && c < m) ? ld_hint(Xt + (int64_t)c * a.ld + i, pol_x) : 0.0;
+        }
+        if (warp == 0) cp_async_wait_all();
+        __syncthreads();
+        if (panel_warp) {
+            t2_panel(Pb, Rp, tau, pvall, dpart, Sm, warp, lane);
+            if (warp == 0) {
+                la_store_rdiag(Rp, R, lane, pol_r);
+                if (npan > 1) la_build_t(Sm, tau, Tm0, lane);
+            }
+        }
+        __syncthreads();
+        for (int p = 0; p + 1 < npan; ++p) {
+            const int c0 = 32 * p, nxt = c0 + 32;
+            const double* V = Pb + (p & 1) * 32 * kT2Pld;
+            double* Pn = Pb + ((p + 1) & 1) * 32 * kT2Pld;
+            const double* Tp = Tm0 + (p & 1) * 32 * kLaTld;
+            double* Rrow = R + blk_roff(p, M);
+            if (warp == 0) la_fetch_rdiag(Rp, R + blk_roff(p + 1, M), lane);
+            // phase A: panel p+1's columns, alone on the tensor pipes
+            if (uw >= 0 && uw < 4) {
+                if (p == 0)
+                    t2_group<true, true>(Xt, a.ld, rows, m, Pn, kT2Pld, V, Tp, Rrow, c0, nxt + 8 * uw, 8 * uw, lane, pol_x,
+                                         pol_r);
+                else
+                    t2_group<false, true>(Scr, kT2Rows, rows, m, Pn, kT2Pld, V, Tp, Rrow, c0, nxt + 8 * uw, 8 * uw, lane,
+                                          pol_x, pol_r);
+            }
+            if (warp == 0) cp_async_wait_all();
+            __syncthreads();
+            if (panel_warp) {
+                t2_panel(Pn, Rp, tau, pvall, dpart, Sm, warp, lane);
+                if (warp == 0) {
+                    la_store_rdiag(Rp, R + blk_roff(p + 1, M), lane, pol_r);
+                    if (p + 2 < npan) la_build_t(Sm, tau, Tm0 + ((p + 1) & 1) * 32 * kLaTld, lane);
+                }
+            } else {
+                for (int g = nxt + 32 + 8 * uw; g < M; g += 8 * 12) {
+                    if (p == 0)
+                        t2_group<true, false>(Xt, a.ld, rows, m, Scr, kT2Rows, V, Tp, Rrow, c0, g, g, lane, pol_x, pol_r);
+                    else
+                        t2_group<false, false>(Scr, kT2Rows, rows, m, Scr, kT2Rows, V, Tp, Rrow, c0, g, g, lane, pol_x,
+                                               pol_r);
+                }
+            }
+            __syncthreads();
+        }
+    }
+}
+
+}  // namespace ttsvd_b200

@@ -22,6 +22,7 @@
 #include "gqr.cuh"
 #include "jacobi_blk.cuh"
 #include "tsqr_la.cuh"
+#include "tsqr_t128.cuh"
 
 using namespace ttsvd_b200;
 
@@ -348,45 +349,28 @@ int tsqr_device(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t ld
         // Grid: one CTA per SM, at least 4 tiles of 128 rows per CTA (the
         // merge tree costs ~M reflector steps per level, so very short row
         // ranges do not pay).
-        static const char* tsel = std::getenv("TTSVD_TSQR");  // diagnostics: "tall", "blk"
-        const bool want_tall = tsel ? std::string(tsel) == "tall" : false;
-        if (!R_init && want_tall && n >= (int64_t)4 * kTallRows * 2) {
-            int64_t Gt = std::min<int64_t>(ctx->num_sms, std::max<int64_t>(1, n / (4 * (int64_t)kTallRows)));
+        // 128-row tiles, one CTA per SM, when every CTA gets >= 4 tiles
+        static const char* tsel = std::getenv("TTSVD_TSQR");  // diagnostics: "t128", "la", "blk"
+        const bool want_t128 = tsel ? std::string(tsel) == "t128" : true;
+        if (!R_init && want_t128 && n >= (int64_t)ctx->num_sms * 4 * kT2Rows) {
+            const int64_t Gt = ctx->num_sms;
             TT_TRY(ensure(ctx->ws_R, (size_t)Gt * RS * 8));
-            TT_TRY(ensure(ctx->ws_Scr, (size_t)Gt * kTallRows * M * 8));
+            TT_TRY(ensure(ctx->ws_Scr, (size_t)Gt * kT2Rows * M * 8));
             double* parts = as<double>(ctx->ws_R);
             static bool tattr = false;
             if (!tattr) {
-                TT_CUDA(cudaFuncSetAttribute(tsqr_tall_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)tall_smem_bytes()));
+                TT_CUDA(cudaFuncSetAttribute(tsqr_t128_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)t2_smem_bytes()));
                 tattr = true;
             }
-            static const bool prof = std::getenv("TTSVD_PROF_BLK") != nullptr;
-            long long* dprof = nullptr;
-            if (prof) TT_CUDA(cudaMalloc(&dprof, (size_t)Gt * 8 * sizeof(long long)));
-            TallArgs ta{X, n, ld, parts, as<double>(ctx->ws_Scr), m, M, dprof};
-            tsqr_tall_kernel<<<(unsigned)Gt, kTallThreads, tall_smem_bytes(), ctx->stream>>>(ta);
-            TT_TRY(check_launch(ctx, "tsqr_tall_kernel"));
-            if (prof) {
-                std::vector<long long> hp((size_t)Gt * 8);
-                TT_CUDA(cudaMemcpy(hp.data(), dprof, hp.size() * 8, cudaMemcpyDeviceToHost));
-                cudaFree(dprof);
-                double ph[6] = {0, 0, 0, 0, 0, 0};
-                for (int64_t g = 0; g < Gt; ++g)
-                    for (int q = 0; q < 6; ++q) ph[q] += (double)hp[g * 8 + q] / Gt;
-                const double tiles = (double)n / Gt / kTallRows;
-                std::fprintf(stderr, "[tall prof] n=%lld m=%d G=%lld tiles/CTA=%.1f per tile kcyc: load %.1f panel %.1f S %.1f T %.1f trail %.1f\n",
-                             (long long)n, m, (long long)Gt, tiles, ph[0] / tiles / 1e3, ph[1] / tiles / 1e3,
-                             ph[2] / tiles / 1e3, ph[3] / tiles / 1e3, ph[4] / tiles / 1e3);
-            }
-            if (Gt > 1) {
-                const int rc = merge_stack_gqr(ctx, parts, Gt, m, M, R);
-                if (rc != -1) return rc;
-                TT_TRY(ensure(ctx->ws_P, (size_t)RS * 8));
-                TT_TRY(merge_tree_blk(ctx, parts, Gt, m, M, as<double>(ctx->ws_P)));
-                return copy_leading(ctx, as<double>(ctx->ws_P), M, m, R);
-            }
-            return copy_leading(ctx, parts, M, m, R);
+            T2Args ta{X, n, ld, parts, as<double>(ctx->ws_Scr), m, M};
+            tsqr_t128_kernel<<<(unsigned)Gt, kT2Threads, t2_smem_bytes(), ctx->stream>>>(ta);
+            TT_TRY(check_launch(ctx, "tsqr_t128_kernel"));
+            const int rc = merge_stack_gqr(ctx, parts, Gt, m, M, R);
+            if (rc != -1) return rc;
+            TT_TRY(ensure(ctx->ws_P, (size_t)RS * 8));
+            TT_TRY(merge_tree_blk(ctx, parts, Gt, m, M, as<double>(ctx->ws_P)));
+            return copy_leading(ctx, as<double>(ctx->ws_P), M, m, R);
         }
         int per_sm = 1;
         TT_CUDA(cudaFuncSetAttribute(tsqr_blk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit));

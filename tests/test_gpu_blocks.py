@@ -81,6 +81,31 @@ def test_tsqr_gram_property(tt, n, m):
     assert gram_resid(X, R) <= 1e-12
 
 
+# The wide-factor kernels: 32-row look-ahead tiles (tsqr_la_kernel, n below
+# 4 x 128 rows per SM) and 128-row tiles (tsqr_t128_kernel), including partial
+# tiles, m not a multiple of 32, zero and duplicated columns and low rank.
+@pytest.mark.parametrize("n,m,kind", [(40000, 96, "dense"), (30011, 45, "dup"), (80000, 64, "dense"),
+                                      (90001, 45, "dup"), (77777, 130, "lowrank"), (160000, 256, "dense")])
+def test_tsqr_wide_kernels(tt, n, m, kind):
+    from oracle.oracle import gaussian
+    X = gaussian(n, m, 31 + m).copy(order="F")
+    if kind == "dup":
+        X[:, m - 1] = X[:, 0]
+        X[:, m // 2] = 0.0
+    if kind == "lowrank":
+        X = np.asfortranarray(gaussian(n, 7, 5) @ gaussian(7, m, 6))
+    R = host(tt.tsqr(X))
+    assert np.all(np.isfinite(R))
+    assert np.all(np.tril(R, -1) == 0.0)
+    assert gram_resid(X, R) <= 1e-12
+    s_r = np.linalg.svd(R, compute_uv=False)
+    s_x = np.linalg.svd(X, compute_uv=False)
+    assert np.max(np.abs(s_r - s_x)) <= 1e-10 * s_x[0]
+    if kind != "dense":
+        rank = 7 if kind == "lowrank" else m - 2
+        assert s_r[rank] <= 1e-13 * s_r[0]
+
+
 def test_tsqr_rank_deficient_duplicate_column(tt, orc):
     # test_tsqr.cpp:88-97
     from oracle.oracle import gaussian
