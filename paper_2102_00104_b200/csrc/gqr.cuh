@@ -37,11 +37,26 @@ struct GqrArgs {
     double* Wfin;    // 32 x M: W' = T^T W of the current panel
 };
 
+// 32 per-lane values -> lane k holds the warp sum of value k (butterfly
+// reduce-scatter: 16 + 8 + 4 + 2 + 1 shuffles)
+__device__ __forceinline__ double warp_reduce_scatter32(double (&v)[32], int lane) {
+    const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4, b1 = lane & 2, b0 = lane & 1;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) v[k] = (b4 ? v[k + 16] : v[k]) + __shfl_xor_sync(0xffffffffu, b4 ? v[k] : v[k + 16], 16);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v[k] = (b3 ? v[k + 8] : v[k]) + __shfl_xor_sync(0xffffffffu, b3 ? v[k] : v[k + 8], 8);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) v[k] = (b2 ? v[k + 4] : v[k]) + __shfl_xor_sync(0xffffffffu, b2 ? v[k] : v[k + 4], 4);
+#pragma unroll
+    for (int k = 0; k < 2; ++k) v[k] = (b1 ? v[k + 2] : v[k]) + __shfl_xor_sync(0xffffffffu, b1 ? v[k] : v[k + 2], 2);
+    return (b0 ? v[1] : v[0]) + __shfl_xor_sync(0xffffffffu, b0 ? v[0] : v[1], 1);
+}
+
 __host__ __device__ inline int gqr_ldy(int rows) { return ((((rows + 3) & ~3) + 7) & ~7) + 4; }
 
 inline size_t gqr_smem_bytes(int rows_max) {
     const int ldy = gqr_ldy(rows_max);
-    return ((size_t)32 * ldy + 2 * 32 * 33 + 32 + 8 * 33 + (kGqrThreads / 32) * 32 * 9) * sizeof(double);
+    return ((size_t)32 * ldy + 2 * 32 * 33 + 32 + 16 * 33 + (kGqrThreads / 32) * 32 * 9) * sizeof(double);
 }
 
 __global__ void __launch_bounds__(kGqrThreads, 1) gqr_kernel(GqrArgs a) {
@@ -61,8 +76,8 @@ __global__ void __launch_bounds__(kGqrThreads, 1) gqr_kernel(GqrArgs a) {
     double* Sm = Ys + 32 * ldy;              // 32 x 33
     double* Tm = Sm + 32 * 33;               // 32 x 33
     double* tau = Tm + 32 * 33;              // 32
-    double* red = tau + 32;                  // 8 warps x 33
-    double* Wsc = red + 8 * 33;              // per-warp 32 x 8 (ld 9)
+    double* red = tau + 32;                  // 16 x 33 (warp totals, then slice totals)
+    double* Wsc = red + 16 * 33;             // per-warp 32 x 8 (ld 9)
     double* part = a.part;
     double* A = a.A;
     const int lr = lane >> 2, lc = lane & 3;
@@ -96,12 +111,10 @@ __global__ void __launch_bounds__(kGqrThreads, 1) gqr_kernel(GqrArgs a) {
                 for (int k = 1; k < 32; ++k)
                     if (k > jj) v[k] = fma(xj, Ys[k * ldy + i], v[k]);
             }
-            // block reduction of the 32 values: warp butterfly, then warps via smem
-#pragma unroll
-            for (int k = 0; k < 32; ++k) v[k] = warp_sum(v[k]);
-            if (lane == 0)
-#pragma unroll
-                for (int k = 0; k < 32; ++k) red[warp * 33 + k] = v[k];
+            // block reduction of the 32 values: warp reduce-scatter (lane k ends
+            // with the warp's total of value k, 31 shuffles), then warps via smem
+            const double vk = warp_reduce_scatter32(v, lane);
+            red[warp * 33 + lane] = vk;
             __syncthreads();
             if (tid < 32) {
                 double t = 0.0;
@@ -110,12 +123,21 @@ __global__ void __launch_bounds__(kGqrThreads, 1) gqr_kernel(GqrArgs a) {
             }
             __threadfence();
             grid.sync();
-            // totals in a fixed order (identical on every CTA)
+            // totals in a fixed order (identical on every CTA): value k = tid & 31,
+            // slice s = tid >> 5 sums CTAs q = s, s + 8, ...; then the 8 slices
+            {
+                const int k = tid & 31, sl = tid >> 5;
+                double t = 0.0;
+                for (int q = sl; q < G; q += kGqrThreads / 32) t += __ldcg(&part[((int64_t)buf * G + q) * 33 + k]);
+                red[8 * 33 + sl * 33 + k] = t;
+            }
+            __syncthreads();
             if (tid < 32) {
                 double t = 0.0;
-                for (int q = 0; q < G; ++q) t += part[((int64_t)buf * G + q) * 33 + tid];
+#pragma unroll
+                for (int sl = 0; sl < kGqrThreads / 32; ++sl) t += red[8 * 33 + sl * 33 + tid];
                 red[tid] = t;
-                red[33 + tid] = a.piv[buf * 32 + tid];
+                red[33 + tid] = __ldcg(&a.piv[buf * 32 + tid]);
             }
             __syncthreads();
             const double sp = red[0];
@@ -192,7 +214,7 @@ __global__ void __launch_bounds__(kGqrThreads, 1) gqr_kernel(GqrArgs a) {
         grid.sync();
         for (int e = tid; e < 1024; e += kGqrThreads) {
             double t = 0.0;
-            for (int q = 0; q < G; ++q) t += part[(int64_t)2 * G * 33 + (int64_t)q * 1024 + e];
+            for (int q = 0; q < G; ++q) t += __ldcg(&part[(int64_t)2 * G * 33 + (int64_t)q * 1024 + e]);
             Sm[(e >> 5) * 33 + (e & 31)] = t;
         }
         __syncthreads();
@@ -258,7 +280,7 @@ __global__ void __launch_bounds__(kGqrThreads, 1) gqr_kernel(GqrArgs a) {
             for (int64_t col = ca + warp; col < cb; col += kGqrThreads / 32) {
                 // lane k: W(k, col) summed over CTAs in order
                 double w = 0.0;
-                for (int q = 0; q < G; ++q) w += pw[((int64_t)q * 32 + lane) * M + col];
+                for (int q = 0; q < G; ++q) w += __ldcg(&pw[((int64_t)q * 32 + lane) * M + col]);
                 // W'(i, col) = sum_k T(k, i) W(k, col)
                 double wp = 0.0;
                 for (int k = 0; k < 32; ++k) wp = fma(Tm[k * 33 + lane], __shfl_sync(0xffffffffu, w, k), wp);
@@ -271,7 +293,7 @@ __global__ void __launch_bounds__(kGqrThreads, 1) gqr_kernel(GqrArgs a) {
         for (int gq = warp; gq < ngr; gq += kGqrThreads / 32) {
             const int64_t g = t0 + 8 * gq;
             double* Ws = Wsc + warp * 32 * 9;
-            for (int e = lane; e < 256; e += 32) Ws[(e >> 3) * 9 + (e & 7)] = a.Wfin[(int64_t)(e >> 3) * M + g + (e & 7)];
+            for (int e = lane; e < 256; e += 32) Ws[(e >> 3) * 9 + (e & 7)] = __ldcg(&a.Wfin[(int64_t)(e >> 3) * M + g + (e & 7)]);
             __syncwarp();
             double wf[8];
 #pragma unroll

@@ -339,7 +339,7 @@ int tsqr_device(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t ld
         const int64_t RS = blk_rsize(M);
         // Short-fat (n <= 256 M, n <= 512 rows per SM): one cooperative grid
         // factorises the whole matrix (gqr.cuh), no merge tree.
-        if (!R_init && n >= M && n <= (int64_t)256 * M) {
+        if (!R_init && n >= M && n <= (int64_t)256 * M && !(std::getenv("TTSVD_TSQR") && std::string(std::getenv("TTSVD_TSQR")) == "t128")) {
             const int rc = gqr_device(ctx, X, n, m, ld, R);
             if (rc != -1) return rc;
         }
@@ -351,8 +351,9 @@ int tsqr_device(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t ld
         // ranges do not pay).
         // 128-row tiles, one CTA per SM, when every CTA gets >= 4 tiles
         static const char* tsel = std::getenv("TTSVD_TSQR");  // diagnostics: "t128", "la", "blk"
-        const bool want_t128 = tsel ? std::string(tsel) == "t128" : true;
-        if (!R_init && want_t128 && n >= (int64_t)ctx->num_sms * 4 * kT2Rows) {
+        const bool force_t128 = tsel && std::string(tsel) == "t128";
+        const bool want_t128 = tsel ? force_t128 : true;
+        if (!R_init && want_t128 && (n >= (int64_t)ctx->num_sms * 4 * kT2Rows || (force_t128 && n >= 4 * kT2Rows))) {
             const int64_t Gt = ctx->num_sms;
             TT_TRY(ensure(ctx->ws_R, (size_t)Gt * RS * 8));
             TT_TRY(ensure(ctx->ws_Scr, (size_t)Gt * kT2Rows * M * 8));
@@ -366,7 +367,23 @@ int tsqr_device(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t ld
             T2Args ta{X, n, ld, parts, as<double>(ctx->ws_Scr), m, M};
             tsqr_t128_kernel<<<(unsigned)Gt, kT2Threads, t2_smem_bytes(), ctx->stream>>>(ta);
             TT_TRY(check_launch(ctx, "tsqr_t128_kernel"));
+            static const bool prof = std::getenv("TTSVD_PROF_BLK") != nullptr;
+            cudaEvent_t e0, e1;
+            if (prof) {
+                cudaEventCreate(&e0);
+                cudaEventCreate(&e1);
+                cudaEventRecord(e0, ctx->stream);
+            }
             const int rc = merge_stack_gqr(ctx, parts, Gt, m, M, R);
+            if (prof) {
+                cudaEventRecord(e1, ctx->stream);
+                cudaEventSynchronize(e1);
+                float ms = 0.f;
+                cudaEventElapsedTime(&ms, e0, e1);
+                std::fprintf(stderr, "[t128 prof] n=%lld m=%d merge of %lld parts: %.3f ms\n", (long long)n, m, (long long)Gt, ms);
+                cudaEventDestroy(e0);
+                cudaEventDestroy(e1);
+            }
             if (rc != -1) return rc;
             TT_TRY(ensure(ctx->ws_P, (size_t)RS * 8));
             TT_TRY(merge_tree_blk(ctx, parts, Gt, m, M, as<double>(ctx->ws_P)));
