@@ -16,10 +16,12 @@
 //      the two blocks in 3 more sub-rounds at the first round of a sweep;
 //   3. B <- B Q by DMMA (skipped when no pair rotated).
 //
-// Between rounds the slot of every block pair moves as in jacobi_ring_kernel
-// (top row one slot right, bottom row one slot left); the two blocks that
-// cross a CTA boundary are copied into the neighbour's inbox through
-// distributed shared memory, one cluster barrier per round.  A sweep is
+// Between rounds the slot of every block pair moves (top row one slot right,
+// bottom row one slot left; top[h-1] -> bot[h-1], bot[0] -> top[1]); moves
+// inside a CTA relabel buffers, the two blocks that cross a CTA boundary are
+// copied into the neighbour's inbox through distributed shared memory (the
+// inbox indices are pushed ahead by the receiver), one cluster barrier per
+// round.  A sweep is
 // nblk_pad - 1 rounds, so every column pair meets at least once per sweep;
 // the matrix has converged after a sweep in which no pair rotated (Gram
 // entries are recomputed from the columns at every visit, so the stopping
@@ -56,12 +58,139 @@ __device__ __forceinline__ void bj_group_sync(int grp) {
     asm volatile("bar.sync %0, %1;" ::"r"(1 + grp), "r"(kBjWpg * 32) : "memory");
 }
 
+// One visit of a block pair (8 columns: blocks bt | bb, 4 columns each, ld
+// ldc, rows n8): Gram by DMMA over the group's warps, the rotations on the
+// Gram matrix by the solver warp, B <- B Q by DMMA.  Returns (in the solver
+// warp) whether any pair rotated.
+__device__ __forceinline__ bool bj_visit(double* bt, double* bb, int blt, int blb, bool first_round, int m, int n8,
+                                         int ldc, double (*gpart)[64], double* Gs, double* Qs, int* grp_rot, int grp,
+                                         int wg, bool solver, int lane) {
+    const double tol = 1e2 * DBL_EPSILON;
+    bool rotated = false;
+    // ---- 1. Gram partials: lane l reads column l/4, rows 4q + l%4 ----
+    {
+        const int c = lane >> 2;
+        const double* col = (c < 4 ? bt + c * ldc : bb + (c - 4) * ldc) + (lane & 3);
+        double acc0[2] = {0.0, 0.0}, acc1[2] = {0.0, 0.0};
+        const int nq = n8 >> 2;
+        int q = wg;
+        for (; q + kBjWpg < nq; q += 2 * kBjWpg) {
+            const double v0 = col[4 * q], v1 = col[4 * (q + kBjWpg)];
+            dmma884(acc0, v0, v0);
+            dmma884(acc1, v1, v1);
+        }
+        if (q < nq) {
+            const double v0 = col[4 * q];
+            dmma884(acc0, v0, v0);
+        }
+        double* gp = gpart[wg];
+        gp[(lane >> 2) * 8 + 2 * (lane & 3)] = acc0[0] + acc1[0];
+        gp[(lane >> 2) * 8 + 2 * (lane & 3) + 1] = acc0[1] + acc1[1];
+    }
+    bj_group_sync(grp);
+    // ---- 2. rotations on the Gram matrix (the solver warp) ----
+    if (solver) {
+        double* G = Gs;
+        double* Q = Qs;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int e = lane + 32 * h, i = e >> 3, j = e & 7;
+            double s = 0.0;
+#pragma unroll
+            for (int w = 0; w < kBjWpg; ++w) s += gpart[w][e];
+            G[i * 9 + j] = s;
+            Q[i * 9 + j] = (i == j) ? 1.0 : 0.0;
+        }
+        int any = 0;
+        __syncwarp();
+        // sub-rounds 0..3: the 16 cross pairs (top i, bottom (i + s) mod 4);
+        // sub-rounds 4..6 (first round of a sweep only): the 12 pairs
+        // inside the two blocks, so every pair meets once per sweep
+        const int nsub = first_round ? 7 : 4;
+        const int kp = lane & 3;
+        for (int s = 0; s < nsub; ++s) {
+            int x, y;
+            if (s < 4) {
+                x = kp;
+                y = 4 + ((kp + s) & 3);
+            } else {
+                const int base = kp < 2 ? 0 : 4, j = kp & 1, t = s - 4;
+                x = base + (t == 0 ? 2 * j : j);
+                y = base + (t == 0 ? 2 * j + 1 : (t == 1 ? j + 2 : 3 - j));
+            }
+            const int gx = x < 4 ? 4 * blt + x : 4 * blb + x - 4;
+            const int gy = y < 4 ? 4 * blt + y : 4 * blb + y - 4;
+            const int p = gx < gy ? x : y, q = gx < gy ? y : x;
+            // every lane computes the rotation of pair kp (no broadcast round trip)
+            const double al = G[p * 9 + p], be = G[q * 9 + q], ga = G[p * 9 + q];
+            double c = 1.0, sn = 0.0;
+            if (ga * ga > (tol * tol) * (al * be)) {
+                const double zeta = (be - al) * __drcp_rn(2.0 * ga);
+                const double t =
+                    ((zeta >= 0.0) ? 1.0 : -1.0) * __drcp_rn(fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
+                c = rsqrt(fma(t, t, 1.0));
+                sn = c * t;
+                any = 1;
+            }
+            {
+                // columns: (x_p, x_q) <- (c x_p - s x_q, s x_p + c x_q) on G and Q
+                const int i = lane >> 2;
+                const double gp = G[i * 9 + p], gq = G[i * 9 + q];
+                const double qp = Q[i * 9 + p], qq = Q[i * 9 + q];
+                __syncwarp();
+                G[i * 9 + p] = c * gp - sn * gq;
+                G[i * 9 + q] = sn * gp + c * gq;
+                Q[i * 9 + p] = c * qp - sn * qq;
+                Q[i * 9 + q] = sn * qp + c * qq;
+            }
+            __syncwarp();
+            {
+                // rows of G: J^T (G J); lane -> (pair lane >> 3, column lane & 7)
+                const int src = lane >> 3;
+                const double c2 = __shfl_sync(0xffffffffu, c, src);
+                const double s2 = __shfl_sync(0xffffffffu, sn, src);
+                const int p2 = __shfl_sync(0xffffffffu, p, src), q2 = __shfl_sync(0xffffffffu, q, src);
+                const int j = lane & 7;
+                const double gp = G[p2 * 9 + j], gq = G[q2 * 9 + j];
+                G[p2 * 9 + j] = c2 * gp - s2 * gq;
+                G[q2 * 9 + j] = s2 * gp + c2 * gq;
+            }
+            __syncwarp();
+        }
+        any = __any_sync(0xffffffffu, any);
+        if (lane == 0) *grp_rot = any;
+        rotated = any;
+    }
+    bj_group_sync(grp);
+    // ---- 3. B <- B Q (DMMA; 8-row tiles) ----
+    if (*grp_rot) {
+        const double* Q = Qs;
+        const double q0 = Q[(lane & 3) * 9 + (lane >> 2)];
+        const double q1 = Q[(4 + (lane & 3)) * 9 + (lane >> 2)];
+        const int ce = 2 * (lane & 3);
+        double* o0 = ce < 4 ? bt + ce * ldc : bb + (ce - 4) * ldc;
+#pragma unroll 4
+        for (int t = wg; t < (n8 >> 3); t += kBjWpg) {
+            const int rr = 8 * t + (lane >> 2);
+            const double a0 = bt[(lane & 3) * ldc + rr];
+            const double a1 = bb[(lane & 3) * ldc + rr];
+            double d[2] = {0.0, 0.0};
+            dmma884(d, a0, q0);
+            dmma884(d, a1, q1);
+            o0[rr] = d[0];
+            o0[ldc + rr] = d[1];
+        }
+    }
+        return rotated;
+}
+
 __global__ void __launch_bounds__(kBjThreads, 1) jacobi_bj_kernel(BjArgs a) {
     constexpr int S = kBjSlots;
     cg::cluster_group cl = cg::this_cluster();
     extern __shared__ __align__(16) double smem[];
     __shared__ int top_buf[S], bot_buf[S], top_blk[S], bot_blk[S];
     __shared__ int inbox_idx[2][2], inbox_blk[2][2], rot[2];
+    __shared__ int rdst[2], ldst[2];  // neighbours' inbox buffers for my sends (pushed by them)
     __shared__ int grp_rot[S];
     __shared__ double gpart[S][kBjWpg][64];
     __shared__ double Gs[S][8 * 9], Qs[S][8 * 9];
@@ -80,6 +209,8 @@ __global__ void __launch_bounds__(kBjThreads, 1) jacobi_bj_kernel(BjArgs a) {
     if (tid == 0) {
         inbox_idx[0][0] = 2 * S;
         inbox_idx[0][1] = 2 * S + 1;
+        rdst[0] = 2 * S;
+        ldst[0] = 2 * S + 1;
         rot[0] = rot[1] = 0;
     }
     __syncthreads();
@@ -93,7 +224,6 @@ __global__ void __launch_bounds__(kBjThreads, 1) jacobi_bj_kernel(BjArgs a) {
     }
     cl.sync();
     const int rounds = 2 * S * C - 1;
-    const double tol = 1e2 * DBL_EPSILON;
     int sweep = 0, par = 0;
     bool converged = (m < 2);
     for (; sweep < a.max_sweeps && !converged; ++sweep) {
@@ -105,142 +235,40 @@ __global__ void __launch_bounds__(kBjThreads, 1) jacobi_bj_kernel(BjArgs a) {
             double* bt = smem + (int64_t)top_buf[grp] * bsz;
             double* bb = smem + (int64_t)bot_buf[grp] * bsz;
             if (active) {
-                // ---- 1. Gram partials: lane l reads column l/4, rows 4q + l%4 ----
-                {
-                    const int c = lane >> 2;
-                    const double* col = (c < 4 ? bt + c * ldc : bb + (c - 4) * ldc) + (lane & 3);
-                    double acc0[2] = {0.0, 0.0}, acc1[2] = {0.0, 0.0};
-                    const int nq = n8 >> 2;
-                    int q = wg;
-                    for (; q + kBjWpg < nq; q += 2 * kBjWpg) {
-                        const double v0 = col[4 * q], v1 = col[4 * (q + kBjWpg)];
-                        dmma884(acc0, v0, v0);
-                        dmma884(acc1, v1, v1);
-                    }
-                    if (q < nq) {
-                        const double v0 = col[4 * q];
-                        dmma884(acc0, v0, v0);
-                    }
-                    double* gp = gpart[grp][wg];
-                    gp[(lane >> 2) * 8 + 2 * (lane & 3)] = acc0[0] + acc1[0];
-                    gp[(lane >> 2) * 8 + 2 * (lane & 3) + 1] = acc0[1] + acc1[1];
-                }
-                bj_group_sync(grp);
-                // ---- 2. rotations on the Gram matrix (warp 0 of the group) ----
-                if (wg == 0) {
-                    double* G = Gs[grp];
-                    double* Q = Qs[grp];
-#pragma unroll
-                    for (int h = 0; h < 2; ++h) {
-                        const int e = lane + 32 * h, i = e >> 3, j = e & 7;
-                        double s = 0.0;
-#pragma unroll
-                        for (int w = 0; w < kBjWpg; ++w) s += gpart[grp][w][e];
-                        G[i * 9 + j] = s;
-                        Q[i * 9 + j] = (i == j) ? 1.0 : 0.0;
-                    }
-                    int any = 0;
-                    __syncwarp();
-                    // sub-rounds 0..3: the 16 cross pairs (top i, bottom (i + s) mod 4);
-                    // sub-rounds 4..6 (first round of a sweep only): the 12 pairs
-                    // inside the two blocks, so every pair meets once per sweep
-                    const int nsub = (r == 0) ? 7 : 4;
-                    const int kp = lane & 3;
-                    for (int s = 0; s < nsub; ++s) {
-                        int x, y;
-                        if (s < 4) {
-                            x = kp;
-                            y = 4 + ((kp + s) & 3);
-                        } else {
-                            const int base = kp < 2 ? 0 : 4, j = kp & 1, t = s - 4;
-                            x = base + (t == 0 ? 2 * j : j);
-                            y = base + (t == 0 ? 2 * j + 1 : (t == 1 ? j + 2 : 3 - j));
-                        }
-                        const int gx = x < 4 ? 4 * blt + x : 4 * blb + x - 4;
-                        const int gy = y < 4 ? 4 * blt + y : 4 * blb + y - 4;
-                        const int p = gx < gy ? x : y, q = gx < gy ? y : x;
-                        // every lane computes the rotation of pair kp (no broadcast round trip)
-                        const double al = G[p * 9 + p], be = G[q * 9 + q], ga = G[p * 9 + q];
-                        double c = 1.0, sn = 0.0;
-                        if (ga * ga > (tol * tol) * (al * be)) {
-                            const double zeta = (be - al) * __drcp_rn(2.0 * ga);
-                            const double t =
-                                ((zeta >= 0.0) ? 1.0 : -1.0) * __drcp_rn(fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
-                            c = rsqrt(fma(t, t, 1.0));
-                            sn = c * t;
-                            any = 1;
-                        }
-                        {
-                            // columns: (x_p, x_q) <- (c x_p - s x_q, s x_p + c x_q) on G and Q
-                            const int i = lane >> 2;
-                            const double gp = G[i * 9 + p], gq = G[i * 9 + q];
-                            const double qp = Q[i * 9 + p], qq = Q[i * 9 + q];
-                            __syncwarp();
-                            G[i * 9 + p] = c * gp - sn * gq;
-                            G[i * 9 + q] = sn * gp + c * gq;
-                            Q[i * 9 + p] = c * qp - sn * qq;
-                            Q[i * 9 + q] = sn * qp + c * qq;
-                        }
-                        __syncwarp();
-                        {
-                            // rows of G: J^T (G J); lane -> (pair lane >> 3, column lane & 7)
-                            const int src = lane >> 3;
-                            const double c2 = __shfl_sync(0xffffffffu, c, src);
-                            const double s2 = __shfl_sync(0xffffffffu, sn, src);
-                            const int p2 = __shfl_sync(0xffffffffu, p, src), q2 = __shfl_sync(0xffffffffu, q, src);
-                            const int j = lane & 7;
-                            const double gp = G[p2 * 9 + j], gq = G[q2 * 9 + j];
-                            G[p2 * 9 + j] = c2 * gp - s2 * gq;
-                            G[q2 * 9 + j] = s2 * gp + c2 * gq;
-                        }
-                        __syncwarp();
-                    }
-                    any = __any_sync(0xffffffffu, any);
-                    if (lane == 0) {
-                        grp_rot[grp] = any;
-                        if (any) rot[sweep & 1] = 1;
-                    }
-                }
-                bj_group_sync(grp);
-                // ---- 3. B <- B Q (DMMA; 8-row tiles) ----
-                if (grp_rot[grp]) {
-                    const double* Q = Qs[grp];
-                    const double q0 = Q[(lane & 3) * 9 + (lane >> 2)];
-                    const double q1 = Q[(4 + (lane & 3)) * 9 + (lane >> 2)];
-                    const int ce = 2 * (lane & 3);
-                    double* o0 = ce < 4 ? bt + ce * ldc : bb + (ce - 4) * ldc;
-#pragma unroll 4
-                    for (int t = wg; t < (n8 >> 3); t += kBjWpg) {
-                        const int rr = 8 * t + (lane >> 2);
-                        const double a0 = bt[(lane & 3) * ldc + rr];
-                        const double a1 = bb[(lane & 3) * ldc + rr];
-                        double d[2] = {0.0, 0.0};
-                        dmma884(d, a0, q0);
-                        dmma884(d, a1, q1);
-                        o0[rr] = d[0];
-                        o0[ldc + rr] = d[1];
-                    }
-                }
+                if (bj_visit(bt, bb, blt, blb, r == 0, m, n8, ldc, gpart[grp], Gs[grp], Qs[grp], &grp_rot[grp], grp, wg,
+                             wg == grp, lane))
+                    rot[sweep & 1] = 1;
             }
             __syncthreads();
             // ---- block moves: boundary blocks -> neighbours' inboxes ----
             if (k < C - 1) {
-                const int dst_idx = *(volatile int*)cl.map_shared_rank(&inbox_idx[par][0], k + 1);
+                const int dst_idx = rdst[par];
                 double2* dst = reinterpret_cast<double2*>(cl.map_shared_rank(smem, k + 1) + (int64_t)dst_idx * bsz);
                 const double2* src = reinterpret_cast<const double2*>(smem + (int64_t)top_buf[S - 1] * bsz);
                 for (int i = tid; i < bsz / 2; i += kBjThreads) dst[i] = src[i];
                 if (tid == 0) *cl.map_shared_rank(&inbox_blk[par][0], k + 1) = top_blk[S - 1];
             }
             if (k > 0) {
-                const int dst_idx = *(volatile int*)cl.map_shared_rank(&inbox_idx[par][1], k - 1);
+                const int dst_idx = ldst[par];
                 double2* dst = reinterpret_cast<double2*>(cl.map_shared_rank(smem, k - 1) + (int64_t)dst_idx * bsz);
                 const double2* src = reinterpret_cast<const double2*>(smem + (int64_t)bot_buf[0] * bsz);
                 for (int i = tid; i < bsz / 2; i += kBjThreads) dst[i] = src[i];
                 if (tid == 0) *cl.map_shared_rank(&inbox_blk[par][1], k - 1) = bot_blk[0];
             }
             if (tid == 0) {
-                if (k < C - 1) inbox_idx[par ^ 1][k > 0 ? 0 : 1] = top_buf[S - 1];
-                if (k > 0) inbox_idx[par ^ 1][k < C - 1 ? 1 : 0] = bot_buf[0];
+                // the blocks just sent free their buffers: they become my inboxes for
+                // the next round, and the neighbours that fill them are told now
+                int in0 = -1, in1 = -1;
+                if (k < C - 1) (k > 0 ? in0 : in1) = top_buf[S - 1];
+                if (k > 0) (k < C - 1 ? in1 : in0) = bot_buf[0];
+                if (in0 >= 0) {
+                    inbox_idx[par ^ 1][0] = in0;
+                    if (k > 0) *cl.map_shared_rank(&rdst[par ^ 1], k - 1) = in0;
+                }
+                if (in1 >= 0) {
+                    inbox_idx[par ^ 1][1] = in1;
+                    if (k < C - 1) *cl.map_shared_rank(&ldst[par ^ 1], k + 1) = in1;
+                }
             }
             cl.sync();
             if (warp == 0) {
@@ -289,5 +317,7 @@ __global__ void __launch_bounds__(kBjThreads, 1) jacobi_bj_kernel(BjArgs a) {
     if (k == 0 && tid == 0) *a.status = converged ? sweep : -1;
     cl.sync();  // no CTA leaves while a neighbour may still read its flags
 }
+
+
 
 }  // namespace ttsvd_b200
