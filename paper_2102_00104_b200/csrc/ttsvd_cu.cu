@@ -23,6 +23,7 @@
 #include "jacobi_blk.cuh"
 #include "tsqr_la.cuh"
 #include "tsqr_t128.cuh"
+#include "tsqr_ws.cuh"
 
 using namespace ttsvd_b200;
 
@@ -332,6 +333,47 @@ int merge_stack_gqr(ttsvd_cu_ctx* ctx, const double* parts, int64_t count, int m
 // R (m x m) of X (n x m, ld) — n may be smaller than m (the structured kernel
 // does not need n >= m; gram_triangular's square padding is implicit).
 // R_init (m x m) optionally seeds a single job (reduce_block).
+// m <= 32: warp streams (tsqr_ws.cuh), levels of stacked factors until one
+// stream is left.
+template <int SW>
+int tsqr_ws_levels(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t ld, double* R) {
+    static int per_sm = -1;
+    const size_t smem = ws_smem_bytes<SW>();
+    if (per_sm < 0) {
+        TT_CUDA(cudaFuncSetAttribute(tsqr_ws_kernel<SW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        TT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tsqr_ws_kernel<SW>, kWsThreads, smem));
+        per_sm = std::max(1, per_sm);
+    }
+    constexpr int per_cta = (kWsThreads / 32) * (32 / SW);
+    const int64_t max_streams = (int64_t)per_sm * ctx->num_sms * per_cta;
+    const double* src = X;
+    int64_t rows = n, sld = ld;
+    int flip = 0;
+    for (;;) {
+        int64_t S = std::min<int64_t>(rows / 128, max_streams);  // >= 4 tiles per stream
+        if (S < 1) S = 1;
+        if (S > 1) {
+            TT_TRY(ensure(ctx->ws_R, (size_t)S * m * m * 8));
+            TT_TRY(ensure(ctx->ws_R2, (size_t)S * m * m * 8));
+        }
+        double* out = (S == 1) ? R : as<double>(flip ? ctx->ws_R2 : ctx->ws_R);
+        const int64_t ldo = (S == 1) ? m : S * m;
+        WsArgs wa{src, rows, sld, m, S, out, ldo};
+        const int64_t grid = (S + per_cta - 1) / per_cta;
+        tsqr_ws_kernel<SW><<<(unsigned)grid, kWsThreads, smem, ctx->stream>>>(wa);
+        TT_TRY(check_launch(ctx, "tsqr_ws_kernel"));
+        if (S == 1) return TTSVD_OK;
+        src = out;
+        rows = S * m;
+        sld = S * m;
+        flip ^= 1;
+    }
+}
+
+int tsqr_ws_device(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t ld, double* R) {
+    return m <= 16 ? tsqr_ws_levels<16>(ctx, X, n, m, ld, R) : tsqr_ws_levels<32>(ctx, X, n, m, ld, R);
+}
+
 int tsqr_device(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t ld, double* R,
                 const double* R_init = nullptr) {
     if (m > kSmallM) {
@@ -435,6 +477,11 @@ int tsqr_device(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t ld
             return copy_leading(ctx, as<double>(ctx->ws_P), M, m, R);
         }
         return copy_leading(ctx, parts, M, m, R);
+    }
+    {
+        static const char* tsel = std::getenv("TTSVD_TSQR");  // diagnostics: "v1" = the block-per-job kernel
+        const bool v1 = tsel && std::string(tsel) == "v1";
+        if (!R_init && !v1 && n >= 4096) return tsqr_ws_device(ctx, X, n, m, ld, R);
     }
     TsqrPlan p = tsqr_plan(m);
     const int64_t min_rows = std::max<int64_t>(p.bt, 8 * (int64_t)m);
