@@ -34,9 +34,11 @@ __host__ __device__ constexpr int ws_rld() {
     return SW + 1;
 }
 
+constexpr int kWsSld = 34;  // column stride of a stream's staged tile (32 rows, 16-byte aligned)
+
 template <int SW>
 inline size_t ws_smem_bytes() {
-    return (size_t)(kWsThreads / 32) * (32 / SW) * (32 + SW * ws_rld<SW>()) * sizeof(double);
+    return (size_t)(kWsThreads / 32) * (32 / SW) * (32 + SW * ws_rld<SW>() + SW * kWsSld) * sizeof(double);
 }
 
 template <int SW>
@@ -48,8 +50,9 @@ __global__ void __launch_bounds__(kWsThreads, 2) tsqr_ws_kernel(WsArgs a) {
     const int sub = lane / SW, sl = lane % SW;
     const int64_t s = ((int64_t)blockIdx.x * (kWsThreads / 32) + warp) * SPW + sub;
     const bool live = s < a.S;
-    double* pv = sm + (size_t)(warp * SPW + sub) * (32 + SW * RLD);
+    double* pv = sm + (size_t)(warp * SPW + sub) * (32 + SW * RLD + SW * kWsSld);
     double* Rs = pv + 32;
+    double* stg = Rs + SW * RLD;  // the tile, column-major (ld kWsSld), staged by coalesced loads
     const int m = a.m;
     for (int e = sl; e < SW * RLD; e += SW) Rs[e] = 0.0;
     int64_t row0 = 0, row1 = 0;
@@ -68,14 +71,27 @@ __global__ void __launch_bounds__(kWsThreads, 2) tsqr_ws_kernel(WsArgs a) {
     const unsigned s_pv = (unsigned)__cvta_generic_to_shared(pv);
     const unsigned s_rcol = (unsigned)__cvta_generic_to_shared(Rs + sl * RLD);
     const unsigned s_r = (unsigned)__cvta_generic_to_shared(Rs);
-    const double* Xc = a.X + (int64_t)sl * a.ld;
     __syncwarp();
     for (int64_t t = 0; t < tiles; ++t) {
         const int64_t r0 = row0 + 32 * t;
         const int rows = (t < my_tiles) ? (int)((row1 - r0) < 32 ? (row1 - r0) : 32) : 0;
+        // coalesced: the stream's lanes walk down each column (32 rows = SW lanes x 32/SW)
+        for (int c = 0; c < m; ++c) {
+            const double* col = a.X + (int64_t)c * a.ld + r0;
+#pragma unroll
+            for (int h = 0; h < 32 / SW; ++h) {
+                const int i = sl + SW * h;
+                stg[c * kWsSld + i] = (i < rows) ? __ldcs(col + i) : 0.0;
+            }
+        }
+        __syncwarp();
         double x[32];
 #pragma unroll
-        for (int i = 0; i < 32; ++i) x[i] = (i < rows && sl < m) ? __ldcs(Xc + r0 + i) : 0.0;
+        for (int i = 0; i < 32; i += 2) {
+            const double2 v = (sl < m) ? *reinterpret_cast<const double2*>(stg + sl * kWsSld + i) : make_double2(0.0, 0.0);
+            x[i] = v.x;
+            x[i + 1] = v.y;
+        }
         for (int j = 0; j < m; ++j) {
             const bool piv = (sl == j);
 #pragma unroll
