@@ -51,7 +51,20 @@ typedef struct ttsvd_cu_tt ttsvd_cu_tt;   /* a TensorTrain result (tensor_train.
 typedef struct {
     int64_t rows, cols, nsig, rank;
     double t_tsqr_ms, t_svd_ms, t_tsmm_ms; /* device time, CUDA events */
+    double t_tsqr_sweep_ms;                /* the TSQR's main sweep kernel alone (no merge) */
+    int32_t tsqr_kernel;                   /* which: TTSVD_K_* below */
+    int32_t svd_sweeps;                    /* Jacobi sweeps of the step's small SVD */
 } ttsvd_cu_step;
+
+/* tsqr_kernel values (diagnostics) */
+enum {
+    TTSVD_K_NONE = 0,
+    TTSVD_K_WS = 1,    /* warp streams, m <= 32 */
+    TTSVD_K_V1 = 2,    /* block-per-job tiles, m <= 32 */
+    TTSVD_K_LA = 3,    /* 32-row look-ahead tiles */
+    TTSVD_K_T128 = 4,  /* 128-row tiles, one CTA per SM */
+    TTSVD_K_GQR = 5    /* cooperative whole-grid QR */
+};
 
 /* All-gather over the ranks of a distributed run (replaces the in-process
  * combine over partitions at tt_svd.hpp:568-575; Alg. 5's MPI_Allreduce,

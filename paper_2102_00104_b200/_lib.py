@@ -22,7 +22,12 @@ i64p = C.POINTER(C.c_int64)
 
 class Step(C.Structure):
     _fields_ = [("rows", i64), ("cols", i64), ("nsig", i64), ("rank", i64),
-                ("t_tsqr_ms", C.c_double), ("t_svd_ms", C.c_double), ("t_tsmm_ms", C.c_double)]
+                ("t_tsqr_ms", C.c_double), ("t_svd_ms", C.c_double), ("t_tsmm_ms", C.c_double),
+                ("t_tsqr_sweep_ms", C.c_double), ("tsqr_kernel", C.c_int32), ("svd_sweeps", C.c_int32)]
+
+
+TSQR_KERNELS = {0: "none", 1: "tsqr_ws_kernel", 2: "tsqr_tile_kernel", 3: "tsqr_la_kernel", 4: "tsqr_t128_kernel",
+                5: "gqr_kernel"}
 
 
 EXCHANGE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, i64, C.c_void_p)

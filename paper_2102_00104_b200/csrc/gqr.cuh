@@ -52,6 +52,25 @@ __device__ __forceinline__ double warp_reduce_scatter32(double (&v)[32], int lan
     return (b0 ? v[1] : v[0]) + __shfl_xor_sync(0xffffffffu, b0 ? v[0] : v[1], 1);
 }
 
+// sum over q = first, first + step, ... < G of base[q * qstride] (L2 reads,
+// data of other CTAs), four independent accumulators so the loads overlap; a
+// fixed association order, so every CTA computes bit-identical totals
+__device__ __forceinline__ double gqr_strided_sum(const double* base, int64_t qstride, int G, int first, int step) {
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    int q = first;
+    for (; q + 3 * step < G; q += 4 * step) {
+        const double v0 = __ldcg(base + (int64_t)q * qstride), v1 = __ldcg(base + (int64_t)(q + step) * qstride);
+        const double v2 = __ldcg(base + (int64_t)(q + 2 * step) * qstride),
+                     v3 = __ldcg(base + (int64_t)(q + 3 * step) * qstride);
+        a0 += v0;
+        a1 += v1;
+        a2 += v2;
+        a3 += v3;
+    }
+    for (; q < G; q += step) a0 += __ldcg(base + (int64_t)q * qstride);
+    return (a0 + a1) + (a2 + a3);
+}
+
 __host__ __device__ inline int gqr_ldy(int rows) { return ((((rows + 3) & ~3) + 7) & ~7) + 4; }
 
 inline size_t gqr_smem_bytes(int rows_max) {
@@ -127,9 +146,7 @@ __global__ void __launch_bounds__(kGqrThreads, 1) gqr_kernel(GqrArgs a) {
             // slice s = tid >> 5 sums CTAs q = s, s + 8, ...; then the 8 slices
             {
                 const int k = tid & 31, sl = tid >> 5;
-                double t = 0.0;
-                for (int q = sl; q < G; q += kGqrThreads / 32) t += __ldcg(&part[((int64_t)buf * G + q) * 33 + k]);
-                red[8 * 33 + sl * 33 + k] = t;
+                red[8 * 33 + sl * 33 + k] = gqr_strided_sum(part + (int64_t)buf * G * 33 + k, 33, G, sl, kGqrThreads / 32);
             }
             __syncthreads();
             if (tid < 32) {
@@ -213,9 +230,7 @@ __global__ void __launch_bounds__(kGqrThreads, 1) gqr_kernel(GqrArgs a) {
         __threadfence();
         grid.sync();
         for (int e = tid; e < 1024; e += kGqrThreads) {
-            double t = 0.0;
-            for (int q = 0; q < G; ++q) t += __ldcg(&part[(int64_t)2 * G * 33 + (int64_t)q * 1024 + e]);
-            Sm[(e >> 5) * 33 + (e & 31)] = t;
+            Sm[(e >> 5) * 33 + (e & 31)] = gqr_strided_sum(part + (int64_t)2 * G * 33 + e, 1024, G, 0, 1);
         }
         __syncthreads();
         if (warp == 0) {
@@ -259,11 +274,21 @@ __global__ void __launch_bounds__(kGqrThreads, 1) gqr_kernel(GqrArgs a) {
 #pragma unroll
             for (int mt = 0; mt < 4; ++mt) acc[mt][0] = acc[mt][1] = 0.0;
             const double* colp = A + (g + lr) * lda + r0;
-            for (int kk = 0; kk < rows4 / 4; ++kk) {
-                const int row = 4 * kk + lc;
-                const double b = row < rows ? colp[row] : 0.0;
+            for (int k0 = 0; k0 < rows4 / 4; k0 += 8) {
+                double bv[8];
 #pragma unroll
-                for (int mt = 0; mt < 4; ++mt) dmma884(acc[mt], Ys[(8 * mt + lr) * ldy + 4 * kk + lc], b);
+                for (int u = 0; u < 8; ++u) {
+                    const int row = 4 * (k0 + u) + lc;
+                    bv[u] = (k0 + u < rows4 / 4 && row < rows) ? colp[row] : 0.0;
+                }
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    if (k0 + u < rows4 / 4) {
+#pragma unroll
+                        for (int mt = 0; mt < 4; ++mt)
+                            dmma884(acc[mt], Ys[(8 * mt + lr) * ldy + 4 * (k0 + u) + lc], bv[u]);
+                    }
+                }
             }
 #pragma unroll
             for (int mt = 0; mt < 4; ++mt)
@@ -279,8 +304,7 @@ __global__ void __launch_bounds__(kGqrThreads, 1) gqr_kernel(GqrArgs a) {
             const int64_t ca = t0 + c * chunk, cb = (ca + chunk < M) ? ca + chunk : M;
             for (int64_t col = ca + warp; col < cb; col += kGqrThreads / 32) {
                 // lane k: W(k, col) summed over CTAs in order
-                double w = 0.0;
-                for (int q = 0; q < G; ++q) w += __ldcg(&pw[((int64_t)q * 32 + lane) * M + col]);
+                const double w = gqr_strided_sum(pw + (int64_t)lane * M + col, (int64_t)32 * M, G, 0, 1);
                 // W'(i, col) = sum_k T(k, i) W(k, col)
                 double wp = 0.0;
                 for (int k = 0; k < 32; ++k) wp = fma(Tm[k * 33 + lane], __shfl_sync(0xffffffffu, w, k), wp);

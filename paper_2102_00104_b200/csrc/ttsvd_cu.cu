@@ -68,7 +68,8 @@ struct ttsvd_cu_ctx {
     // grow-only device workspaces
     DevBuf ws_R, ws_R2, ws_P, ws_Scr, ws_G, ws_Gp, ws_A, ws_V, ws_Vacc, ws_U, ws_sigma, ws_flags, ws_work[2], ws_X, ws_send, ws_recv;
     DevBuf host_stage;  // pinned
-    cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+    cudaEvent_t ev[7] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+    int last_kernel = 0;  // TTSVD_K_* of the last tsqr_device main sweep (ev[5], ev[6] bracket it when timing)
 };
 
 struct ttsvd_cu_tt {
@@ -333,6 +334,12 @@ int merge_stack_gqr(ttsvd_cu_ctx* ctx, const double* parts, int64_t count, int m
 // R (m x m) of X (n x m, ld) — n may be smaller than m (the structured kernel
 // does not need n >= m; gram_triangular's square padding is implicit).
 // R_init (m x m) optionally seeds a single job (reduce_block).
+// events bracketing the main sweep kernel of tsqr_device (timing mode)
+inline void kmark(ttsvd_cu_ctx* ctx, int i, int kernel) {
+    if (ctx->timing) cudaEventRecord(ctx->ev[5 + i], ctx->stream);
+    ctx->last_kernel = kernel;
+}
+
 // m <= 32: warp streams (tsqr_ws.cuh), levels of stacked factors until one
 // stream is left.
 template <int SW>
@@ -360,8 +367,10 @@ int tsqr_ws_levels(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t
         const int64_t ldo = (S == 1) ? m : S * m;
         WsArgs wa{src, rows, sld, m, S, out, ldo};
         const int64_t grid = (S + per_cta - 1) / per_cta;
+        if (src == X) kmark(ctx, 0, TTSVD_K_WS);
         tsqr_ws_kernel<SW><<<(unsigned)grid, kWsThreads, smem, ctx->stream>>>(wa);
         TT_TRY(check_launch(ctx, "tsqr_ws_kernel"));
+        if (src == X) kmark(ctx, 1, TTSVD_K_WS);
         if (S == 1) return TTSVD_OK;
         src = out;
         rows = S * m;
@@ -376,14 +385,18 @@ int tsqr_ws_device(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t
 
 int tsqr_device(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t ld, double* R,
                 const double* R_init = nullptr) {
+    ctx->last_kernel = TTSVD_K_NONE;
     if (m > kSmallM) {
         const int M = (m + 31) / 32 * 32;
         const int64_t RS = blk_rsize(M);
         // Short-fat (n <= 256 M, n <= 512 rows per SM): one cooperative grid
         // factorises the whole matrix (gqr.cuh), no merge tree.
         if (!R_init && n >= M && n <= (int64_t)256 * M && !(std::getenv("TTSVD_TSQR") && std::string(std::getenv("TTSVD_TSQR")) == "t128")) {
+            kmark(ctx, 0, TTSVD_K_GQR);
             const int rc = gqr_device(ctx, X, n, m, ld, R);
+            kmark(ctx, 1, TTSVD_K_GQR);
             if (rc != -1) return rc;
+            ctx->last_kernel = 0;
         }
         // Tall tiles pay off for wide factors (M >= 384: the 32-row tiles of
         // tsqr_blk_kernel only fit one CTA per SM there); measured on config
@@ -407,8 +420,10 @@ int tsqr_device(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t ld
                 tattr = true;
             }
             T2Args ta{X, n, ld, parts, as<double>(ctx->ws_Scr), m, M};
+            kmark(ctx, 0, TTSVD_K_T128);
             tsqr_t128_kernel<<<(unsigned)Gt, kT2Threads, t2_smem_bytes(), ctx->stream>>>(ta);
             TT_TRY(check_launch(ctx, "tsqr_t128_kernel"));
+            kmark(ctx, 1, TTSVD_K_T128);
             static const bool prof = std::getenv("TTSVD_PROF_BLK") != nullptr;
             cudaEvent_t e0, e1;
             if (prof) {
@@ -456,7 +471,9 @@ int tsqr_device(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t ld
         long long* dprof = nullptr;
         if (prof) TT_CUDA(cudaMalloc(&dprof, (size_t)G * 8 * sizeof(long long)));
         a.prof = dprof;
+        kmark(ctx, 0, TTSVD_K_LA);
         TT_TRY(launch_blk(ctx, a, (int)G));
+        kmark(ctx, 1, TTSVD_K_LA);
         if (prof) {
             std::vector<long long> hp((size_t)G * 8);
             TT_CUDA(cudaMemcpy(hp.data(), dprof, hp.size() * 8, cudaMemcpyDeviceToHost));
@@ -491,7 +508,9 @@ int tsqr_device(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t ld
     TT_TRY(ensure(ctx->ws_R, (size_t)G * m * m * 8));
     double* parts = as<double>(ctx->ws_R);
     TsqrArgs a{X, n, ld, G == 1 ? R : parts, m, p.bt, p.ldb, 0, p.r_in_smem, R_init};
+    kmark(ctx, 0, TTSVD_K_V1);
     TT_TRY(launch_tsqr_kernel(ctx, a, (int)G, p.smem));
+    kmark(ctx, 1, TTSVD_K_V1);
     if (G == 1) return TTSVD_OK;
     return merge_tree(ctx, parts, G, m, R);
 }
@@ -813,7 +832,10 @@ int run_chain(ttsvd_cu_ctx* ctx, WorkView cur, const std::vector<int64_t>& dims,
             st.t_tsqr_ms = tm.ms(0, 1);
             st.t_svd_ms = tm.ms(1, 2);
             st.t_tsmm_ms = tm.ms(3, 4);
+            if (tall && ctx->last_kernel) st.t_tsqr_sweep_ms = tm.ms(5, 6);
         }
+        st.tsqr_kernel = tall ? ctx->last_kernel : TTSVD_K_NONE;
+        st.svd_sweeps = sweeps;
         out->steps.push_back(st);
         out->sigmas.push_back(sig);
         cur = WorkView{Y, out_rows, out_cols, ldy};

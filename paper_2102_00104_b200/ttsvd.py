@@ -373,6 +373,9 @@ class StepRecord:
     t_tsqr: float = 0.0
     t_small_svd: float = 0.0
     t_tsmm: float = 0.0
+    t_tsqr_sweep: float = 0.0  # the TSQR main sweep kernel alone (diagnostics)
+    tsqr_kernel: str = "none"
+    svd_sweeps: int = 0
 
 
 @dataclass
@@ -420,7 +423,8 @@ def _collect(handle: C.c_void_p) -> TensorTrain:
             _check(L.ttsvd_cu_tt_sigma(handle, s, sig.ctypes.data))
             steps.append(StepRecord(s + 1, st.rows, st.cols, st.rank, st.nsig,
                                     st.rank / st.cols if st.cols else 0.0, st.t_tsqr_ms * 1e-3, st.t_svd_ms * 1e-3,
-                                    st.t_tsmm_ms * 1e-3))
+                                    st.t_tsmm_ms * 1e-3, st.t_tsqr_sweep_ms * 1e-3,
+                                    _lib.TSQR_KERNELS.get(st.tsqr_kernel, "?"), st.svd_sweeps))
             tt.sigmas.append(sig)
         tt.steps = steps
         return tt, ranks
