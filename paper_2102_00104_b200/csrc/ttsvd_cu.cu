@@ -165,11 +165,6 @@ int launch_tsqr_kernel(ttsvd_cu_ctx* ctx, const TsqrArgs& a, int grid, size_t sm
 // ---- blocked DMMA path (m > 32) ----
 constexpr int kSmallM = 32;
 
-bool use_old_blk() {
-    static const char* t = std::getenv("TTSVD_TSQR");  // diagnostics: "blk" = the non-look-ahead kernel
-    return t && std::string(t) == "blk";
-}
-
 int set_la_attr() {
     static int done = 0;
     if (!done) {
@@ -183,16 +178,7 @@ int set_la_attr() {
 }
 
 int launch_blk(ttsvd_cu_ctx* ctx, const BlkArgs& a, int grid) {
-    static bool attr_set = false;
-    if (!attr_set) {
-        TT_CUDA(cudaFuncSetAttribute(tsqr_blk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit));
-        TT_TRY(set_la_attr());
-        attr_set = true;
-    }
-    if (use_old_blk()) {
-        tsqr_blk_kernel<<<grid, kBlkThreads, blk_smem_bytes(a.M), ctx->stream>>>(a);
-        return check_launch(ctx, "tsqr_blk_kernel");
-    }
+    TT_TRY(set_la_attr());
     tsqr_la_kernel<<<grid, kLaThreads, la_smem_bytes(a.M), ctx->stream>>>(a);
     return check_launch(ctx, "tsqr_la_kernel");
 }
@@ -398,14 +384,9 @@ int tsqr_device(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t ld
             if (rc != -1) return rc;
             ctx->last_kernel = 0;
         }
-        // Tall tiles pay off for wide factors (M >= 384: the 32-row tiles of
-        // tsqr_blk_kernel only fit one CTA per SM there); measured on config
-        // 2: 65536x512 41 -> see profiles, 2^20x256 40.4 ms tall vs 36.7 ms blk.
-        // Grid: one CTA per SM, at least 4 tiles of 128 rows per CTA (the
-        // merge tree costs ~M reflector steps per level, so very short row
-        // ranges do not pay).
-        // 128-row tiles, one CTA per SM, when every CTA gets >= 4 tiles
-        static const char* tsel = std::getenv("TTSVD_TSQR");  // diagnostics: "t128", "la", "blk"
+        // 128-row tiles, one CTA per SM, when every CTA gets >= 4 tiles (the
+        // 148 factors are merged by one cooperative QR of their stack)
+        static const char* tsel = std::getenv("TTSVD_TSQR");  // diagnostics: "t128", "la"
         const bool force_t128 = tsel && std::string(tsel) == "t128";
         const bool want_t128 = tsel ? force_t128 : true;
         if (!R_init && want_t128 && (n >= (int64_t)ctx->num_sms * 4 * kT2Rows || (force_t128 && n >= 4 * kT2Rows))) {
@@ -447,12 +428,8 @@ int tsqr_device(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t ld
             return copy_leading(ctx, as<double>(ctx->ws_P), M, m, R);
         }
         int per_sm = 1;
-        TT_CUDA(cudaFuncSetAttribute(tsqr_blk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit));
         TT_TRY(set_la_attr());
-        if (use_old_blk())
-            TT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tsqr_blk_kernel, kBlkThreads, blk_smem_bytes(M)));
-        else
-            TT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tsqr_la_kernel, kLaThreads, la_smem_bytes(M)));
+        TT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tsqr_la_kernel, kLaThreads, la_smem_bytes(M)));
         per_sm = std::max(1, per_sm);
         int64_t G = std::max<int64_t>(1, n / (4 * (int64_t)M));
         G = std::min<int64_t>(G, (int64_t)per_sm * ctx->num_sms);
