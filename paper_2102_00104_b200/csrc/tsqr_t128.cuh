@@ -11,13 +11,13 @@
 //     reference's zero rules, tsqr.hpp:120-160) and updates its rows;
 //   * warps 4..7 first apply panel p's block reflector to panel p+1's columns
 //     ("phase A", DMMA, result straight into the next panel buffer), then all
-//     twelve update warps apply it to the remaining columns while warps 0..3
+//     eight update warps apply it to the remaining columns while warps 0..3
 //     factor panel p+1;
 //   * the tile's trailing columns live in a per-CTA scratch in global memory
 //     (L2 resident, 128 x M doubles); panel 0 and the first trailing update of
 //     a tile read the input directly.
 // T of the compact WY form is built from S = V^T V, which falls out of the
-// panel's dot products (see la_panel).
+// panel's dot products, by the four panel warps (t2_build_t).
 #pragma once
 
 #include <cfloat>
@@ -26,7 +26,7 @@
 namespace ttsvd_b200 {
 
 constexpr int kT2Rows = 128;
-constexpr int kT2Threads = 512;
+constexpr int kT2Threads = 384;  // 4 panel warps + 8 update warps
 constexpr int kT2Pld = 132;  // smem ld of a panel buffer (128 rows + 4)
 
 struct T2Args {
@@ -35,6 +35,8 @@ struct T2Args {
     double* Rws;  // per-CTA packed R (blk_rsize(M))
     double* Scr;  // per-CTA tile scratch (kT2Rows x M, ld kT2Rows)
     int m, M;
+    long long* prof;  // optional per-CTA phase cycle counters (8 per CTA), diagnostics
+    int dbg;          // diagnostics only (timing experiments, wrong results): bit 0 skip the trailing update
 };
 
 inline size_t t2_smem_bytes() {
@@ -152,6 +154,78 @@ __device__ __forceinline__ void t2_panel(double* P, double* Rp, double* tau, dou
     t2_bar_panel();
 }
 
+// panel warps 0..3: T = (diag(1/tau) + striu(S))^{-1} (row-major, ld kLaTld)
+// by 8 x 8 diagonal blocks (warp k back-substitutes block k, lane j < 8 one
+// column) and two levels of [[A, B], [0, C]]^{-1} = [[A^-1, -A^-1 B C^-1],
+// [0, C^-1]]; X (16 x 16 scratch) holds the B C^-1 products.
+__device__ __forceinline__ void t2_build_t(const double* Sm, const double* tau, double* Tm, double* X, int warp,
+                                           int lane) {
+    {
+        const int b0 = 8 * warp, j = lane & 7;
+        double t[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) t[i] = (i == j) ? tau[b0 + j] : 0.0;
+#pragma unroll
+        for (int i = 6; i >= 0; --i) {
+            double acc = 0.0;
+#pragma unroll
+            for (int l = i + 1; l < 8; ++l) acc = fma(Sm[(b0 + i) * kTld + b0 + l], t[l], acc);
+            if (i < j) t[i] = -tau[b0 + i] * acc;
+        }
+        if (lane < 8) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) Tm[(b0 + i) * kLaTld + b0 + j] = t[i];
+            // the strictly lower blocks of this block row
+            for (int c = 0; c < b0; ++c)
+#pragma unroll
+                for (int i = 0; i < 8; ++i) Tm[(b0 + i) * kLaTld + c] = 0.0;
+        }
+    }
+    t2_bar_panel();
+    // level 1: blocks (0,1) by warp 0, (2,3) by warp 1: T_ab = -T_aa (S_ab T_bb)
+    if (warp < 2) {
+        const int a0 = 16 * warp, b0 = a0 + 8;
+        double* Xw = X + warp * 64;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int e = lane + 32 * h, i = e >> 3, j = e & 7;
+            double acc = 0.0;
+#pragma unroll
+            for (int l = 0; l < 8; ++l) acc = fma(Sm[(a0 + i) * kTld + b0 + l], Tm[(b0 + l) * kLaTld + b0 + j], acc);
+            Xw[i * 8 + j] = acc;
+        }
+        __syncwarp();
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int e = lane + 32 * h, i = e >> 3, j = e & 7;
+            double acc = 0.0;
+#pragma unroll
+            for (int l = 0; l < 8; ++l) acc = fma(Tm[(a0 + i) * kLaTld + a0 + l], Xw[l * 8 + j], acc);
+            Tm[(a0 + i) * kLaTld + b0 + j] = -acc;
+        }
+    }
+    t2_bar_panel();
+    // level 2: T[0:16, 16:32] = -T[0:16, 0:16] (S[0:16, 16:32] T[16:32, 16:32])
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const int e = 64 * warp + lane + 32 * h, i = e >> 4, j = e & 15;
+        double acc = 0.0;
+#pragma unroll
+        for (int l = 0; l < 16; ++l) acc = fma(Sm[i * kTld + 16 + l], Tm[(16 + l) * kLaTld + 16 + j], acc);
+        X[i * 16 + j] = acc;
+    }
+    t2_bar_panel();
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const int e = 64 * warp + lane + 32 * h, i = e >> 4, j = e & 15;
+        double acc = 0.0;
+#pragma unroll
+        for (int l = 0; l < 16; ++l) acc = fma(Tm[i * kLaTld + l], X[l * 16 + j], acc);
+        Tm[i * kLaTld + 16 + j] = -acc;
+    }
+    t2_bar_panel();
+}
+
 // one warp: apply panel p's block reflector (V: 128 x 32 in smem, ld kT2Pld;
 // T) to tile columns g..g+7 (source: input X or the scratch; destination:
 // scratch or a panel buffer) and to R(p, g..g+7).
@@ -263,6 +337,14 @@ __global__ void __launch_bounds__(kT2Threads, 1) tsqr_t128_kernel(T2Args a) {
     __syncthreads();
     const int npan = M / 32;
     const bool panel_warp = warp < 4;
+    long long t_prev = 0, t_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#define T2_PROF(ph)                                   \
+    if (a.prof && tid == 0) {                         \
+        const long long t_now = clock64();            \
+        if (t_prev) t_acc[ph] += t_now - t_prev;      \
+        t_prev = t_now;                               \
+    }
+    T2_PROF(7);
     const int uw = warp - 4;  // update warp index 0..11
     for (int64_t r0 = row0; r0 < row1; r0 += kT2Rows) {
         const int rows = (int)((row1 - r0) < kT2Rows ? (row1 - r0) : kT2Rows);
@@ -275,14 +357,14 @@ __global__ void __launch_bounds__(kT2Threads, 1) tsqr_t128_kernel(T2Args a) {
         }
         if (warp == 0) cp_async_wait_all();
         __syncthreads();
+        T2_PROF(0);
         if (panel_warp) {
             t2_panel(Pb, Rp, tau, pvall, dpart, Sm, warp, lane);
-            if (warp == 0) {
-                la_store_rdiag(Rp, R, lane, pol_r);
-                if (npan > 1) la_build_t(Sm, tau, Tm0, lane);
-            }
+            if (warp == 0) la_store_rdiag(Rp, R, lane, pol_r);
+            if (npan > 1) t2_build_t(Sm, tau, Tm0, dpart, warp, lane);
         }
         __syncthreads();
+        T2_PROF(0);
         for (int p = 0; p + 1 < npan; ++p) {
             const int c0 = 32 * p, nxt = c0 + 32;
             const double* V = Pb + (p & 1) * 32 * kT2Pld;
@@ -301,14 +383,15 @@ __global__ void __launch_bounds__(kT2Threads, 1) tsqr_t128_kernel(T2Args a) {
             }
             if (warp == 0) cp_async_wait_all();
             __syncthreads();
+            T2_PROF(1);
             if (panel_warp) {
                 t2_panel(Pn, Rp, tau, pvall, dpart, Sm, warp, lane);
-                if (warp == 0) {
-                    la_store_rdiag(Rp, R + blk_roff(p + 1, M), lane, pol_r);
-                    if (p + 2 < npan) la_build_t(Sm, tau, Tm0 + ((p + 1) & 1) * 32 * kLaTld, lane);
-                }
-            } else {
-                for (int g = nxt + 32 + 8 * uw; g < M; g += 8 * 12) {
+                T2_PROF(2);
+                if (warp == 0) la_store_rdiag(Rp, R + blk_roff(p + 1, M), lane, pol_r);
+                if (p + 2 < npan) t2_build_t(Sm, tau, Tm0 + ((p + 1) & 1) * 32 * kLaTld, dpart, warp, lane);
+                T2_PROF(3);
+            } else if (!(a.dbg & 1)) {
+                for (int g = nxt + 32 + 8 * uw; g < M; g += 8 * (kT2Threads / 32 - 4)) {
                     if (p == 0)
                         t2_group<true, false>(Xt, a.ld, rows, m, Scr, kT2Rows, V, Tp, Rrow, c0, g, g, lane, pol_x, pol_r);
                     else
@@ -317,8 +400,12 @@ __global__ void __launch_bounds__(kT2Threads, 1) tsqr_t128_kernel(T2Args a) {
                 }
             }
             __syncthreads();
+            T2_PROF(4);
         }
     }
+    if (a.prof && tid == 0)
+        for (int q = 0; q < 8; ++q) a.prof[blockIdx.x * 8 + q] = t_acc[q];
+#undef T2_PROF
 }
 
 }  // namespace ttsvd_b200

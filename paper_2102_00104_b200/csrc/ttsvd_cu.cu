@@ -400,11 +400,27 @@ int tsqr_device(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t ld
                                              (int)t2_smem_bytes()));
                 tattr = true;
             }
-            T2Args ta{X, n, ld, parts, as<double>(ctx->ws_Scr), m, M};
+            static const bool tprof = std::getenv("TTSVD_PROF_BLK") != nullptr;
+            long long* dprof = nullptr;
+            if (tprof) TT_CUDA(cudaMalloc(&dprof, (size_t)Gt * 8 * sizeof(long long)));
+            static const char* tdbg = std::getenv("TTSVD_BLK_DBG");  // diagnostics only: wrong results by design
+            T2Args ta{X, n, ld, parts, as<double>(ctx->ws_Scr), m, M, dprof, tdbg ? std::atoi(tdbg) : 0};
             kmark(ctx, 0, TTSVD_K_T128);
             tsqr_t128_kernel<<<(unsigned)Gt, kT2Threads, t2_smem_bytes(), ctx->stream>>>(ta);
             TT_TRY(check_launch(ctx, "tsqr_t128_kernel"));
             kmark(ctx, 1, TTSVD_K_T128);
+            if (tprof) {
+                std::vector<long long> hp((size_t)Gt * 8);
+                TT_CUDA(cudaMemcpy(hp.data(), dprof, hp.size() * 8, cudaMemcpyDeviceToHost));
+                cudaFree(dprof);
+                double ph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+                for (int64_t g = 0; g < Gt; ++g)
+                    for (int q = 0; q < 8; ++q) ph[q] += (double)hp[g * 8 + q] / Gt;
+                const double tiles = (double)n / Gt / kT2Rows;
+                std::fprintf(stderr, "[t128 prof] n=%lld m=%d tiles/CTA=%.1f per tile kcyc: load+panel0 %.1f, phaseA %.1f, panel %.1f, T+store %.1f, trailing wait %.1f\n",
+                             (long long)n, m, tiles, ph[0] / tiles / 1e3, ph[1] / tiles / 1e3, ph[2] / tiles / 1e3,
+                             ph[3] / tiles / 1e3, ph[4] / tiles / 1e3);
+            }
             static const bool prof = std::getenv("TTSVD_PROF_BLK") != nullptr;
             cudaEvent_t e0, e1;
             if (prof) {
