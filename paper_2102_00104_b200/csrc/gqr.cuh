@@ -35,7 +35,14 @@ struct GqrArgs {
     double* part;    // reduction partials: 2 x G x 33 (reflectors), G x 32 x 32 (S), G x 32 x M (W)
     double* piv;     // 2 x 32: the pivot row of the current reflector
     double* Wfin;    // 32 x M: W' = T^T W of the current panel
+    long long* prof; // optional (diagnostics): CTA 0 cycle sums [stage, reflectors, writeback+S+T, W partial, W reduce, update]
 };
+
+__device__ __forceinline__ long long gqr_clock() {
+    long long t;
+    asm volatile("mov.u64 %0, %%clock64;" : "=l"(t)::"memory");
+    return t;
+}
 
 // 32 per-lane values -> lane k holds the warp sum of value k (butterfly
 // reduce-scatter: 16 + 8 + 4 + 2 + 1 shuffles)
@@ -101,6 +108,14 @@ __global__ void __launch_bounds__(kGqrThreads, 1) gqr_kernel(GqrArgs a) {
     double* A = a.A;
     const int lr = lane >> 2, lc = lane & 3;
 
+    const bool pf = a.prof && c == 0 && tid == 0;
+    long long tpv = pf ? gqr_clock() : 0;
+#define GQR_PROF(ph)                          \
+    if (pf) {                                 \
+        const long long tn = gqr_clock();     \
+        a.prof[ph] += tn - tpv;               \
+        tpv = tn;                             \
+    }
     for (int p = 0; p < M / 32; ++p) {
         const int64_t c0 = 32 * (int64_t)p;
         // ---- stage my rows of the panel ----
@@ -110,9 +125,11 @@ __global__ void __launch_bounds__(kGqrThreads, 1) gqr_kernel(GqrArgs a) {
         }
         __syncthreads();
         // ---- 32 reflectors, one grid barrier each ----
+        GQR_PROF(0);
         for (int jj = 0; jj < 32; ++jj) {
             const int64_t j = c0 + jj;
             const int buf = jj & 1;
+            long long tr0 = pf ? gqr_clock() : 0;
             // partials over my rows below the pivot: v[0] = sum x_j^2, v[k] = sum x_j x_k (k > jj)
             double v[32];
 #pragma unroll
@@ -140,13 +157,18 @@ __global__ void __launch_bounds__(kGqrThreads, 1) gqr_kernel(GqrArgs a) {
                 for (int w = 0; w < kGqrThreads / 32; ++w) t += red[w * 33 + tid];
                 part[((int64_t)buf * G + c) * 33 + tid] = t;
             }
-            __threadfence();
+            long long tq0 = pf ? gqr_clock() : 0;
+            if (pf) a.prof[6] += tq0 - tr0;
+            // grid.sync orders the partials: its barrier is preceded by a
+            // device-scope fence on behalf of the whole CTA
             grid.sync();
             // totals in a fixed order (identical on every CTA): value k = tid & 31,
             // slice s = tid >> 5 sums CTAs q = s, s + 8, ...; then the 8 slices
             {
                 const int k = tid & 31, sl = tid >> 5;
+                const double pv = (sl == 0) ? __ldcg(&a.piv[buf * 32 + k]) : 0.0;  // in flight with the sums
                 red[8 * 33 + sl * 33 + k] = gqr_strided_sum(part + (int64_t)buf * G * 33 + k, 33, G, sl, kGqrThreads / 32);
+                if (sl == 0) red[33 + k] = pv;
             }
             __syncthreads();
             if (tid < 32) {
@@ -154,9 +176,12 @@ __global__ void __launch_bounds__(kGqrThreads, 1) gqr_kernel(GqrArgs a) {
 #pragma unroll
                 for (int sl = 0; sl < kGqrThreads / 32; ++sl) t += red[8 * 33 + sl * 33 + tid];
                 red[tid] = t;
-                red[33 + tid] = __ldcg(&a.piv[buf * 32 + tid]);
             }
             __syncthreads();
+            if (pf) {
+                const long long tq1 = gqr_clock();
+                a.prof[7] += tq1 - tq0;
+            }
             const double sp = red[0];
             const double u0 = red[33 + jj];
             const double nrm2 = u0 * u0 + sp;
@@ -199,6 +224,7 @@ __global__ void __launch_bounds__(kGqrThreads, 1) gqr_kernel(GqrArgs a) {
             if (tid == 0) tau[jj] = tj;
             __syncthreads();
         }
+        GQR_PROF(1);
         // ---- write back the panel (R rows and v), then the structured Y in smem ----
         for (int e = tid; e < 32 * ldy; e += kGqrThreads) {
             const int k = e / ldy, i = e - k * ldy;
@@ -264,6 +290,7 @@ __global__ void __launch_bounds__(kGqrThreads, 1) gqr_kernel(GqrArgs a) {
             }
             __syncthreads();
         }
+        GQR_PROF(2);
         // ---- W partial = Y_c^T A(rows_c, trail): DMMA, K = my rows ----
         const int64_t t0 = c0 + 32;
         const int ngr = (int)((M - t0) / 8);
@@ -297,6 +324,7 @@ __global__ void __launch_bounds__(kGqrThreads, 1) gqr_kernel(GqrArgs a) {
         }
         __threadfence();
         grid.sync();
+        GQR_PROF(3);
         // ---- reduce W over the CTAs (column chunks), W' = T^T W -> Wfin ----
         {
             const int64_t ncols = M - t0;
@@ -313,6 +341,7 @@ __global__ void __launch_bounds__(kGqrThreads, 1) gqr_kernel(GqrArgs a) {
         }
         __threadfence();
         grid.sync();
+        GQR_PROF(4);
         // ---- A(rows_c, trail) -= Y_c W': DMMA per 8-column group, 64-row chunks ----
         for (int gq = warp; gq < ngr; gq += kGqrThreads / 32) {
             const int64_t g = t0 + 8 * gq;
@@ -351,7 +380,9 @@ __global__ void __launch_bounds__(kGqrThreads, 1) gqr_kernel(GqrArgs a) {
         }
         __threadfence();
         grid.sync();
+        GQR_PROF(5);
     }
+#undef GQR_PROF
 }
 
 // count packed panel-major factors (blk_rsize(M) each) -> the dense stacked

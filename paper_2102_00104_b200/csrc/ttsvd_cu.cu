@@ -294,11 +294,25 @@ int gqr_device(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t ld,
         if (M > m) TT_CUDA(cudaMemsetAsync(Aw + (size_t)n * m, 0, (size_t)n * (M - m) * 8, ctx->stream));
     }
     double* pp = as<double>(ctx->ws_Gp);
-    GqrArgs ga{Aw, n, n, m, M, pp, pp + np, pp + np + 64};
+    static const bool prof = std::getenv("TTSVD_PROF_GQR") != nullptr;
+    long long* dprof = nullptr;
+    if (prof) {
+        TT_CUDA(cudaMalloc(&dprof, 8 * sizeof(long long)));
+        TT_CUDA(cudaMemset(dprof, 0, 8 * sizeof(long long)));
+    }
+    GqrArgs ga{Aw, n, n, m, M, pp, pp + np, pp + np + 64, dprof};
     void* args[] = {&ga};
     TT_CUDA(cudaLaunchCooperativeKernel((const void*)gqr_kernel, dim3((unsigned)Gq), dim3(kGqrThreads), args, smem,
                                         ctx->stream));
     TT_TRY(check_launch(ctx, "gqr_kernel"));
+    if (prof) {
+        long long h[8];
+        TT_CUDA(cudaMemcpy(h, dprof, sizeof(h), cudaMemcpyDeviceToHost));
+        cudaFree(dprof);
+        std::fprintf(stderr, "[gqr prof] n=%lld m=%d G=%lld kcyc: stage %.0f reflectors %.0f (%.2f per refl) S+T %.0f Wpart %.0f Wred %.0f update %.0f | per refl: partials %.2f, fence+sync+sums %.2f\n",
+                     (long long)n, m, (long long)Gq, h[0] / 1e3, h[1] / 1e3, h[1] / 1e3 / M, h[2] / 1e3, h[3] / 1e3,
+                     h[4] / 1e3, h[5] / 1e3, h[6] / 1e3 / M, h[7] / 1e3 / M);
+    }
     gqr_extract_kernel<<<std::max(1, std::min(1024, (m * m + 255) / 256)), 256, 0, ctx->stream>>>(Aw, n, m, R);
     return check_launch(ctx, "gqr_extract_kernel");
 }
