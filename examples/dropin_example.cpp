@@ -19,6 +19,8 @@ int main(int argc, char** argv) {
         return 4;
     } catch (const DegenerateDimension&) {
     }
+    if (choose_combined_dims({4, 4, 4, 4, 4, 4, 4, 4, 4, 4}, ThickBoundsParams{}, 16) != std::make_pair<index_t, index_t>(3, 64))
+        return 6;
     if (argc > 1 && std::strcmp(argv[1], "host") == 0) {
         std::printf("host entry points ok\n");
         return 0;
@@ -33,6 +35,10 @@ int main(int argc, char** argv) {
     std::printf("ranks:");
     for (auto v : r) std::printf(" %lld", static_cast<long long>(v));
     std::printf("\n");
+    ThickBoundsParams tb;
+    tb.m_min = 8;
+    TensorTrain tk = tt_svd_thick_bounds(X, spec, tb);
+    if (tk.cores.size() != 8 || tk.ranks().back() != 1) return 7;
     PaddedMatrix M(1000, 4);
     for (index_t j = 0; j < 4; ++j) M(j, j) = 1.0;
     TriangularFactor R = tsqr(M.view(), BlockParams::for_cols(4), 1);

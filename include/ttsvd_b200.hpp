@@ -9,6 +9,7 @@
 //   jacobi_svd       small_svd.hpp:120   select_rank      small_svd.hpp:49
 //   derive_delta     small_svd.hpp:41    tsmm_reshape     tsmm.hpp:20, :74
 //   tt_svd_tsqr      tt_svd.hpp:281      tt_svd_distributed tt_svd.hpp:520
+//   choose_combined_dims tt_svd.hpp:316  tt_svd_thick_bounds tt_svd.hpp:338
 //
 // Host views are staged to the device and results copied back (the
 // reference's by-value contract); the Device* overloads keep data resident.
@@ -20,6 +21,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <utility>
 #include <limits>
 #include <stdexcept>
 #include <string>
@@ -414,6 +416,43 @@ inline TensorTrain tt_svd_tsqr(const double* X_device, const std::vector<index_t
     b200::check(ttsvd_cu_tt_svd(b200::context(), X_device, dims.data(), static_cast<index_t>(dims.size()), ld, rmax,
                                 spec.eps, &h));
     return b200::collect(h, dims);
+}
+
+// tt_svd.hpp:292-310
+struct ThickBoundsParams {
+    index_t m_min = 16;
+    double f1_min = 0.5;
+    std::vector<index_t> r_tilde;  // empty = derive from r_max
+};
+
+// tt_svd.hpp:316-330
+inline std::pair<index_t, index_t> choose_combined_dims(const std::vector<index_t>& dims,
+                                                        const ThickBoundsParams& params,
+                                                        index_t r_max = std::numeric_limits<index_t>::max()) {
+    index_t k = 0, m = 0;
+    const index_t rmax = r_max == std::numeric_limits<index_t>::max() ? 0 : r_max;
+    b200::check(ttsvd_cu_choose_combined_dims(dims.data(), static_cast<index_t>(dims.size()), params.m_min,
+                                              params.f1_min, params.r_tilde.empty() ? nullptr : params.r_tilde.data(),
+                                              static_cast<index_t>(params.r_tilde.size()), rmax, &k, &m));
+    return {k, m};
+}
+
+// tt_svd.hpp:338 (Alg. 3): the tensor is staged to the device, then merged,
+// swept and recovered there
+inline TensorTrain tt_svd_thick_bounds(const DenseTensor& X, TruncationSpec spec, const ThickBoundsParams& params,
+                                       const ExecContext& = {}) {
+    const index_t d = static_cast<index_t>(X.dims().size());
+    if (d < 2) throw DegenerateDimension("tt_svd_thick_bounds: requires d >= 2");
+    const index_t rmax = spec.r_max == std::numeric_limits<index_t>::max() ? 0 : spec.r_max;
+    const index_t cols = X.dims()[static_cast<std::size_t>(d - 1)];
+    b200::DeviceBuffer dx(static_cast<std::size_t>(X.leading_stride() * cols));
+    dx.upload(X.data(), dx.size());
+    ttsvd_cu_tt* h = nullptr;
+    b200::check(ttsvd_cu_tt_svd_thick(b200::context(), dx.get(), X.dims().data(), d, X.leading_stride(), rmax,
+                                      spec.eps, params.m_min, params.f1_min,
+                                      params.r_tilde.empty() ? nullptr : params.r_tilde.data(),
+                                      static_cast<index_t>(params.r_tilde.size()), &h));
+    return b200::collect(h, X.dims());
 }
 
 inline TensorTrain tt_svd_distributed(const std::vector<DenseTensor>& slabs, TruncationSpec spec,

@@ -111,6 +111,9 @@ class Oracle:
             f("tensor_new").argtypes = [dptr, i64ptr, i64, i64]
             f("tensor_free").argtypes = [C.c_void_p]
             f("tt_svd_tsqr_tensor").argtypes = [C.c_void_p, i64, C.c_double, C.c_int, i64ptr]
+            f("choose_combined_dims").argtypes = [i64ptr, i64, i64, C.c_double, C.c_void_p, i64, i64, i64ptr, i64ptr]
+            f("tt_svd_thick_bounds").argtypes = [dptr, i64ptr, i64, i64, i64, C.c_double, i64, C.c_double,
+                                                 C.c_void_p, i64, C.c_int, i64ptr, dptr, i64, i64ptr]
             L.ref_set_budget(1 << 40)
 
     def _f(self, name):
@@ -257,6 +260,37 @@ class Oracle:
         if P == 1:
             gdims[0] = 1
         return ranks.tolist(), split_cores(cores, gdims, ranks)
+
+    def choose_combined_dims(self, dims, m_min: int = 16, f1_min: float = 0.5, r_tilde=(), r_max: int = 2 ** 62):
+        """Reference only (tt_svd.hpp:316-330)."""
+        dims = np.ascontiguousarray(dims, dtype=np.int64)
+        rt = np.ascontiguousarray(r_tilde, dtype=np.int64)
+        k, m = np.zeros(1, dtype=np.int64), np.zeros(1, dtype=np.int64)
+        self._check(self._f("choose_combined_dims")(_pi(dims), len(dims), m_min, f1_min,
+                                                    rt.ctypes.data if len(rt) else None, len(rt), r_max, _pi(k),
+                                                    _pi(m)), "choose_combined_dims")
+        return int(k[0]), int(m[0])
+
+    def tt_svd_thick_bounds(self, X: np.ndarray, dims, ld: int, r_max: int, eps: float = 0.0, m_min: int = 16,
+                            f1_min: float = 0.5, r_tilde=(), workers: int = 1):
+        """Reference only (tt_svd.hpp:338, Alg. 3).  Returns (ranks, cores)."""
+        dims = np.ascontiguousarray(dims, dtype=np.int64)
+        rt = np.ascontiguousarray(r_tilde, dtype=np.int64)
+        d = len(dims)
+        ranks = np.zeros(d + 1, dtype=np.int64)
+        need = np.zeros(1, dtype=np.int64)
+        cap = max(1, min(int(np.prod(dims)), 1 << 22))
+        while True:
+            cores = np.zeros(cap)
+            rc = self._f("tt_svd_thick_bounds")(_p(X), _pi(dims), d, ld, r_max, eps, m_min, f1_min,
+                                                rt.ctypes.data if len(rt) else None, len(rt), workers, _pi(ranks),
+                                                _p(cores), cap, _pi(need))
+            if rc == 11:
+                cap = int(need[0])
+                continue
+            self._check(rc, "tt_svd_thick_bounds")
+            break
+        return ranks.tolist(), split_cores(cores, dims, ranks)
 
     def tt_error(self, X: np.ndarray, ld: int, dims, ranks, cores: list[np.ndarray]) -> float:
         dims = np.ascontiguousarray(dims, dtype=np.int64)

@@ -168,6 +168,38 @@ int ref_tt_svd_tsqr(const double* X, const int64_t* dims, int64_t d, int64_t ldx
     } catch (const std::exception& e) { return code_of(e); }
 }
 
+// tt_svd.hpp:316-330 and tt_svd.hpp:338 (Alg. 3)
+int ref_choose_combined_dims(const int64_t* dims, int64_t d, int64_t m_min, double f1_min, const int64_t* r_tilde,
+                             int64_t n_r_tilde, int64_t r_max, int64_t* k_out, int64_t* m_out) {
+    try {
+        ThickBoundsParams p;
+        p.m_min = m_min;
+        p.f1_min = f1_min;
+        if (r_tilde) p.r_tilde.assign(r_tilde, r_tilde + n_r_tilde);
+        const auto km = choose_combined_dims(Shape(std::vector<index_t>(dims, dims + d)), p, r_max);
+        *k_out = km.first;
+        *m_out = km.second;
+        return 0;
+    } catch (const std::exception& e) { return code_of(e); }
+}
+
+int ref_tt_svd_thick_bounds(const double* X, const int64_t* dims, int64_t d, int64_t ldx, int64_t r_max, double eps,
+                            int64_t m_min, double f1_min, const int64_t* r_tilde, int64_t n_r_tilde, int workers,
+                            int64_t* ranks, double* cores, int64_t cap, int64_t* needed) {
+    try {
+        DenseTensor t = tensor_from(X, dims, d, ldx);
+        ThickBoundsParams p;
+        p.m_min = m_min;
+        p.f1_min = f1_min;
+        if (r_tilde) p.r_tilde.assign(r_tilde, r_tilde + n_r_tilde);
+        ExecContext ctx;
+        ctx.threads = workers;
+        ctx.validate_reflectors = false;
+        TensorTrain tt = tt_svd_thick_bounds(t, spec_of(r_max, eps), p, ctx);
+        return export_tt(tt, ranks, cores, cap, needed);
+    } catch (const std::exception& e) { return code_of(e); }
+}
+
 // Timing entry for the CPU baseline: the input is already a reference
 // DenseTensor built once by ref_tensor_new, so only tt_svd_tsqr is timed.
 void* ref_tensor_new(const double* X, const int64_t* dims, int64_t d, int64_t ldx) {

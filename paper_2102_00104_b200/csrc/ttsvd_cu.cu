@@ -66,7 +66,7 @@ struct ttsvd_cu_ctx {
     int64_t launches = 0;
     bool timing = false;
     // grow-only device workspaces
-    DevBuf ws_R, ws_R2, ws_P, ws_Scr, ws_G, ws_Gp, ws_A, ws_V, ws_Vacc, ws_U, ws_sigma, ws_flags, ws_work[2], ws_X, ws_send, ws_recv;
+    DevBuf ws_R, ws_R2, ws_P, ws_Scr, ws_G, ws_Gp, ws_A, ws_V, ws_Vacc, ws_U, ws_sigma, ws_flags, ws_work[2], ws_X, ws_send, ws_recv, ws_thick[2];
     DevBuf host_stage;  // pinned
     cudaEvent_t ev[7] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
     int last_kernel = 0;  // TTSVD_K_* of the last tsqr_device main sweep (ev[5], ev[6] bracket it when timing)
@@ -769,13 +769,18 @@ int d2h(ttsvd_cu_ctx* ctx, double* dst, const double* src, size_t count) {
 }
 
 // Alg. 2 loop (tt_svd.hpp:159-199).
+// delta_io: in, a truncation parameter (< 0: derive it from the first step,
+// small_svd.hpp:41 — run_chain takes the spec by reference, tt_svd.hpp:160);
+// out, the one used.  first_sigma_norm_out: ||Sigma||_F of the first step
+// (ChainResult::first_sigma_norm, tt_svd.hpp:153-156).
 int run_chain(ttsvd_cu_ctx* ctx, WorkView cur, const std::vector<int64_t>& dims, int64_t r_max, double eps,
-              int64_t d_for_delta, ttsvd_cu_tt* out) {
+              int64_t d_for_delta, ttsvd_cu_tt* out, double* delta_io = nullptr,
+              double* first_sigma_norm_out = nullptr) {
     const int64_t d = (int64_t)dims.size();
     out->dims = dims;
     out->cores.assign(d, {});
     out->ranks.assign(d + 1, 1);
-    double delta = -1.0;
+    double delta = delta_io ? *delta_io : -1.0;
     int64_t r = 1;
     int which = 0;
     Timer tm(ctx);
@@ -809,9 +814,11 @@ int run_chain(ttsvd_cu_ctx* ctx, WorkView cur, const std::vector<int64_t>& dims,
         tm.mark(2);
         sig.resize(nsig);
         TT_TRY(d2h(ctx, sig.data(), d_sigma, nsig));
+        if (i == d - 1 && first_sigma_norm_out) *first_sigma_norm_out = sigma_norm_h(sig.data(), nsig);
         if (delta < 0.0) {
             if (d_for_delta < 2) return fail(TTSVD_ERR_DEGENERATE, "derive_delta: requires d >= 2");
             delta = eps / std::sqrt((double)(d_for_delta - 1)) * sigma_norm_h(sig.data(), nsig);
+            if (delta_io) *delta_io = delta;
         }
         const int64_t rnew = choose_rank_h(sig.data(), nsig, cur.cols, nsig, delta, r_max, cur.rows);
         st.nsig = nsig;
@@ -912,7 +919,7 @@ int ttsvd_cu_ctx_destroy(ttsvd_cu_ctx* ctx) {
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
     for (DevBuf* b : {&ctx->ws_R, &ctx->ws_R2, &ctx->ws_P, &ctx->ws_Scr, &ctx->ws_G, &ctx->ws_Gp, &ctx->ws_A, &ctx->ws_V, &ctx->ws_Vacc, &ctx->ws_U, &ctx->ws_sigma, &ctx->ws_flags, &ctx->ws_work[0],
-                      &ctx->ws_work[1], &ctx->ws_X, &ctx->ws_send, &ctx->ws_recv})
+                      &ctx->ws_work[1], &ctx->ws_X, &ctx->ws_send, &ctx->ws_recv, &ctx->ws_thick[0], &ctx->ws_thick[1]})
         if (b->p) cudaFree(b->p);
     if (ctx->host_stage.p) cudaFreeHost(ctx->host_stage.p);
     for (auto& e : ctx->ev)
@@ -1063,6 +1070,129 @@ int ttsvd_cu_tt_svd(ttsvd_cu_ctx* ctx, const double* X, const int64_t* dims, int
         delete tt;
         return rc;
     }
+    *out = tt;
+    return TTSVD_OK;
+}
+
+int ttsvd_cu_choose_combined_dims(const int64_t* dims, int64_t d, int64_t m_min, double f1_min, const int64_t* r_tilde,
+                                  int64_t n_r_tilde, int64_t r_max, int64_t* k_out, int64_t* m_out) {
+    if (!dims || !k_out || !m_out) return fail(TTSVD_ERR_INVALID, "choose_combined_dims: null argument");
+    if (d < 2) return fail(TTSVD_ERR_DEGENERATE, "choose_combined_dims: requires d >= 2");
+    if (m_min < 1 || !(f1_min > 0.0) || f1_min > 1.0)
+        return fail(TTSVD_ERR_DIMENSION_MISMATCH, "choose_combined_dims: invalid parameters");
+    if (r_max <= 0) r_max = INT64_MAX;
+    int64_t total = 1;
+    for (int64_t i = 0; i < d; ++i) total *= dims[i];
+    // ThickBoundsParams::estimate_at (tt_svd.hpp:298-309)
+    auto estimate_at = [&](int64_t pos) {
+        int64_t lead = 1;
+        for (int64_t i = 0; i < pos; ++i) lead *= dims[i];
+        const int64_t cap = std::min(lead, total / lead);
+        int64_t rt = r_max;
+        if (r_tilde && n_r_tilde > 0) rt = r_tilde[std::min(pos - 1, n_r_tilde - 1)];
+        return std::min(rt, cap);
+    };
+    int64_t trail = 1;
+    for (int64_t k = 1; k < d; ++k) {
+        trail *= dims[d - k];
+        const double need = std::max((double)m_min, (double)estimate_at(d - k) / f1_min);
+        if ((double)trail >= need) {
+            *k_out = k;
+            *m_out = trail;
+            return TTSVD_OK;
+        }
+    }
+    *k_out = d - 1;
+    *m_out = total / dims[0];
+    return TTSVD_OK;
+}
+
+int ttsvd_cu_tt_svd_thick(ttsvd_cu_ctx* ctx, const double* X, const int64_t* dims, int64_t d, int64_t ldx,
+                          int64_t r_max, double eps, int64_t m_min, double f1_min, const int64_t* r_tilde,
+                          int64_t n_r_tilde, ttsvd_cu_tt** out) {
+    TT_TRY(set_device(ctx));
+    if (!out || !dims || !X) return fail(TTSVD_ERR_INVALID, "tt_svd_thick: null argument");
+    *out = nullptr;
+    if (d < 2) return fail(TTSVD_ERR_DEGENERATE, "tt_svd_thick_bounds: requires d >= 2");
+    int64_t total = 1;
+    for (int64_t i = 0; i < d; ++i) {
+        if (dims[i] < 1) return fail(TTSVD_ERR_DIMENSION, "Shape: extents must be >= 1");
+        total *= dims[i];
+    }
+    if (r_max <= 0) r_max = INT64_MAX;
+    const int64_t rows0 = total / dims[d - 1];
+    if (ldx < rows0) return fail(TTSVD_ERR_LAYOUT, "tt_svd_thick: leading stride below the row count");
+    int64_t k = 1, m = dims[d - 1];
+    TT_TRY(ttsvd_cu_choose_combined_dims(dims, d, m_min, f1_min, r_tilde, n_r_tilde, r_max, &k, &m));
+    if (k == 1) return ttsvd_cu_tt_svd(ctx, X, dims, d, ldx, r_max, eps, out);
+
+    // merged tensor (n_1, ..., n_{d-k}, m) in its own padded layout (copy_logical,
+    // storage.hpp:158-172): column x of its matricization is the contiguous run
+    // of X's column x / q starting at row (x mod q) (N/m), q = m / n_d
+    const int64_t rows_m = total / m, ldm = padded_stride_h(rows_m), q = m / dims[d - 1];
+    TT_TRY(ensure(ctx->ws_thick[0], (size_t)ldm * m * 8));
+    double* W = as<double>(ctx->ws_thick[0]);
+    for (int64_t id = 0; id < dims[d - 1]; ++id)
+        TT_CUDA(cudaMemcpy2DAsync(W + id * q * ldm, (size_t)ldm * 8, X + id * ldx, (size_t)rows_m * 8,
+                                  (size_t)rows_m * 8, (size_t)q, cudaMemcpyDeviceToDevice, ctx->stream));
+    std::vector<int64_t> mdims(dims, dims + d - k);
+    mdims.push_back(m);
+    const int64_t dm = (int64_t)mdims.size();
+    ttsvd_cu_tt main_tt;
+    double delta = -1.0, fsn = 0.0;
+    TT_TRY(run_chain(ctx, WorkView{W, rows_m, m, ldm}, mdims, r_max, eps, dm, &main_tt, &delta, &fsn));
+
+    // recovery: TT-SVD of the combined core T_bar (r_b x m) as the (k+1)-mode
+    // tensor (r_b, n_{d-k+1}, ..., n_d) (tt_svd.hpp:350-371)
+    const std::vector<double>& tbar = main_tt.cores[dm - 1];
+    const int64_t rb = main_tt.ranks[dm - 1];
+    std::vector<int64_t> rdims{rb};
+    for (int64_t i = d - k; i < d; ++i) rdims.push_back(dims[i]);
+    const int64_t rrows = rb * m / dims[d - 1], ldr = padded_stride_h(rrows);
+    std::vector<double> hr((size_t)ldr * dims[d - 1], 0.0);
+    double tnorm = 0.0;
+    for (int64_t l = 0; l < rb * m; ++l) {
+        hr[(size_t)((l / rrows) * ldr + l % rrows)] = tbar[(size_t)l];
+        tnorm += tbar[(size_t)l] * tbar[(size_t)l];
+    }
+    TT_TRY(ensure(ctx->ws_thick[1], hr.size() * 8));
+    double* Rw = as<double>(ctx->ws_thick[1]);
+    TT_CUDA(cudaMemcpyAsync(Rw, hr.data(), hr.size() * 8, cudaMemcpyHostToDevice, ctx->stream));
+    double rdelta = delta * std::sqrt(tnorm) / (fsn > 0.0 ? fsn : 1.0);
+    ttsvd_cu_tt rec_tt;
+    TT_TRY(run_chain(ctx, WorkView{Rw, rrows, dims[d - 1], ldr}, rdims, r_max, eps, (int64_t)rdims.size(), &rec_tt,
+                     &rdelta, nullptr));
+
+    // absorb the dummy-mode core theta (1 x r_b x rho) into its neighbour
+    // (tt_svd.hpp:373-398)
+    std::vector<double> theta = rec_tt.cores[0];
+    const int64_t rho = rec_tt.ranks[1];
+    const std::vector<double>& c1 = rec_tt.cores[1];
+    const int64_t n1 = rdims[1], r2 = rec_tt.ranks[2];
+    auto* tt = new ttsvd_cu_tt();
+    tt->dims.assign(dims, dims + d);
+    tt->cores.assign(main_tt.cores.begin(), main_tt.cores.end() - 1);
+    if (rb == 1 && rho == 1) {
+        const double sc = theta[0];
+        for (auto& v : tt->cores[0]) v *= sc;
+        theta[0] = 1.0;
+    }
+    std::vector<double> boundary((size_t)(rb * n1 * r2), 0.0);
+    for (int64_t b = 0; b < r2; ++b)
+        for (int64_t x = 0; x < n1; ++x)
+            for (int64_t a = 0; a < rb; ++a) {
+                double acc = 0.0;
+                for (int64_t l = 0; l < rho; ++l) acc += theta[(size_t)(a + rb * l)] * c1[(size_t)(l + rho * (x + n1 * b))];
+                boundary[(size_t)(a + rb * (x + n1 * b))] = acc;
+            }
+    tt->cores.push_back(std::move(boundary));
+    for (size_t j = 2; j < rec_tt.cores.size(); ++j) tt->cores.push_back(rec_tt.cores[j]);
+    tt->ranks.assign(main_tt.ranks.begin(), main_tt.ranks.begin() + dm);  // r_0 .. r_{dm-1} = r_b
+    for (size_t j = 2; j < rec_tt.ranks.size(); ++j) tt->ranks.push_back(rec_tt.ranks[j]);
+    tt->steps = main_tt.steps;
+    tt->steps.insert(tt->steps.end(), rec_tt.steps.begin(), rec_tt.steps.end());
+    tt->sigmas = main_tt.sigmas;
+    tt->sigmas.insert(tt->sigmas.end(), rec_tt.sigmas.begin(), rec_tt.sigmas.end());
     *out = tt;
     return TTSVD_OK;
 }

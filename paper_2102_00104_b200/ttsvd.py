@@ -487,6 +487,49 @@ def tt_svd_tsqr(X, dims, spec: TruncationSpec | tuple | None = None, ctx_exec=No
     return _finish(h, dims)
 
 
+@dataclass
+class ThickBoundsParams:
+    """tt_svd.hpp:292-310"""
+    m_min: int = 16
+    f1_min: float = 0.5
+    r_tilde: list = field(default_factory=list)
+
+
+def choose_combined_dims(dims, params: ThickBoundsParams | None = None, r_max: int | None = None):
+    """tt_svd.hpp:316-330: (k, m), the k trailing modes merged into extent m."""
+    params = params or ThickBoundsParams()
+    dv = np.asarray([int(x) for x in dims], dtype=np.int64)
+    rt = np.asarray(params.r_tilde, dtype=np.int64)
+    k, m = C.c_int64(), C.c_int64()
+    _check(_lib.lib().ttsvd_cu_choose_combined_dims(dv.ctypes.data_as(_lib.i64p), len(dv), int(params.m_min),
+                                                    float(params.f1_min), rt.ctypes.data if len(rt) else None,
+                                                    len(rt), int(r_max or 0), C.byref(k), C.byref(m)))
+    return int(k.value), int(m.value)
+
+
+def tt_svd_thick_bounds(X, dims, spec: TruncationSpec | tuple | None = None,
+                        params: ThickBoundsParams | None = None) -> TensorTrain:
+    """tt_svd.hpp:338 (Alg. 3) on a device tensor in the padded layout (as
+    tt_svd_tsqr; host numpy buffers are staged to the device first)."""
+    spec = _spec(spec)
+    params = params or ThickBoundsParams()
+    dims = [int(x) for x in dims]
+    d = len(dims)
+    if d < 2:
+        raise DegenerateDimension("tt_svd_thick_bounds: requires d >= 2")
+    r_max = spec.r_max if spec.r_max < 2 ** 62 else 0
+    X = to_device_matrix(X)
+    dv = np.asarray(dims, dtype=np.int64)
+    rt = np.asarray(params.r_tilde, dtype=np.int64)
+    ctx = context(X.device.index)
+    p, rows, cols, ld = _mat(X)
+    h = C.c_void_p()
+    _check(_lib.lib().ttsvd_cu_tt_svd_thick(ctx.handle, p, dv.ctypes.data_as(_lib.i64p), d, ld, r_max,
+                                            float(spec.eps), int(params.m_min), float(params.f1_min),
+                                            rt.ctypes.data if len(rt) else None, len(rt), C.byref(h)))
+    return _finish(h, dims)
+
+
 class _CAI:
     """Zero-copy torch view of a raw device pointer (for the exchange)."""
 

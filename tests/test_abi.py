@@ -4,6 +4,7 @@ without a GPU.  No compute calls here."""
 import ctypes as C
 import os
 
+import numpy as np
 import pytest
 
 
@@ -82,3 +83,22 @@ def test_cpp_dropin_device_path(tmp_path):
     r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, (r.returncode, r.stdout, r.stderr)
     assert "device entry points ok" in r.stdout
+
+
+@pytest.mark.parametrize("dims,m_min,f1_min,r_tilde,r_max", [
+    ([4] * 10, 16, 0.5, (), 16), ([2] * 20, 16, 0.5, (), 64), ([16] * 7, 16, 0.5, (), 32),
+    ([3, 5, 7, 2], 64, 0.25, (), 8), ([2] * 8, 4096, 0.5, (), 4), ([5, 6], 2, 1.0, (3,), 10),
+    ([2] * 10, 16, 0.5, (2, 4, 8, 16, 32, 16, 8, 4, 2), 100)])
+def test_choose_combined_dims_matches_reference(dims, m_min, f1_min, r_tilde, r_max, ref):
+    # tt_svd.hpp:316-330 — host arithmetic of the C-ABI, no GPU needed
+    import ctypes as C
+    from paper_2102_00104_b200 import _lib
+    L = _lib.lib()
+    dv = np.asarray(dims, dtype=np.int64)
+    rt = np.asarray(r_tilde, dtype=np.int64)
+    k, m = C.c_int64(), C.c_int64()
+    rc = L.ttsvd_cu_choose_combined_dims(dv.ctypes.data_as(_lib.i64p), len(dv), m_min, f1_min,
+                                         rt.ctypes.data if len(rt) else None, len(rt), r_max, C.byref(k),
+                                         C.byref(m))
+    assert rc == 0
+    assert (k.value, m.value) == ref.choose_combined_dims(dims, m_min, f1_min, r_tilde, r_max)
