@@ -27,12 +27,6 @@ struct BlkArgs {
     int dbg = 0;            // diagnostics only (timing experiments): bit 0 skip trailing, bit 1 skip phase A
 };
 
-__device__ __forceinline__ void dmma884(double (&d)[2], double a, double b) {
-    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
-                 : "+d"(d[0]), "+d"(d[1])
-                 : "d"(a), "d"(b));
-}
-
 // offset of row panel p in the packed layout, and the packed size
 __host__ __device__ __forceinline__ int64_t blk_roff(int p, int M) {
     return 32 * ((int64_t)p * M - 32 * (int64_t)p * (p - 1) / 2);

@@ -689,9 +689,42 @@ int launch_tsmm(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t ld
     return check_launch(ctx, "tsmm_kernel");
 }
 
+template <int NT>
+int launch_tsmm_dmma(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t ldx, const double* V, int64_t ldv,
+                     int k, double* Y, int64_t out_rows, int64_t ldy) {
+    const size_t smem = (size_t)((m + 3) & ~3) * tsmm_vld(NT) * 8;
+    static bool attr = false;
+    if (!attr) {
+        TT_CUDA(cudaFuncSetAttribute(tsmm_dmma_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit));
+        attr = true;
+    }
+    const int chunks = (k + 8 * NT - 1) / (8 * NT);
+    int64_t blocks = (n + 255) / 256;
+    blocks = std::min<int64_t>(blocks, (int64_t)ctx->num_sms * 4);
+    dim3 grid((unsigned)std::max<int64_t>(blocks, 1), (unsigned)chunks);
+    tsmm_dmma_kernel<NT><<<grid, 256, smem, ctx->stream>>>(X, n, m, ldx, V, ldv, k, Y, out_rows, ldy);
+    return check_launch(ctx, "tsmm_dmma_kernel");
+}
+
 int tsmm_device(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t ldx, const double* V, int64_t ldv, int k,
                 double* Y, int64_t out_rows, int64_t out_cols, int64_t ldy) {
     int rc;
+    static const char* tsel = std::getenv("TTSVD_TSMM");  // diagnostics: "ffma" = the one-row-per-thread kernel
+    // measured (tools/config3_sweep.py): the tensor-core path wins only once the
+    // FFMA kernel turns compute-bound (k > 16 output columns, m >= 32)
+    const bool dmma = !(tsel && std::string(tsel) == "ffma") && k > 16 && m >= 32 && n >= (int64_t)1 << 18 &&
+                      (size_t)((m + 3) & ~3) * tsmm_vld(4) * 8 <= 200 * 1024;
+    if (dmma) {
+        rc = launch_tsmm_dmma<4>(ctx, X, n, m, ldx, V, ldv, k, Y, out_rows, ldy);
+        if (rc != TTSVD_OK) return rc;
+        if (ldy > out_rows) {
+            const int64_t pad = (ldy - out_rows) * out_cols;
+            const int blocks = (int)std::min<int64_t>((pad + 255) / 256, 1024);
+            zero_padding_kernel<<<std::max(blocks, 1), 256, 0, ctx->stream>>>(Y, out_rows, ldy, out_cols);
+            return check_launch(ctx, "zero_padding_kernel");
+        }
+        return TTSVD_OK;
+    }
     if (k <= 1) rc = launch_tsmm<1>(ctx, X, n, m, ldx, V, ldv, k, Y, out_rows, ldy);
     else if (k <= 2) rc = launch_tsmm<2>(ctx, X, n, m, ldx, V, ldv, k, Y, out_rows, ldy);
     else if (k <= 4) rc = launch_tsmm<4>(ctx, X, n, m, ldx, V, ldv, k, Y, out_rows, ldy);

@@ -33,6 +33,14 @@ __device__ __forceinline__ double warp_sum(double v) {
     return v;
 }
 
+// D += A B on the FP64 tensor cores (mma.sync m8n8k4 f64).  Fragments: lane l
+// holds A[l/4][l%4], B[l%4][l/4] and C/D[l/4][2(l%4) + e].
+__device__ __forceinline__ void dmma884(double (&d)[2], double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                 : "+d"(d[0]), "+d"(d[1])
+                 : "d"(a), "d"(b));
+}
+
 __device__ __forceinline__ double ldg_stream(const double* p) {
     double v;
     asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
@@ -546,6 +554,80 @@ __global__ void __launch_bounds__(256) tsmm_kernel(const double* __restrict__ X,
                     const int64_t p = i + n * (c0 + c);
                     const int64_t col = p / out_rows;
                     Y[col * ldy + (p - col * out_rows)] = acc[c];
+                }
+        }
+    }
+}
+
+// K_TSMM on the FP64 tensor cores: each warp computes a 32-row x 8NT-column
+// block of X V with DMMA m8n8k4 (A fragments loaded straight from X — for a
+// fixed fragment column the 8 rows are one contiguous 64-byte run — B
+// fragments from the chunk of V staged in shared memory), then scatters it
+// into the next step's padded layout exactly as tsmm_kernel (element (i, c)
+// at flat position i + n c).  Output columns c0 .. c0 + 8NT - 1 (grid.y
+// chunks).  The product of a unit column of V is exact (column selection).
+__host__ __device__ inline int tsmm_vld(int nt) { return ((8 * nt + 15) / 16) * 16 + 4; }
+
+template <int NT>
+__global__ void __launch_bounds__(256) tsmm_dmma_kernel(const double* __restrict__ X, int64_t n, int m, int64_t ldx,
+                                                        const double* __restrict__ V, int64_t ldv, int k,
+                                                        double* __restrict__ Y, int64_t out_rows, int64_t ldy) {
+    extern __shared__ __align__(16) double Vs[];  // (m rounded to 4) x tsmm_vld(NT)
+    constexpr int VLD = ((8 * NT + 15) / 16) * 16 + 4;
+    const int c0 = blockIdx.y * 8 * NT;
+    const int kc = min(8 * NT, k - c0);
+    const int m4 = (m + 3) & ~3;
+    for (int e = threadIdx.x; e < m4 * VLD; e += blockDim.x) {
+        const int j = e / VLD, c = e % VLD;
+        Vs[e] = (j < m && c < kc) ? V[(int64_t)(c0 + c) * ldv + j] : 0.0;
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int r = lane >> 2, q = lane & 3;
+    const bool divisible = (n % out_rows) == 0;
+    const int64_t n_next = divisible ? n / out_rows : 0;
+    const int64_t stride = (int64_t)gridDim.x * (blockDim.x / 32) * 32;
+    for (int64_t rb = ((int64_t)blockIdx.x * (blockDim.x / 32) + warp) * 32; rb < n; rb += stride) {
+        double acc[4][NT][2];
+#pragma unroll
+        for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
+        const bool full = rb + 32 <= n;
+#pragma unroll 2
+        for (int kk = 0; kk < m4 / 4; ++kk) {
+            const int col = 4 * kk + q;
+            const double* xc = X + (int64_t)col * ldx + rb + r;
+            double a[4];
+#pragma unroll
+            for (int mt = 0; mt < 4; ++mt)
+                a[mt] = (col < m && (full || rb + 8 * mt + r < n)) ? ldg_stream(xc + 8 * mt) : 0.0;
+            double b[NT];
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt) b[nt] = Vs[col * VLD + 8 * nt + r];
+#pragma unroll
+            for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+                for (int nt = 0; nt < NT; ++nt) dmma884(acc[mt][nt], a[mt], b[nt]);
+        }
+#pragma unroll
+        for (int mt = 0; mt < 4; ++mt) {
+            const int64_t i = rb + 8 * mt + r;
+            if (i >= n) continue;
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const int c = 8 * nt + 2 * q + e;
+                    if (c >= kc) continue;
+                    if (divisible) {
+                        const int64_t b = i / out_rows, ii = i - b * out_rows;
+                        Y[(b + n_next * (c0 + c)) * ldy + ii] = acc[mt][nt][e];
+                    } else {
+                        const int64_t p = i + n * (c0 + c);
+                        const int64_t cl = p / out_rows;
+                        Y[cl * ldy + (p - cl * out_rows)] = acc[mt][nt][e];
+                    }
                 }
         }
     }
