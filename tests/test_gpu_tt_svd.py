@@ -179,6 +179,19 @@ def test_wide_steps_and_odd_shapes(tt, orc):
         assert_parity(tt, orc, X, dims, T, o)
 
 
+# Steps that reach every small-SVD kernel: the cluster block Jacobi for
+# m >= 96 (tall steps on R^T and wide steps on W^T, m and n not multiples of
+# 4 or 8), the single-CTA shared-memory kernel, and the cooperative kernel
+# for a wide W^T too large for one CTA's shared memory.
+@pytest.mark.parametrize("dims,r_max", [([6, 7, 9, 13, 11], 400), ([2] * 16, 200), ([4] * 9, 130),
+                                        ([7, 11, 13, 17], 300)])
+def test_svd_kernel_shapes(tt, orc, dims, r_max):
+    from oracle.oracle import random_tensor
+    X = random_tensor(211 + len(dims), dims)
+    T, o = run_both(tt, orc, X, dims, r_max)
+    assert_parity(tt, orc, X, dims, T, o, err_tol=1e-9)
+
+
 def test_exact_tt_rank32_scaled_config2(tt, orc):
     # config 2's structure at a reduced size: 16^5, exact TT rank 8 + 1e-8 noise
     rng = np.random.default_rng(2)
