@@ -45,9 +45,16 @@ struct BjArgs {
     int C;    // CTAs in the cluster
     int* status;
     int max_sweeps;
+    long long* prof;  // optional (diagnostics): CTA 0 cycle sums [gram, solve, apply, moves + cluster barrier]
 };
 
 constexpr int kBjThreads = 512;
+
+__device__ __forceinline__ long long bj_clock() {
+    long long t;
+    asm volatile("mov.u64 %0, %%clock64;" : "=l"(t)::"memory");
+    return t;
+}
 constexpr int kBjWpg = 4;                               // warps per block pair
 constexpr int kBjSlots = kBjThreads / (32 * kBjWpg);   // block-pair slots per CTA
 
@@ -64,7 +71,8 @@ __device__ __forceinline__ void bj_group_sync(int grp) {
 // warp) whether any pair rotated.
 __device__ __forceinline__ bool bj_visit(double* bt, double* bb, int blt, int blb, bool first_round, int m, int n8,
                                          int ldc, double (*gpart)[64], double* Gs, double* Qs, int* grp_rot, int grp,
-                                         int wg, bool solver, int lane) {
+                                         int wg, bool solver, int lane, long long* pf = nullptr) {
+    const long long tv0 = pf ? bj_clock() : 0;
     const double tol = 1e2 * DBL_EPSILON;
     bool rotated = false;
     // ---- 1. Gram partials: lane l reads column l/4, rows 4q + l%4 ----
@@ -88,6 +96,7 @@ __device__ __forceinline__ bool bj_visit(double* bt, double* bb, int blt, int bl
         gp[(lane >> 2) * 8 + 2 * (lane & 3) + 1] = acc0[1] + acc1[1];
     }
     bj_group_sync(grp);
+    const long long tv1 = pf ? bj_clock() : 0;
     // ---- 2. rotations on the Gram matrix (the solver warp) ----
     if (solver) {
         double* G = Gs;
@@ -162,6 +171,7 @@ __device__ __forceinline__ bool bj_visit(double* bt, double* bb, int blt, int bl
         rotated = any;
     }
     bj_group_sync(grp);
+    const long long tv2 = pf ? bj_clock() : 0;
     // ---- 3. B <- B Q (DMMA; 8-row tiles) ----
     if (*grp_rot) {
         const double* Q = Qs;
@@ -181,7 +191,13 @@ __device__ __forceinline__ bool bj_visit(double* bt, double* bb, int blt, int bl
             o0[ldc + rr] = d[1];
         }
     }
-        return rotated;
+    if (pf) {
+        const long long tv3 = bj_clock();
+        pf[0] += tv1 - tv0;
+        pf[1] += tv2 - tv1;
+        pf[2] += tv3 - tv2;
+    }
+    return rotated;
 }
 
 __global__ void __launch_bounds__(kBjThreads, 1) jacobi_bj_kernel(BjArgs a) {
@@ -234,11 +250,14 @@ __global__ void __launch_bounds__(kBjThreads, 1) jacobi_bj_kernel(BjArgs a) {
             const bool active = 4 * blt < m || 4 * blb < m;
             double* bt = smem + (int64_t)top_buf[grp] * bsz;
             double* bb = smem + (int64_t)bot_buf[grp] * bsz;
+            long long* pfv = (a.prof && blockIdx.x == 0 && tid == 0) ? a.prof : nullptr;
+            const long long tr0 = pfv ? bj_clock() : 0;
             if (active) {
                 if (bj_visit(bt, bb, blt, blb, r == 0, m, n8, ldc, gpart[grp], Gs[grp], Qs[grp], &grp_rot[grp], grp, wg,
-                             wg == grp, lane))
+                             wg == grp, lane, pfv))
                     rot[sweep & 1] = 1;
             }
+            const long long tr1 = pfv ? bj_clock() : 0;
             __syncthreads();
             // ---- block moves: boundary blocks -> neighbours' inboxes ----
             if (k < C - 1) {
@@ -271,6 +290,7 @@ __global__ void __launch_bounds__(kBjThreads, 1) jacobi_bj_kernel(BjArgs a) {
                 }
             }
             cl.sync();
+            if (pfv) pfv[3] += bj_clock() - tr1;
             if (warp == 0) {
                 const int j = lane < S ? lane : S - 1;
                 const int tb = top_buf[j], tc = top_blk[j], bb_ = bot_buf[j], bc = bot_blk[j];
