@@ -65,13 +65,23 @@ __device__ __forceinline__ void bj_group_sync(int grp) {
     asm volatile("bar.sync %0, %1;" ::"r"(1 + grp), "r"(kBjWpg * 32) : "memory");
 }
 
+// a block that leaves the CTA unchanged: copy it into the neighbour's inbox
+// (the 4 warps of its group; no-op for blocks that stay)
+__device__ __forceinline__ void bj_copy_block(const double* src, double* dst, int bsz, int t) {
+    if (src == dst) return;
+    const double2* s2 = reinterpret_cast<const double2*>(src);
+    double2* d2 = reinterpret_cast<double2*>(dst);
+    for (int i = t; i < bsz / 2; i += kBjWpg * 32) d2[i] = s2[i];
+}
+
 // One visit of a block pair (8 columns: blocks bt | bb, 4 columns each, ld
 // ldc, rows n8): Gram by DMMA over the group's warps, the rotations on the
 // Gram matrix by the solver warp, B <- B Q by DMMA.  Returns (in the solver
 // warp) whether any pair rotated.
 __device__ __forceinline__ bool bj_visit(double* bt, double* bb, int blt, int blb, bool first_round, int m, int n8,
                                          int ldc, double (*gpart)[64], double* Gs, double* Qs, int* grp_rot, int grp,
-                                         int wg, bool solver, int lane, long long* pf = nullptr) {
+                                         int wg, bool solver, int lane, double* dt, double* db, int bsz,
+                                         long long* pf = nullptr) {
     const long long tv0 = pf ? bj_clock() : 0;
     const double tol = 1e2 * DBL_EPSILON;
     bool rotated = false;
@@ -134,9 +144,11 @@ __device__ __forceinline__ bool bj_visit(double* bt, double* bb, int blt, int bl
             const double al = G[p * 9 + p], be = G[q * 9 + q], ga = G[p * 9 + q];
             double c = 1.0, sn = 0.0;
             if (ga * ga > (tol * tol) * (al * be)) {
-                const double zeta = (be - al) * __drcp_rn(2.0 * ga);
-                const double t =
-                    ((zeta >= 0.0) ? 1.0 : -1.0) * __drcp_rn(fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
+                // t = sign(zeta) / (|zeta| + sqrt(1 + zeta^2)), zeta = (be - al) / (2 ga),
+                // rewritten without the first division: t = sign(dd) h / (|dd| + sqrt(dd^2 + h^2))
+                const double dd = be - al, h = 2.0 * ga;
+                const double t = (dd == 0.0) ? 1.0
+                                             : ((dd > 0.0) ? h : -h) * __drcp_rn(fabs(dd) + sqrt(fma(dd, dd, h * h)));
                 c = rsqrt(fma(t, t, 1.0));
                 sn = c * t;
                 any = 1;
@@ -178,7 +190,7 @@ __device__ __forceinline__ bool bj_visit(double* bt, double* bb, int blt, int bl
         const double q0 = Q[(lane & 3) * 9 + (lane >> 2)];
         const double q1 = Q[(4 + (lane & 3)) * 9 + (lane >> 2)];
         const int ce = 2 * (lane & 3);
-        double* o0 = ce < 4 ? bt + ce * ldc : bb + (ce - 4) * ldc;
+        double* o0 = ce < 4 ? dt + ce * ldc : db + (ce - 4) * ldc;  // a block leaving the CTA goes straight to its inbox
 #pragma unroll 4
         for (int t = wg; t < (n8 >> 3); t += kBjWpg) {
             const int rr = 8 * t + (lane >> 2);
@@ -190,6 +202,9 @@ __device__ __forceinline__ bool bj_visit(double* bt, double* bb, int blt, int bl
             o0[rr] = d[0];
             o0[ldc + rr] = d[1];
         }
+    } else {
+        bj_copy_block(bt, dt, bsz, wg * 32 + lane);
+        bj_copy_block(bb, db, bsz, wg * 32 + lane);
     }
     if (pf) {
         const long long tv3 = bj_clock();
@@ -252,27 +267,26 @@ __global__ void __launch_bounds__(kBjThreads, 1) jacobi_bj_kernel(BjArgs a) {
             double* bb = smem + (int64_t)bot_buf[grp] * bsz;
             long long* pfv = (a.prof && blockIdx.x == 0 && tid == 0) ? a.prof : nullptr;
             const long long tr0 = pfv ? bj_clock() : 0;
+            // the two blocks that leave the CTA this round are written straight
+            // into the neighbours' inboxes (DSMEM) by their visit
+            double* dt = bt;
+            double* db = bb;
+            if (k < C - 1 && grp == S - 1) dt = cl.map_shared_rank(smem, k + 1) + (int64_t)rdst[par] * bsz;
+            if (k > 0 && grp == 0) db = cl.map_shared_rank(smem, k - 1) + (int64_t)ldst[par] * bsz;
             if (active) {
                 if (bj_visit(bt, bb, blt, blb, r == 0, m, n8, ldc, gpart[grp], Gs[grp], Qs[grp], &grp_rot[grp], grp, wg,
-                             wg == grp, lane, pfv))
+                             wg == grp, lane, dt, db, bsz, pfv))
                     rot[sweep & 1] = 1;
+            } else {
+                bj_copy_block(bt, dt, bsz, wg * 32 + lane);
+                bj_copy_block(bb, db, bsz, wg * 32 + lane);
             }
             const long long tr1 = pfv ? bj_clock() : 0;
             __syncthreads();
             // ---- block moves: boundary blocks -> neighbours' inboxes ----
-            if (k < C - 1) {
-                const int dst_idx = rdst[par];
-                double2* dst = reinterpret_cast<double2*>(cl.map_shared_rank(smem, k + 1) + (int64_t)dst_idx * bsz);
-                const double2* src = reinterpret_cast<const double2*>(smem + (int64_t)top_buf[S - 1] * bsz);
-                for (int i = tid; i < bsz / 2; i += kBjThreads) dst[i] = src[i];
-                if (tid == 0) *cl.map_shared_rank(&inbox_blk[par][0], k + 1) = top_blk[S - 1];
-            }
-            if (k > 0) {
-                const int dst_idx = ldst[par];
-                double2* dst = reinterpret_cast<double2*>(cl.map_shared_rank(smem, k - 1) + (int64_t)dst_idx * bsz);
-                const double2* src = reinterpret_cast<const double2*>(smem + (int64_t)bot_buf[0] * bsz);
-                for (int i = tid; i < bsz / 2; i += kBjThreads) dst[i] = src[i];
-                if (tid == 0) *cl.map_shared_rank(&inbox_blk[par][1], k - 1) = bot_blk[0];
+            if (tid == 0) {
+                if (k < C - 1) *cl.map_shared_rank(&inbox_blk[par][0], k + 1) = top_blk[S - 1];
+                if (k > 0) *cl.map_shared_rank(&inbox_blk[par][1], k - 1) = bot_blk[0];
             }
             if (tid == 0) {
                 // the blocks just sent free their buffers: they become my inboxes for
