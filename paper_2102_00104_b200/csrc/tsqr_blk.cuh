@@ -24,7 +24,6 @@ struct BlkArgs {
     int M;                  // padded columns (multiple of 32)
     int mode;
     long long* prof;        // optional per-CTA phase cycle counters (8 per CTA), diagnostics
-    int dbg = 0;            // diagnostics only (timing experiments): bit 0 skip trailing, bit 1 skip phase A
 };
 
 // offset of row panel p in the packed layout, and the packed size

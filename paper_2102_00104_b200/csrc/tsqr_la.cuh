@@ -362,7 +362,7 @@ __global__ void __launch_bounds__(kLaThreads, 2) tsqr_la_kernel(BlkArgs a) {
             const double* Tp = Tm0 + (p & 1) * 32 * kLaTld;
             double* Rrow = R + blk_roff(p, M);
             if (is_panel) la_fetch_rdiag(Rp, R + blk_roff(p + 1, M), lane);
-            if (!is_panel && !is_idle && wi < 4 && !(a.dbg & 2)) {
+            if (!is_panel && !is_idle && wi < 4) {
                 // phase A: the next panel's columns
                 la_group(Bt, c0, nxt + 8 * wi, Tp, Rrow, lane, pol_r);
                 __threadfence_block();
@@ -370,7 +370,7 @@ __global__ void __launch_bounds__(kLaThreads, 2) tsqr_la_kernel(BlkArgs a) {
             }
             if (is_panel) {
                 TT_PROF(5);
-                if (!(a.dbg & 2)) asm volatile("bar.sync 1, 160;" ::: "memory");
+                asm volatile("bar.sync 1, 160;" ::: "memory");
                 cp_async_wait_all();
                 __syncwarp();
                 TT_PROF(1);
@@ -380,7 +380,7 @@ __global__ void __launch_bounds__(kLaThreads, 2) tsqr_la_kernel(BlkArgs a) {
                 TT_PROF(2);
                 if (p + 2 < npan) la_build_t(Sm, tau, Tm0 + ((p + 1) & 1) * 32 * kLaTld, lane);
                 TT_PROF(3);
-            } else if (!is_idle && !(a.dbg & 1)) {
+            } else if (!is_idle) {
                 const int idx = (wi + 2) % 6;  // the two warps without phase A work first
                 for (int g = nxt + 32 + 8 * idx; g < M; g += 8 * 6) la_group(Bt, c0, g, Tp, Rrow, lane, pol_r);
             }

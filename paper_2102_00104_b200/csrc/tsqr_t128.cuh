@@ -36,7 +36,6 @@ struct T2Args {
     double* Scr;  // per-CTA tile scratch (kT2Rows x M, ld kT2Rows)
     int m, M;
     long long* prof;  // optional per-CTA phase cycle counters (8 per CTA), diagnostics
-    int dbg;          // diagnostics only (timing experiments, wrong results): bit 0 skip the trailing update
 };
 
 inline size_t t2_smem_bytes() {
@@ -390,7 +389,7 @@ __global__ void __launch_bounds__(kT2Threads, 1) tsqr_t128_kernel(T2Args a) {
                 if (warp == 0) la_store_rdiag(Rp, R + blk_roff(p + 1, M), lane, pol_r);
                 if (p + 2 < npan) t2_build_t(Sm, tau, Tm0 + ((p + 1) & 1) * 32 * kLaTld, dpart, warp, lane);
                 T2_PROF(3);
-            } else if (!(a.dbg & 1)) {
+            } else {
                 for (int g = nxt + 32 + 8 * uw; g < M; g += 8 * (kT2Threads / 32 - 4)) {
                     if (p == 0)
                         t2_group<true, false>(Xt, a.ld, rows, m, Scr, kT2Rows, V, Tp, Rrow, c0, g, g, lane, pol_x, pol_r);

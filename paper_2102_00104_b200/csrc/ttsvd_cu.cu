@@ -417,8 +417,7 @@ int tsqr_device(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t ld
             static const bool tprof = std::getenv("TTSVD_PROF_BLK") != nullptr;
             long long* dprof = nullptr;
             if (tprof) TT_CUDA(cudaMalloc(&dprof, (size_t)Gt * 8 * sizeof(long long)));
-            static const char* tdbg = std::getenv("TTSVD_BLK_DBG");  // diagnostics only: wrong results by design
-            T2Args ta{X, n, ld, parts, as<double>(ctx->ws_Scr), m, M, dprof, tdbg ? std::atoi(tdbg) : 0};
+            T2Args ta{X, n, ld, parts, as<double>(ctx->ws_Scr), m, M, dprof};
             kmark(ctx, 0, TTSVD_K_T128);
             tsqr_t128_kernel<<<(unsigned)Gt, kT2Threads, t2_smem_bytes(), ctx->stream>>>(ta);
             TT_TRY(check_launch(ctx, "tsqr_t128_kernel"));
@@ -472,8 +471,6 @@ int tsqr_device(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t ld
             TT_TRY(pack_parts(ctx, R_init, 1, m, M, Rinit_ws));
         }
         BlkArgs a{X, n, ld, parts, Rinit_ws, m, M, 0, nullptr};
-        static const char* dbg = std::getenv("TTSVD_BLK_DBG");  // diagnostics only: wrong results by design
-        a.dbg = dbg ? std::atoi(dbg) : 0;
         static const bool prof = std::getenv("TTSVD_PROF_BLK") != nullptr;
         long long* dprof = nullptr;
         if (prof) TT_CUDA(cudaMalloc(&dprof, (size_t)G * 8 * sizeof(long long)));
