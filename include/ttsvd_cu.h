@@ -63,7 +63,8 @@ enum {
     TTSVD_K_V1 = 2,    /* block-per-job tiles, m <= 32 */
     TTSVD_K_LA = 3,    /* 32-row look-ahead tiles */
     TTSVD_K_T128 = 4,  /* 128-row tiles, one CTA per SM */
-    TTSVD_K_GQR = 5    /* cooperative whole-grid QR */
+    TTSVD_K_GQR = 5,   /* cooperative whole-grid QR */
+    TTSVD_K_PT = 6     /* thread streams, m <= 8 */
 };
 
 /* All-gather over the ranks of a distributed run (replaces the in-process

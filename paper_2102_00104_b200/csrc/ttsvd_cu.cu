@@ -24,6 +24,7 @@
 #include "tsqr_la.cuh"
 #include "tsqr_t128.cuh"
 #include "tsqr_ws.cuh"
+#include "tsqr_pt.cuh"
 
 using namespace ttsvd_b200;
 
@@ -383,6 +384,58 @@ int tsqr_ws_device(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t
     return m <= 16 ? tsqr_ws_levels<16>(ctx, X, n, m, ld, R) : tsqr_ws_levels<32>(ctx, X, n, m, ld, R);
 }
 
+// m <= 8: thread streams (tsqr_pt.cuh), levels of stacked factors (~64 rows
+// per thread stream once the grid is full) until one thread is left.
+template <int M>
+int tsqr_pt_levels(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int64_t ld, double* R) {
+    // rows per fold (x (U x M) and R stay in registers); measured on B200:
+    // U = 4 keeps two CTAs per SM for m = 5, 6, U = 8 wins at m = 7, 8
+    constexpr int U = (M == 5 || M == 6) ? 4 : 8;
+    static int per_sm = -1;
+    if (per_sm < 0) {
+        TT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tsqr_pt_kernel<M, U>, kPtThreads, 0));
+        per_sm = std::max(1, per_sm);
+    }
+    const int64_t max_t = (int64_t)per_sm * ctx->num_sms * kPtThreads;
+    const double* src = X;
+    int64_t rows = n, sld = ld;
+    int flip = 0;
+    for (;;) {
+        int64_t T = std::min<int64_t>(rows / 64, max_t);
+        if (T < 1) T = 1;
+        if (T > 1) {
+            TT_TRY(ensure(ctx->ws_R, (size_t)T * M * M * 8));
+            TT_TRY(ensure(ctx->ws_R2, (size_t)T * M * M * 8));
+        }
+        double* out = (T == 1) ? R : as<double>(flip ? ctx->ws_R2 : ctx->ws_R);
+        const int64_t ldo = (T == 1) ? M : T * M;
+        PtArgs pa{src, rows, sld, T, out, ldo};
+        if (src == X) kmark(ctx, 0, TTSVD_K_PT);
+        tsqr_pt_kernel<M, U><<<(unsigned)((T + kPtThreads - 1) / kPtThreads), kPtThreads, 0, ctx->stream>>>(pa);
+        TT_TRY(check_launch(ctx, "tsqr_pt_kernel"));
+        if (src == X) kmark(ctx, 1, TTSVD_K_PT);
+        if (T == 1) return TTSVD_OK;
+        src = out;
+        rows = T * M;
+        sld = T * M;
+        flip ^= 1;
+    }
+}
+
+int tsqr_pt_device(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t ld, double* R) {
+    switch (m) {
+        case 1: return tsqr_pt_levels<1>(ctx, X, n, ld, R);
+        case 2: return tsqr_pt_levels<2>(ctx, X, n, ld, R);
+        case 3: return tsqr_pt_levels<3>(ctx, X, n, ld, R);
+        case 4: return tsqr_pt_levels<4>(ctx, X, n, ld, R);
+        case 5: return tsqr_pt_levels<5>(ctx, X, n, ld, R);
+        case 6: return tsqr_pt_levels<6>(ctx, X, n, ld, R);
+        case 7: return tsqr_pt_levels<7>(ctx, X, n, ld, R);
+        case 8: return tsqr_pt_levels<8>(ctx, X, n, ld, R);
+        default: return TTSVD_ERR_INVALID;
+    }
+}
+
 int tsqr_device(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t ld, double* R,
                 const double* R_init = nullptr) {
     ctx->last_kernel = TTSVD_K_NONE;
@@ -502,6 +555,8 @@ int tsqr_device(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t ld
     {
         static const char* tsel = std::getenv("TTSVD_TSQR");  // diagnostics: "v1" = the block-per-job kernel
         const bool v1 = tsel && std::string(tsel) == "v1";
+        const bool ws = tsel && std::string(tsel) == "ws";
+        if (!R_init && !v1 && !ws && m <= 8 && n >= 4096) return tsqr_pt_device(ctx, X, n, m, ld, R);
         if (!R_init && !v1 && n >= 4096) return tsqr_ws_device(ctx, X, n, m, ld, R);
     }
     TsqrPlan p = tsqr_plan(m);

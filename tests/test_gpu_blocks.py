@@ -106,6 +106,34 @@ def test_tsqr_wide_kernels(tt, n, m, kind):
         assert s_r[rank] <= 1e-13 * s_r[0]
 
 
+# The thread-stream kernel (tsqr_pt_kernel, m <= 8, n >= 4096): every
+# thread folds 8 strided rows at a time into its own R; ragged row counts,
+# zero / duplicated columns and low rank.
+@pytest.mark.parametrize("n,m,kind", [(100003, 1, "dense"), (50000, 2, "dense"), (70001, 3, "dup"),
+                                      (1 << 20, 4, "dense"), (65537, 5, "lowrank"), (200000, 8, "dup"),
+                                      (4096, 8, "dense"), (300001, 6, "dense"), (4099, 7, "dup")])
+def test_tsqr_thread_streams(tt, n, m, kind):
+    from oracle.oracle import gaussian
+    X = gaussian(n, m, 41 + m).copy(order="F")
+    if kind == "dup" and m >= 3:
+        X[:, m - 1] = X[:, 0]
+        X[:, 1] = 0.0
+    if kind == "lowrank":
+        X = np.asfortranarray(gaussian(n, 2, 5) @ gaussian(2, m, 6))
+    R = host(tt.tsqr(X))
+    assert np.all(np.isfinite(R))
+    assert np.all(np.tril(R, -1) == 0.0)
+    assert gram_resid(X, R) <= 1e-12
+    s_r = np.linalg.svd(R, compute_uv=False)
+    s_x = np.linalg.svd(X, compute_uv=False)
+    assert np.max(np.abs(s_r - s_x)) <= 1e-10 * s_x[0]
+    if kind != "dense":
+        rank = 2 if kind == "lowrank" else m - 2
+        assert s_r[rank] <= 1e-13 * s_r[0]
+    # the same bytes give the same R (fixed reduction order)
+    assert np.array_equal(host(tt.tsqr(X)), R)
+
+
 def test_tsqr_rank_deficient_duplicate_column(tt, orc):
     # test_tsqr.cpp:88-97
     from oracle.oracle import gaussian
