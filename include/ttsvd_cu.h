@@ -64,7 +64,8 @@ enum {
     TTSVD_K_LA = 3,    /* 32-row look-ahead tiles */
     TTSVD_K_T128 = 4,  /* 128-row tiles, one CTA per SM */
     TTSVD_K_GQR = 5,   /* cooperative whole-grid QR */
-    TTSVD_K_PT = 6     /* thread streams, m <= 8 */
+    TTSVD_K_PT = 6,    /* thread streams, m <= 8 */
+    TTSVD_K_GS = 7     /* lane-group streams, 8 < m <= 32 */
 };
 
 /* All-gather over the ranks of a distributed run (replaces the in-process

@@ -12,7 +12,7 @@ import re
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
-LIB_PATH = os.path.join(HERE, "libttsvd_cu.so")
+LIB_PATH = os.environ.get("TTSVD_LIB_VARIANT") or os.path.join(HERE, "libttsvd_cu.so")  # override: diagnostics builds
 HEADER = os.path.join(ROOT, "include", "ttsvd_cu.h")
 
 i64 = C.c_int64
@@ -27,7 +27,8 @@ class Step(C.Structure):
 
 
 TSQR_KERNELS = {0: "none", 1: "tsqr_ws_kernel", 2: "tsqr_tile_kernel", 3: "tsqr_la_kernel", 4: "tsqr_t128_kernel",
-                5: "gqr_kernel", 6: "tsqr_pt_kernel"}
+                5: "gqr_kernel", 6: "tsqr_pt_kernel",
+                7: "tsqr_gs_kernel"}
 
 
 EXCHANGE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, i64, C.c_void_p)

@@ -436,6 +436,37 @@ int tsqr_pt_device(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t
     }
 }
 
+// 8 < m <= 32: group streams (tsqr_gs_kernel, P lanes per stream, M the
+// padded width), levels of stacked factors as tsqr_pt_levels.
+template <int M, int P, int U>
+int tsqr_gs_levels(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t ld, double* R) {
+    static int per_sm = -1;
+    if (per_sm < 0) {
+        TT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tsqr_gs_kernel<M, P, U>, kPtThreads, 0));
+        per_sm = std::max(1, per_sm);
+    }
+    const int64_t max_t = (int64_t)per_sm * ctx->num_sms * (kPtThreads / P);
+    int64_t T = std::max<int64_t>(1, std::min<int64_t>(n / 64, max_t));
+    if (T > 1) TT_TRY(ensure(ctx->ws_Scr, (size_t)T * m * m * 8));
+    double* out = (T == 1) ? R : as<double>(ctx->ws_Scr);
+    const int64_t ldo = (T == 1) ? m : T * m;
+    GsArgs ga{X, n, ld, m, T, out, ldo};
+    kmark(ctx, 0, TTSVD_K_GS);
+    const int64_t threads = (T * P + 31) / 32 * 32;
+    tsqr_gs_kernel<M, P, U><<<(unsigned)((threads + kPtThreads - 1) / kPtThreads), kPtThreads, 0, ctx->stream>>>(ga);
+    TT_TRY(check_launch(ctx, "tsqr_gs_kernel"));
+    kmark(ctx, 1, TTSVD_K_GS);
+    if (T == 1) return TTSVD_OK;
+    // the stacked factors are short: warp streams finish them with far
+    // shorter per-stream chains than another group-stream level
+    return tsqr_ws_device(ctx, out, T * m, m, T * m, R);
+}
+
+int tsqr_gs_device(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t ld, double* R) {
+    // measured on B200 (tools/gs_var.sh): 4 lanes per stream at m <= 16, 8 at m <= 32
+    return m <= 16 ? tsqr_gs_levels<16, 4, 8>(ctx, X, n, m, ld, R) : tsqr_gs_levels<32, 8, 8>(ctx, X, n, m, ld, R);
+}
+
 int tsqr_device(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t ld, double* R,
                 const double* R_init = nullptr) {
     ctx->last_kernel = TTSVD_K_NONE;
@@ -557,6 +588,7 @@ int tsqr_device(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t ld
         const bool v1 = tsel && std::string(tsel) == "v1";
         const bool ws = tsel && std::string(tsel) == "ws";
         if (!R_init && !v1 && !ws && m <= 8 && n >= 4096) return tsqr_pt_device(ctx, X, n, m, ld, R);
+        if (!R_init && !v1 && !ws && n >= 4096) return tsqr_gs_device(ctx, X, n, m, ld, R);
         if (!R_init && !v1 && n >= 4096) return tsqr_ws_device(ctx, X, n, m, ld, R);
     }
     TsqrPlan p = tsqr_plan(m);

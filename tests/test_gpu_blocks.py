@@ -106,12 +106,17 @@ def test_tsqr_wide_kernels(tt, n, m, kind):
         assert s_r[rank] <= 1e-13 * s_r[0]
 
 
-# The thread-stream kernel (tsqr_pt_kernel, m <= 8, n >= 4096): every
-# thread folds 8 strided rows at a time into its own R; ragged row counts,
-# zero / duplicated columns and low rank.
+# The thread-stream kernel (tsqr_pt_kernel, m <= 8, n >= 4096: every thread
+# folds 8 strided rows at a time into its own R) and the lane-group kernel
+# (tsqr_gs_kernel, 8 < m <= 32: 4 or 8 lanes share a stream by columns);
+# ragged row counts, zero / duplicated columns, low rank and a column whose
+# squared norms are subnormal.
 @pytest.mark.parametrize("n,m,kind", [(100003, 1, "dense"), (50000, 2, "dense"), (70001, 3, "dup"),
                                       (1 << 20, 4, "dense"), (65537, 5, "lowrank"), (200000, 8, "dup"),
-                                      (4096, 8, "dense"), (300001, 6, "dense"), (4099, 7, "dup")])
+                                      (4096, 8, "dense"), (300001, 6, "dense"), (4099, 7, "dup"),
+                                      (4096, 16, "dense"), (100003, 12, "dup"), (1 << 20, 16, "dense"),
+                                      (65537, 20, "lowrank"), (300001, 32, "dup"), (8191, 25, "dense"),
+                                      (200000, 9, "tiny")])
 def test_tsqr_thread_streams(tt, n, m, kind):
     from oracle.oracle import gaussian
     X = gaussian(n, m, 41 + m).copy(order="F")
@@ -120,6 +125,9 @@ def test_tsqr_thread_streams(tt, n, m, kind):
         X[:, 1] = 0.0
     if kind == "lowrank":
         X = np.asfortranarray(gaussian(n, 2, 5) @ gaussian(2, m, 6))
+    if kind == "tiny":
+        X[:, 3] *= 1e-156
+        X[:, 5] = 0.0
     R = host(tt.tsqr(X))
     assert np.all(np.isfinite(R))
     assert np.all(np.tril(R, -1) == 0.0)
@@ -127,9 +135,13 @@ def test_tsqr_thread_streams(tt, n, m, kind):
     s_r = np.linalg.svd(R, compute_uv=False)
     s_x = np.linalg.svd(X, compute_uv=False)
     assert np.max(np.abs(s_r - s_x)) <= 1e-10 * s_x[0]
-    if kind != "dense":
+    if kind in ("dup", "lowrank"):
         rank = 2 if kind == "lowrank" else m - 2
         assert s_r[rank] <= 1e-13 * s_r[0]
+    # orthogonal transforms keep column norms: ||R e_c|| = ||X e_c||, also for
+    # the 1e-156 column whose squares are subnormal (no flush to zero)
+    cn_r, cn_x = np.linalg.norm(R, axis=0), np.linalg.norm(X, axis=0)
+    assert np.allclose(cn_r, cn_x, rtol=1e-6 if kind == "tiny" else 1e-12, atol=1e-150)
     # the same bytes give the same R (fixed reduction order)
     assert np.array_equal(host(tt.tsqr(X)), R)
 
