@@ -67,7 +67,7 @@ struct ttsvd_cu_ctx {
     int64_t launches = 0;
     bool timing = false;
     // grow-only device workspaces
-    DevBuf ws_R, ws_R2, ws_P, ws_Scr, ws_G, ws_Gp, ws_A, ws_V, ws_Vacc, ws_U, ws_sigma, ws_flags, ws_work[2], ws_X, ws_send, ws_recv, ws_thick[2];
+    DevBuf ws_R, ws_R2, ws_P, ws_Scr, ws_G, ws_Gp, ws_A, ws_V, ws_Vacc, ws_U, ws_sigma, ws_flags, ws_work[2], ws_X, ws_send, ws_recv, ws_thick[2], ws_gs;
     DevBuf host_stage;  // pinned
     cudaEvent_t ev[7] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
     int last_kernel = 0;  // TTSVD_K_* of the last tsqr_device main sweep (ev[5], ev[6] bracket it when timing)
@@ -344,7 +344,7 @@ inline void kmark(ttsvd_cu_ctx* ctx, int i, int kernel) {
 // m <= 32: warp streams (tsqr_ws.cuh), levels of stacked factors until one
 // stream is left.
 template <int SW>
-int tsqr_ws_levels(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t ld, double* R) {
+int tsqr_ws_levels(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t ld, double* R, bool mark) {
     static int per_sm = -1;
     const size_t smem = ws_smem_bytes<SW>();
     if (per_sm < 0) {
@@ -368,10 +368,10 @@ int tsqr_ws_levels(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t
         const int64_t ldo = (S == 1) ? m : S * m;
         WsArgs wa{src, rows, sld, m, S, out, ldo};
         const int64_t grid = (S + per_cta - 1) / per_cta;
-        if (src == X) kmark(ctx, 0, TTSVD_K_WS);
+        if (mark && src == X) kmark(ctx, 0, TTSVD_K_WS);
         tsqr_ws_kernel<SW><<<(unsigned)grid, kWsThreads, smem, ctx->stream>>>(wa);
         TT_TRY(check_launch(ctx, "tsqr_ws_kernel"));
-        if (src == X) kmark(ctx, 1, TTSVD_K_WS);
+        if (mark && src == X) kmark(ctx, 1, TTSVD_K_WS);
         if (S == 1) return TTSVD_OK;
         src = out;
         rows = S * m;
@@ -380,8 +380,10 @@ int tsqr_ws_levels(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t
     }
 }
 
-int tsqr_ws_device(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t ld, double* R) {
-    return m <= 16 ? tsqr_ws_levels<16>(ctx, X, n, m, ld, R) : tsqr_ws_levels<32>(ctx, X, n, m, ld, R);
+// mark: bracket the first level with the timing events (false for the tail
+// of another kernel's levels)
+int tsqr_ws_device(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t ld, double* R, bool mark = true) {
+    return m <= 16 ? tsqr_ws_levels<16>(ctx, X, n, m, ld, R, mark) : tsqr_ws_levels<32>(ctx, X, n, m, ld, R, mark);
 }
 
 // m <= 8: thread streams (tsqr_pt.cuh), levels of stacked factors (~64 rows
@@ -447,8 +449,11 @@ int tsqr_gs_levels(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t
     }
     const int64_t max_t = (int64_t)per_sm * ctx->num_sms * (kPtThreads / P);
     int64_t T = std::max<int64_t>(1, std::min<int64_t>(n / 64, max_t));
-    if (T > 1) TT_TRY(ensure(ctx->ws_Scr, (size_t)T * m * m * 8));
-    double* out = (T == 1) ? R : as<double>(ctx->ws_Scr);
+    // the stacked factors get their own buffer (the warp-stream tail uses
+    // ws_R / ws_R2)
+    DevBuf& ob = ctx->ws_gs;
+    if (T > 1) TT_TRY(ensure(ob, (size_t)T * m * m * 8));
+    double* out = (T == 1) ? R : as<double>(ob);
     const int64_t ldo = (T == 1) ? m : T * m;
     GsArgs ga{X, n, ld, m, T, out, ldo};
     kmark(ctx, 0, TTSVD_K_GS);
@@ -459,11 +464,12 @@ int tsqr_gs_levels(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t
     if (T == 1) return TTSVD_OK;
     // the stacked factors are short: warp streams finish them with far
     // shorter per-stream chains than another group-stream level
-    return tsqr_ws_device(ctx, out, T * m, m, T * m, R);
+    return tsqr_ws_device(ctx, out, T * m, m, T * m, R, false);
 }
 
 int tsqr_gs_device(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t ld, double* R) {
     // measured on B200 (tools/gs_var.sh): 4 lanes per stream at m <= 16, 8 at m <= 32
+    // (a whole warp per stream at 32 < m <= 64 measured slower than t128)
     return m <= 16 ? tsqr_gs_levels<16, 4, 8>(ctx, X, n, m, ld, R) : tsqr_gs_levels<32, 8, 8>(ctx, X, n, m, ld, R);
 }
 
@@ -1052,7 +1058,7 @@ int ttsvd_cu_ctx_destroy(ttsvd_cu_ctx* ctx) {
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
     for (DevBuf* b : {&ctx->ws_R, &ctx->ws_R2, &ctx->ws_P, &ctx->ws_Scr, &ctx->ws_G, &ctx->ws_Gp, &ctx->ws_A, &ctx->ws_V, &ctx->ws_Vacc, &ctx->ws_U, &ctx->ws_sigma, &ctx->ws_flags, &ctx->ws_work[0],
-                      &ctx->ws_work[1], &ctx->ws_X, &ctx->ws_send, &ctx->ws_recv, &ctx->ws_thick[0], &ctx->ws_thick[1]})
+                      &ctx->ws_work[1], &ctx->ws_X, &ctx->ws_send, &ctx->ws_recv, &ctx->ws_thick[0], &ctx->ws_thick[1], &ctx->ws_gs})
         if (b->p) cudaFree(b->p);
     if (ctx->host_stage.p) cudaFreeHost(ctx->host_stage.p);
     for (auto& e : ctx->ev)
