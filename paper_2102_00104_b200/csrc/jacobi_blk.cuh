@@ -45,7 +45,8 @@ struct BjArgs {
     int C;    // CTAs in the cluster
     int* status;
     int max_sweeps;
-    long long* prof;  // optional (diagnostics): CTA 0 cycle sums [gram, solve, apply, moves + cluster barrier]
+    long long* prof;  // optional (diagnostics): CTA 0 cycle sums [gram, solve, apply, moves + cluster barrier],
+                      // then block-pair visits that rotated, per sweep (all CTAs) [4 + sweep]
 };
 
 constexpr int kBjThreads = 512;
@@ -275,8 +276,10 @@ __global__ void __launch_bounds__(kBjThreads, 1) jacobi_bj_kernel(BjArgs a) {
             if (k > 0 && grp == 0) db = cl.map_shared_rank(smem, k - 1) + (int64_t)ldst[par] * bsz;
             if (active) {
                 if (bj_visit(bt, bb, blt, blb, r == 0, m, n8, ldc, gpart[grp], Gs[grp], Qs[grp], &grp_rot[grp], grp, wg,
-                             wg == grp, lane, dt, db, bsz, pfv))
+                             wg == grp, lane, dt, db, bsz, pfv)) {
                     rot[sweep & 1] = 1;
+                    if (a.prof && lane == 0 && sweep < 28) atomicAdd((unsigned long long*)&a.prof[4 + sweep], 1ull);
+                }
             } else {
                 bj_copy_block(bt, dt, bsz, wg * 32 + lane);
                 bj_copy_block(bb, db, bsz, wg * 32 + lane);

@@ -31,31 +31,6 @@ struct PtArgs {
     int64_t ldo;
 };
 
-// 1/sqrt(x) and 1/x for the reflector scalars without the libdevice slow-path
-// calls (a call site inside the unrolled reflector loop pins every live value
-// across it): the SFU seed (measured max relative error 2^-20,
-// tools/approx_probe.cu) and one cubic Newton step (error ~2^-60, below the
-// final rounding).
-// x > 0; zero and the all-zero rules are handled by the caller.
-__device__ __forceinline__ double pt_rsqrt(double x) {
-    // subnormal squared norms (entries ~1e-155) would flush to zero in the
-    // seed: scale by an exact power of two instead
-    const bool tiny = x < 0x1p-1000;
-    const double xs = tiny ? x * 0x1p1000 : x;
-    double y;
-    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(xs));
-    const double e = fma(-xs, y * y, 1.0);
-    y = fma(fma(0.375, e, 0.5), e * y, y);
-    return tiny ? y * 0x1p500 : y;
-}
-
-__device__ __forceinline__ double pt_rcp(double x) {
-    double y;
-    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
-    const double e = fma(-x, y, 1.0);
-    return fma(fma(e, e, e), y, y);
-}
-
 template <int M, int U>
 __global__ void __launch_bounds__(kPtThreads) tsqr_pt_kernel(PtArgs a) {
     const int64_t s = (int64_t)blockIdx.x * kPtThreads + threadIdx.x;
@@ -81,7 +56,7 @@ __global__ void __launch_bounds__(kPtThreads) tsqr_pt_kernel(PtArgs a) {
             for (int u = 0; u < U; ++u) sp = fma(x[u][j], x[u][j], sp);
             const double u0 = R[j][j];
             const double nrm2 = u0 * u0 + sp;
-            const double inv = pt_rsqrt(nrm2);
+            const double inv = fast_rsqrt(nrm2);
             const double nr = nrm2 * inv;
             const double sg = (u0 > 0.0) ? 1.0 : -1.0;
             double alpha = -sg * nr;
@@ -89,7 +64,7 @@ __global__ void __launch_bounds__(kPtThreads) tsqr_pt_kernel(PtArgs a) {
             if (nrm2 == 0.0) alpha = sqrt(2.0 * DBL_MIN);  // all-zero u
             if (j + 1 < M) {
                 double tj = 1.0 + fabs(u0) * inv;
-                double scale = sg * pt_rcp(fabs(u0) + nr);
+                double scale = sg * fast_rcp(fabs(u0) + nr);
                 if (sp == 0.0 && u0 != 0.0) {
                     tj = 0.0;
                     scale = 0.0;
@@ -187,7 +162,7 @@ __global__ void __launch_bounds__(kPtThreads, GS_MINB) tsqr_gs_kernel(GsArgs a) 
             }
             const double u0 = __shfl_sync(kFull, R[j][kj], qj, P);
             const double nrm2 = u0 * u0 + sp;
-            const double inv = pt_rsqrt(nrm2);
+            const double inv = fast_rsqrt(nrm2);
             const double nr = nrm2 * inv;
             const double sg = (u0 > 0.0) ? 1.0 : -1.0;
             double alpha = -sg * nr;
@@ -195,7 +170,7 @@ __global__ void __launch_bounds__(kPtThreads, GS_MINB) tsqr_gs_kernel(GsArgs a) 
             if (nrm2 == 0.0) alpha = sqrt(2.0 * DBL_MIN);  // all-zero u
             if (j + 1 < M) {
                 double tj = 1.0 + fabs(u0) * inv;
-                double scale = sg * pt_rcp(fabs(u0) + nr);
+                double scale = sg * fast_rcp(fabs(u0) + nr);
                 if (sp == 0.0 && u0 != 0.0) {
                     tj = 0.0;
                     scale = 0.0;

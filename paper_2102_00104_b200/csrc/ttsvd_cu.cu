@@ -663,21 +663,23 @@ int jacobi_bj(ttsvd_cu_ctx* ctx, double* A, int n, int m, int* status, bool* lau
     static const bool prof = std::getenv("TTSVD_PROF_BJ") != nullptr;
     long long* dprof = nullptr;
     if (prof) {
-        TT_CUDA(cudaMalloc(&dprof, 8 * sizeof(long long)));
-        TT_CUDA(cudaMemset(dprof, 0, 8 * sizeof(long long)));
+        TT_CUDA(cudaMalloc(&dprof, 32 * sizeof(long long)));
+        TT_CUDA(cudaMemset(dprof, 0, 32 * sizeof(long long)));
     }
     BjArgs ba{A, n, m, n8, ldc, C, status, 30, dprof};
     TT_CUDA(cudaLaunchKernelEx(&cfg, jacobi_bj_kernel, ba));
     TT_TRY(check_launch(ctx, "jacobi_bj_kernel"));
     if (prof) {
-        long long h[8];
+        long long h[32];
         int sw = 0;
         TT_CUDA(cudaMemcpy(h, dprof, sizeof(h), cudaMemcpyDeviceToHost));
         TT_CUDA(cudaMemcpy(&sw, status, sizeof(int), cudaMemcpyDeviceToHost));
         cudaFree(dprof);
         const double rounds = (double)std::max(sw, 1) * (2 * kBjSlots * C - 1);
-        std::fprintf(stderr, "[bj prof] n=%d m=%d sweeps=%d per round cycles: gram %.0f solve %.0f apply %.0f moves+sync %.0f\n",
-                     n, m, sw, h[0] / rounds, h[1] / rounds, h[2] / rounds, h[3] / rounds);
+        std::fprintf(stderr, "[bj prof] n=%d m=%d sweeps=%d per round cycles: gram %.0f solve %.0f apply %.0f moves+sync %.0f; rotating visits per sweep (of %d):",
+                     n, m, sw, h[0] / rounds, h[1] / rounds, h[2] / rounds, h[3] / rounds, (2 * kBjSlots * C - 1) * kBjSlots * C);
+        for (int i = 0; i < std::min(sw, 28); ++i) std::fprintf(stderr, " %lld", h[4 + i]);
+        std::fprintf(stderr, "\n");
     }
     *launched = true;
     return TTSVD_OK;

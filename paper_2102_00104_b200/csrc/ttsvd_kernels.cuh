@@ -41,6 +41,31 @@ __device__ __forceinline__ void dmma884(double (&d)[2], double a, double b) {
                  : "d"(a), "d"(b));
 }
 
+// 1/sqrt(x) and 1/x for reflector / rotation scalars without the libdevice slow-path
+// calls (a call site inside the unrolled reflector loop pins every live value
+// across it): the SFU seed (measured max relative error 2^-20,
+// tools/approx_probe.cu) and one cubic Newton step (error ~2^-60, below the
+// final rounding).
+// x > 0; zero and the all-zero rules are handled by the caller.
+__device__ __forceinline__ double fast_rsqrt(double x) {
+    // subnormal squared norms (entries ~1e-155) would flush to zero in the
+    // seed: scale by an exact power of two instead
+    const bool tiny = x < 0x1p-1000;
+    const double xs = tiny ? x * 0x1p1000 : x;
+    double y;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(xs));
+    const double e = fma(-xs, y * y, 1.0);
+    y = fma(fma(0.375, e, 0.5), e * y, y);
+    return tiny ? y * 0x1p500 : y;
+}
+
+__device__ __forceinline__ double fast_rcp(double x) {
+    double y;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    const double e = fma(-x, y, 1.0);
+    return fma(fma(e, e, e), y, y);
+}
+
 __device__ __forceinline__ double ldg_stream(const double* p) {
     double v;
     asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
