@@ -1,0 +1,564 @@
+// K_SVD for the TT-SVD driver (no rotation accumulation): sigma and the
+// leading left singular vectors of the n x m work matrix A (n >= m; A = R^T
+// of a tall step or W^T of a wide step, so A's left singular vectors are the
+// right singular vectors of the step's matrix) by Householder
+// bidiagonalisation, bisection and inverse iteration — in place of the
+// one-sided Jacobi sweeps, whose ~13 sweeps x 127 rounds are latency bound.
+//
+//   1. bd_kernel (one thread-block cluster, A in the CTAs' shared memory,
+//      `cpc` columns per CTA): A = U_B B V_B^T, B upper bidiagonal (d, e).
+//      Step k: the left reflector of column k (owner CTA; LAPACK dlarfg
+//      normalisation, beta = -sign(alpha) ||x||), broadcast through
+//      distributed shared memory and applied by every CTA to its columns;
+//      then the right reflector of row k (row norm: one partial per CTA,
+//      summed in CTA order so every CTA derives the same reflector), its
+//      product z = A v reduce-scattered and all-gathered through DSMEM, and
+//      the rank-1 update.  Four cluster barriers per step.  Column k keeps
+//      the left reflector u_k below the diagonal (u_k[k] = 1).
+//   2. bd_bisect_kernel: every sigma of B (descending) by 32-way
+//      multisection per warp on the Golub-Kahan tridiagonal T (zero
+//      diagonal, off-diagonals d1 e1 d2 ... dm; Sturm counts of T - s I).
+//   3. bd_vectors_kernel: the left singular vectors x of B for the leading
+//      r sigmas by inverse iteration on T (the x entries of T's eigenvector
+//      (y1 x1 y2 x2 ...)); sigmas closer than 1e-3 ||T|| form a cluster that
+//      one thread iterates with modified Gram-Schmidt against its earlier
+//      members (LAPACK dstein's scheme).
+//   4. bd_back_kernel: V = U_B [x; 0] by the stored left reflectors.
+//
+// sigma is accurate to ~eps ||A|| absolute (backward stable
+// bidiagonalisation; bisection to 1e-18 ||T||), vector i to
+// ~eps ||A|| / gap_i, the same orders as the Jacobi path's normalised
+// columns.
+#pragma once
+
+#include <cfloat>
+#include <cstdint>
+
+namespace ttsvd_b200 {
+
+constexpr int kBdThreads = 512;
+
+struct BdArgs {
+    double* A;  // n x m (ld n), overwritten below the diagonal with the left reflectors
+    int n, m, cpc;
+    double* d;     // m
+    double* e;     // m - 1
+    double* tauL;  // m
+    long long* prof;  // optional (diagnostics): CTA 0 cycle sums per phase
+};
+
+inline size_t bd_smem_bytes(int n, int cpc) { return ((size_t)cpc * n + 4 * (size_t)n + (size_t)cpc + 8) * sizeof(double); }
+
+// sum over the CTA (every thread gets the same value; fixed order)
+__device__ __forceinline__ double bd_block_sum(double v, double* red) {
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    __syncthreads();
+    if (lane == 0) red[warp] = v;
+    __syncthreads();
+    double s = 0.0;
+#pragma unroll
+    for (int w = 0; w < kBdThreads / 32; ++w) s += red[w];
+    return s;
+}
+
+__device__ __forceinline__ double bd_warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+__global__ void __launch_bounds__(kBdThreads, 1) bd_kernel(BdArgs a) {
+    cg::cluster_group cl = cg::this_cluster();
+    extern __shared__ __align__(16) double sm[];
+    __shared__ double red[32];
+    __shared__ double pub[4];  // [k & 1] tau_L (owner of column k; two slots: the last steps have no
+                               // barrier between a read and the next write), [2] row-norm partial, [3] A[k][k+1]
+    __shared__ double rs[2];   // row reflector inputs, CTA-local copies
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int C = (int)cl.num_blocks(), rank = (int)cl.block_rank();
+    const int n = a.n, m = a.m, cpc = a.cpc;
+    double* As = sm;          // cpc columns, ld n
+    double* ub = As + (size_t)cpc * n;
+    double* zp = ub + n;      // partial z over my columns
+    double* zr = zp + n;      // reduced z, my row slice
+    double* zf = zr + n;      // full z
+    double* vl = zf + n;      // right reflector, my columns
+    const int c0 = rank * cpc;
+    const int sl = (n + C - 1) / C;
+    for (int e = tid; e < cpc * n; e += kBdThreads) {
+        const int j = e / n, i = e - j * n, gj = c0 + j;
+        As[e] = gj < m ? a.A[(int64_t)gj * n + i] : 0.0;
+    }
+    __syncthreads();
+    cl.sync();
+    long long* pf = (a.prof && rank == 0 && tid == 0) ? a.prof : nullptr;
+    long long tp = pf ? bj_clock() : 0;
+#define BD_MARK(i)                           \
+    if (pf) {                                \
+        const long long tq = bj_clock();     \
+        pf[i] += tq - tp;                    \
+        tp = tq;                             \
+    }
+    for (int k = 0; k < m; ++k) {
+        const int o = k / cpc, lk = k - o * cpc;
+        // ---- left reflector of column k (owner) ----
+        if (rank == o) {
+            double* col = As + (size_t)lk * n;
+            double s = 0.0;
+            for (int i = k + 1 + tid; i < n; i += kBdThreads) s = fma(col[i], col[i], s);
+            s = bd_block_sum(s, red);
+            const double alpha = col[k];
+            double tau = 0.0, beta = alpha, scale = 0.0;
+            if (s != 0.0) {
+                const double nr = sqrt(fma(alpha, alpha, s));
+                beta = alpha >= 0.0 ? -nr : nr;
+                tau = (beta - alpha) / beta;
+                scale = 1.0 / (alpha - beta);
+            }
+            for (int i = k + 1 + tid; i < n; i += kBdThreads) col[i] *= scale;
+            __syncthreads();
+            if (tid == 0) {
+                col[k] = 1.0;
+                pub[k & 1] = tau;
+                a.d[k] = beta;
+                a.tauL[k] = tau;
+            }
+        }
+        cl.sync();
+        BD_MARK(0)
+        {
+            const double* ucol = cl.map_shared_rank(As, o) + (size_t)lk * n;
+            for (int i = k + tid; i < n; i += kBdThreads) ub[i] = ucol[i];
+            if (tid == 0) rs[0] = *cl.map_shared_rank(&pub[k & 1], o);
+        }
+        __syncthreads();
+        BD_MARK(1)
+        const double tauL = rs[0];
+        if (tauL != 0.0) {
+            for (int lj = warp; lj < cpc; lj += kBdThreads / 32) {
+                const int gj = c0 + lj;
+                if (gj <= k || gj >= m) continue;
+                double* col = As + (size_t)lj * n;
+                double dot = 0.0;
+                for (int i = k + lane; i < n; i += 32) dot = fma(ub[i], col[i], dot);
+                const double w = tauL * bd_warp_sum(dot);
+                for (int i = k + lane; i < n; i += 32) col[i] = fma(-w, ub[i], col[i]);
+            }
+        }
+        __syncthreads();
+        BD_MARK(2)
+        if (k + 2 < m) {
+            // ---- right reflector of row k (columns k+1 ..) ----
+            double s = 0.0;
+            if (tid < cpc) {
+                const int gj = c0 + tid;
+                if (gj >= k + 2 && gj < m) {
+                    const double v = As[(size_t)tid * n + k];
+                    s = v * v;
+                }
+            }
+            s = bd_block_sum(s, red);
+            if (tid == 0) {
+                pub[2] = s;
+                if ((k + 1) / cpc == rank) pub[3] = As[(size_t)(k + 1 - c0) * n + k];
+            }
+            cl.sync();
+            BD_MARK(3)
+            if (warp == 0) {
+                double p = lane < C ? *cl.map_shared_rank(&pub[2], lane) : 0.0;
+                p = bd_warp_sum(p);
+                if (lane == 0) {
+                    rs[0] = p;
+                    rs[1] = *cl.map_shared_rank(&pub[3], (k + 1) / cpc);
+                }
+            }
+            __syncthreads();
+            const double st = rs[0], y0 = rs[1];
+            double tauR = 0.0, gamma = y0, scaleR = 0.0;
+            if (st != 0.0) {
+                const double nr = sqrt(fma(y0, y0, st));
+                gamma = y0 >= 0.0 ? -nr : nr;
+                tauR = (gamma - y0) / gamma;
+                scaleR = 1.0 / (y0 - gamma);
+            }
+            if (rank == 0 && tid == 0) a.e[k] = gamma;
+            if (tid < cpc) {
+                const int gj = c0 + tid;
+                vl[tid] = (gj == k + 1) ? 1.0 : ((gj >= k + 2 && gj < m) ? As[(size_t)tid * n + k] * scaleR : 0.0);
+            }
+            __syncthreads();
+            if (tauR != 0.0) {
+                for (int i = k + 1 + tid; i < n; i += kBdThreads) {
+                    double z = 0.0;
+                    for (int lj = 0; lj < cpc; ++lj) z = fma(As[(size_t)lj * n + i], vl[lj], z);
+                    zp[i] = z;
+                }
+                BD_MARK(4)
+                cl.sync();
+                BD_MARK(5)
+                {
+                    const int i0 = max(rank * sl, k + 1), i1 = min(n, (rank + 1) * sl);
+                    for (int i = i0 + tid; i < i1; i += kBdThreads) {
+                        double z = 0.0;
+                        for (int t = 0; t < C; ++t) z += cl.map_shared_rank(zp, t)[i];
+                        zr[i] = tauR * z;
+                    }
+                }
+                BD_MARK(6)
+                cl.sync();
+                BD_MARK(7)
+                for (int i = k + 1 + tid; i < n; i += kBdThreads) zf[i] = cl.map_shared_rank(zr, i / sl)[i];
+                __syncthreads();
+                BD_MARK(8)
+                for (int i = k + 1 + tid; i < n; i += kBdThreads) {
+                    const double z = zf[i];
+                    for (int lj = 0; lj < cpc; ++lj) As[(size_t)lj * n + i] = fma(-z, vl[lj], As[(size_t)lj * n + i]);
+                }
+            }
+            __syncthreads();
+            BD_MARK(9)
+        } else if (k + 2 == m) {
+            if ((k + 1) / cpc == rank && tid == 0) a.e[k] = As[(size_t)(k + 1 - c0) * n + k];
+        }
+    }
+#undef BD_MARK
+    cl.sync();
+    for (int e = tid; e < cpc * n; e += kBdThreads) {
+        const int j = e / n, i = e - j * n, gj = c0 + j;
+        if (gj < m) a.A[(int64_t)gj * n + i] = As[e];
+    }
+}
+
+// off-diagonal t (0..2m-2) of the Golub-Kahan tridiagonal: d0 e0 d1 e1 ... d_{m-1}
+__device__ __forceinline__ double bd_tgk(const double* d, const double* e, int t) {
+    return (t & 1) ? e[t >> 1] : d[t >> 1];
+}
+
+constexpr int kBisThreads = 256;
+
+// Sturm count: eigenvalues of T (zero diagonal, squared off-diagonals b2,
+// 2m x 2m) below s
+__device__ __forceinline__ int bd_sturm(const double* b2, int N, double s, double pivmin) {
+    double q = -s;
+    if (fabs(q) < pivmin) q = -pivmin;
+    int c = q < 0.0;
+    for (int t = 1; t < N; ++t) {
+        q = -s - b2[t - 1] * fast_rcp(q);
+        if (fabs(q) < pivmin) q = -pivmin;
+        c += q < 0.0;
+    }
+    return c;
+}
+
+// warp per sigma (descending index); every CTA stages T's squared
+// off-diagonals and the Gershgorin bound
+__global__ void __launch_bounds__(kBisThreads) bd_bisect_kernel(const double* d, const double* e, int m, double* sigma) {
+    extern __shared__ double b2[];  // 2m - 1
+    __shared__ double red[kBisThreads / 32][2];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int N = 2 * m;
+    double bmax = 0.0, b2max = 0.0;
+    for (int t = tid; t < N - 1; t += kBisThreads) {
+        const double b = bd_tgk(d, e, t);
+        b2[t] = b * b;
+        const double g = fabs(b) + (t > 0 ? fabs(bd_tgk(d, e, t - 1)) : 0.0);
+        const double g2 = fabs(b) + (t + 1 < N - 1 ? fabs(bd_tgk(d, e, t + 1)) : 0.0);
+        bmax = fmax(bmax, fmax(g, g2));
+        b2max = fmax(b2max, b * b);
+    }
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) {
+        bmax = fmax(bmax, __shfl_xor_sync(0xffffffffu, bmax, o));
+        b2max = fmax(b2max, __shfl_xor_sync(0xffffffffu, b2max, o));
+    }
+    if (lane == 0) {
+        red[warp][0] = bmax;
+        red[warp][1] = b2max;
+    }
+    __syncthreads();
+    bmax = 0.0;
+    b2max = 0.0;
+    for (int w = 0; w < kBisThreads / 32; ++w) {
+        bmax = fmax(bmax, red[w][0]);
+        b2max = fmax(b2max, red[w][1]);
+    }
+    const int i = blockIdx.x * (kBisThreads / 32) + warp;
+    if (i >= m) return;
+    if (N == 2) {  // 1 x 1: sigma = |d0|
+        if (lane == 0) sigma[0] = fabs(d[0]);
+        return;
+    }
+    const double pivmin = DBL_MIN * fmax(1.0, b2max);
+    const int j = m - 1 - i;  // ascending index
+    double lo = 0.0, hi = bmax * (1.0 + 4.0 * DBL_EPSILON) + pivmin;
+    const double floor_tol = 1e-18 * hi;
+    for (int it = 0; it < 40; ++it) {
+        if (hi - lo <= fmax(2.0 * DBL_EPSILON * hi, floor_tol)) break;
+        const double s = lo + (hi - lo) * (double)(lane + 1) * (1.0 / 33.0);
+        const int cnt = bd_sturm(b2, N, s, pivmin) - m;
+        const unsigned above = __ballot_sync(0xffffffffu, cnt > j);
+        const double s_f = __shfl_sync(0xffffffffu, s, above ? __ffs(above) - 1 : 31);
+        const double s_b = __shfl_sync(0xffffffffu, s, above ? max(__ffs(above) - 2, 0) : 31);
+        if (above) {
+            const int f = __ffs(above) - 1;
+            hi = s_f;
+            if (f > 0) lo = s_b;
+        } else {
+            lo = s_f;
+        }
+    }
+    if (lane == 0) sigma[i] = 0.5 * (lo + hi);
+}
+
+// inverse iteration on T - sigma I for the leading r sigmas; thread per
+// cluster leader.  Scratch per thread: 5 * 2m doubles + 2m ints (global).
+// sigmas closer than kBdOrtol ||T|| are a cluster (bd_vectors_kernel)
+constexpr double kBdOrtol = 1e-6;
+
+struct BdVecArgs {
+    const double* d;
+    const double* e;
+    const double* sigma;
+    int m, r;
+    double* scratch;  // r * 7 * 2m doubles
+    double* X;        // m x r (ld m): left singular vectors of B
+};
+
+__device__ void bd_solve(const double* dl, const double* dg, const double* du, const double* du2, const int* ip, int N,
+                         double* z) {
+    // L: forward with row interchanges (dgttrs)
+    for (int t = 0; t < N - 1; ++t) {
+        if (ip[t]) {
+            const double tmp = z[t];
+            z[t] = z[t + 1];
+            z[t + 1] = tmp - dl[t] * z[t];
+        } else {
+            z[t + 1] -= dl[t] * z[t];
+        }
+    }
+    // U: backward (diagonal dg, super du, second super du2)
+    z[N - 1] /= dg[N - 1];
+    if (N > 1) z[N - 2] = (z[N - 2] - du[N - 2] * z[N - 1]) / dg[N - 2];
+    for (int t = N - 3; t >= 0; --t) z[t] = (z[t] - du[t] * z[t + 1] - du2[t] * z[t + 2]) / dg[t];
+}
+
+__global__ void bd_vectors_kernel(BdVecArgs a) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const int m = a.m, r = a.r, N = 2 * m;
+    if (i >= r) return;
+    // Gershgorin bound of T (scale of the cluster tolerance and pivot floor)
+    double tn = 0.0;
+    for (int t = 0; t < N - 1; ++t) tn = fmax(tn, fabs(bd_tgk(a.d, a.e, t)) + (t > 0 ? fabs(bd_tgk(a.d, a.e, t - 1)) : 0.0));
+    tn = fmax(tn, N > 1 ? fabs(bd_tgk(a.d, a.e, N - 2)) : 0.0);
+    const double ortol = kBdOrtol * tn;
+    if (i > 0 && a.sigma[i - 1] - a.sigma[i] <= ortol) return;  // not a cluster leader
+    int last = i;
+    while (last + 1 < r && a.sigma[last] - a.sigma[last + 1] <= ortol) ++last;
+    if (last == i) return;  // isolated: bd_twisted_kernel's vector stands
+    double* base = a.scratch + (size_t)i * 7 * N;
+    double* dl = base;
+    double* dg = dl + N;
+    double* du = dg + N;
+    double* du2 = du + N;
+    int* ip = reinterpret_cast<int*>(du2 + 2 * N);
+    const double tiny = DBL_EPSILON * tn + DBL_MIN;
+    for (int v = i; v <= last; ++v) {
+        double* z = a.scratch + (size_t)v * 7 * N + 4 * N;  // member v's eigenvector of T (kept for the later members)
+        const double s = a.sigma[v];
+        // factor T - s I (dgttrf: partial pivoting)
+        for (int t = 0; t < N; ++t) dg[t] = -s;
+        for (int t = 0; t < N - 1; ++t) {
+            du[t] = bd_tgk(a.d, a.e, t);
+            dl[t] = du[t];
+        }
+        for (int t = 0; t < N - 2; ++t) du2[t] = 0.0;
+        for (int t = 0; t < N - 1; ++t) {
+            if (fabs(dg[t]) >= fabs(dl[t])) {
+                ip[t] = 0;
+                if (dg[t] == 0.0) dg[t] = tiny;
+                const double f = dl[t] / dg[t];
+                dl[t] = f;
+                dg[t + 1] -= f * du[t];
+            } else {
+                ip[t] = 1;
+                const double f = dg[t] / dl[t];
+                dg[t] = dl[t];
+                dl[t] = f;
+                const double tmp = du[t];
+                du[t] = dg[t + 1];
+                dg[t + 1] = tmp - f * dg[t + 1];
+                if (t < N - 2) {
+                    du2[t] = du[t + 1];
+                    du[t + 1] = -f * du[t + 1];
+                }
+            }
+        }
+        if (dg[N - 1] == 0.0) dg[N - 1] = tiny;
+        for (int t = 0; t < N - 1; ++t)
+            if (dg[t] == 0.0) dg[t] = tiny;
+        // start: a fixed pseudo-random vector
+        unsigned h = 0x9e3779b9u * (unsigned)(v + 1);
+        for (int t = 0; t < N; ++t) {
+            h ^= h << 13;
+            h ^= h >> 17;
+            h ^= h << 5;
+            z[t] = 0.5 + (double)(h & 0xffffu) * (1.0 / 65536.0);
+        }
+        for (int it = 0; it < 3; ++it) {
+            bd_solve(dl, dg, du, du2, ip, N, z);
+            // orthogonalise against the cluster's earlier members
+            for (int w = i; w < v; ++w) {
+                const double* zw = a.scratch + (size_t)w * 7 * N + 4 * N;
+                double dt = 0.0;
+                for (int t = 0; t < N; ++t) dt = fma(zw[t], z[t], dt);
+                for (int t = 0; t < N; ++t) z[t] = fma(-dt, zw[t], z[t]);
+            }
+            double nr = 0.0;
+            for (int t = 0; t < N; ++t) nr = fma(z[t], z[t], nr);
+            const double inv = 1.0 / sqrt(nr);
+            for (int t = 0; t < N; ++t) z[t] *= inv;
+        }
+        // x entries (odd positions), normalised
+        double nx = 0.0;
+        for (int k = 0; k < m; ++k) nx = fma(z[2 * k + 1], z[2 * k + 1], nx);
+        const double ix = nx > 0.0 ? 1.0 / sqrt(nx) : 0.0;
+        for (int k = 0; k < m; ++k) a.X[(size_t)v * m + k] = z[2 * k + 1] * ix;
+    }
+}
+
+// Fast path of the vectors: one twisted factorisation per sigma (warp per
+// vector; lanes 0 / 1 run the top-down LDL^T and bottom-up UDU^T of T - sI
+// concurrently, the twist index minimises |gamma_k|, and the eigenvector
+// follows from z_k = 1 by products only) — one inverse-iteration step from
+// the optimal start vector e_k.  Vectors whose sigma lies within kBdOrtol
+// ||T|| of a neighbour are redone by bd_vectors_kernel (clusters).
+constexpr int kTwWarps = 4;
+
+__global__ void __launch_bounds__(kTwWarps * 32) bd_twisted_kernel(BdVecArgs a) {
+    extern __shared__ double tw[];  // per warp: D+ (N), D- (N)
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int v = blockIdx.x * kTwWarps + warp;
+    const int m = a.m, N = 2 * m;
+    if (v >= a.r) return;
+    double* dp = tw + (size_t)warp * 2 * N;
+    double* dm = dp + N;
+    double tn = 0.0, b2max = 0.0;
+    for (int t = lane; t < N - 1; t += 32) {
+        const double b = fabs(bd_tgk(a.d, a.e, t));
+        tn = fmax(tn, b + (t > 0 ? fabs(bd_tgk(a.d, a.e, t - 1)) : 0.0));
+        tn = fmax(tn, b + (t + 1 < N - 1 ? fabs(bd_tgk(a.d, a.e, t + 1)) : 0.0));
+        b2max = fmax(b2max, b * b);
+    }
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) {
+        tn = fmax(tn, __shfl_xor_sync(0xffffffffu, tn, o));
+        b2max = fmax(b2max, __shfl_xor_sync(0xffffffffu, b2max, o));
+    }
+    const double s = a.sigma[v];
+    const double pivmin = DBL_MIN * fmax(1.0, b2max);
+    // T - sI = L D+ L^T (top-down, lane 0) = U D- U^T (bottom-up, lane 1)
+    if (lane == 0) {
+        double q = -s;
+        if (fabs(q) < pivmin) q = -pivmin;
+        dp[0] = q;
+        for (int t = 1; t < N; ++t) {
+            const double b = bd_tgk(a.d, a.e, t - 1);
+            q = -s - b * b * fast_rcp(q);
+            if (fabs(q) < pivmin) q = -pivmin;
+            dp[t] = q;
+        }
+    } else if (lane == 1) {
+        double q = -s;
+        if (fabs(q) < pivmin) q = -pivmin;
+        dm[N - 1] = q;
+        for (int t = N - 2; t >= 0; --t) {
+            const double b = bd_tgk(a.d, a.e, t);
+            q = -s - b * b * fast_rcp(q);
+            if (fabs(q) < pivmin) q = -pivmin;
+            dm[t] = q;
+        }
+    }
+    __syncwarp();
+    // twist: gamma_k = D+_k + D-_k - (T - sI)_kk = D+_k + D-_k + s
+    double best = DBL_MAX;
+    int kb = 0;
+    for (int t = lane; t < N; t += 32) {
+        const double g = fabs(dp[t] + dm[t] + s);
+        if (g < best) {
+            best = g;
+            kb = t;
+        }
+    }
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) {
+        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+        const int ok = __shfl_xor_sync(0xffffffffu, kb, o);
+        if (ob < best || (ob == best && ok < kb)) {
+            best = ob;
+            kb = ok;
+        }
+    }
+    // z_k = 1; upward z_t = -(b_t / D+_t) z_{t+1} (lane 0), downward
+    // z_{t+1} = -(b_t / D-_{t+1}) z_t (lane 1); z overwrites dp / dm
+    if (lane == 0) {
+        double z = 1.0;
+        for (int t = kb - 1; t >= 0; --t) {
+            z = -bd_tgk(a.d, a.e, t) * fast_rcp(dp[t]) * z;
+            dp[t] = z;
+        }
+    } else if (lane == 1) {
+        double z = 1.0;
+        for (int t = kb; t < N - 1; ++t) {
+            z = -bd_tgk(a.d, a.e, t) * fast_rcp(dm[t + 1]) * z;
+            dm[t + 1] = z;
+        }
+    }
+    __syncwarp();
+    // x entries: odd positions (z_t from dp for t < kb, 1 at kb, dm for t > kb)
+    double nx = 0.0;
+    for (int k = lane; k < m; k += 32) {
+        const int t = 2 * k + 1;
+        const double z = t < kb ? dp[t] : (t == kb ? 1.0 : dm[t]);
+        nx = fma(z, z, nx);
+    }
+    nx = bd_warp_sum(nx);
+    const double ix = nx > 0.0 ? 1.0 / sqrt(nx) : 0.0;
+    for (int k = lane; k < m; k += 32) {
+        const int t = 2 * k + 1;
+        const double z = t < kb ? dp[t] : (t == kb ? 1.0 : dm[t]);
+        a.X[(size_t)v * m + k] = z * ix;
+    }
+}
+
+// V (n x r, ld n) = U_B [X; 0]: the left reflectors of bd_kernel applied in
+// reverse; warp per vector
+constexpr int kBackWarps = 4;
+
+__global__ void __launch_bounds__(kBackWarps * 32) bd_back_kernel(const double* A, const double* tauL, int n, int m,
+                                                                  const double* X, int r, double* V) {
+    extern __shared__ double xs[];  // kBackWarps x n
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int v = blockIdx.x * kBackWarps + warp;
+    if (v >= r) return;
+    double* x = xs + (size_t)warp * n;
+    for (int i = lane; i < n; i += 32) x[i] = i < m ? X[(size_t)v * m + i] : 0.0;
+    __syncwarp();
+    for (int k = m - 1; k >= 0; --k) {
+        const double tau = tauL[k];
+        if (tau == 0.0) continue;
+        const double* u = A + (size_t)k * n;
+        double dot = 0.0;
+        for (int i = k + 1 + lane; i < n; i += 32) dot = fma(u[i], x[i], dot);
+        dot = bd_warp_sum(dot) + x[k];
+        const double w = tau * dot;
+        __syncwarp();
+        if (lane == 0) x[k] -= w;
+        for (int i = k + 1 + lane; i < n; i += 32) x[i] = fma(-w, u[i], x[i]);
+        __syncwarp();
+    }
+    for (int i = lane; i < n; i += 32) V[(size_t)v * n + i] = x[i];
+}
+
+}  // namespace ttsvd_b200

@@ -21,6 +21,7 @@
 #include "tsqr_blk.cuh"
 #include "gqr.cuh"
 #include "jacobi_blk.cuh"
+#include "bidiag.cuh"
 #include "tsqr_la.cuh"
 #include "tsqr_t128.cuh"
 #include "tsqr_ws.cuh"
@@ -67,9 +68,14 @@ struct ttsvd_cu_ctx {
     int64_t launches = 0;
     bool timing = false;
     // grow-only device workspaces
-    DevBuf ws_R, ws_R2, ws_P, ws_Scr, ws_G, ws_Gp, ws_A, ws_V, ws_Vacc, ws_U, ws_sigma, ws_flags, ws_work[2], ws_X, ws_send, ws_recv, ws_thick[2], ws_gs;
+    DevBuf ws_R, ws_R2, ws_P, ws_Scr, ws_G, ws_Gp, ws_A, ws_V, ws_Vacc, ws_U, ws_sigma, ws_flags, ws_work[2], ws_X, ws_send, ws_recv, ws_thick[2], ws_gs, ws_bd;
     DevBuf host_stage;  // pinned
     cudaEvent_t ev[7] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+    // svd_work's bidiagonal path leaves the vectors for svd_vectors (the
+    // driver knows the rank only after the sigmas): A holds the reflectors
+    bool bd_pending = false;
+    const double* bd_A = nullptr;
+    int bd_n = 0, bd_m = 0;
     int last_kernel = 0;  // TTSVD_K_* of the last tsqr_device main sweep (ev[5], ev[6] bracket it when timing)
 };
 
@@ -739,6 +745,102 @@ int finalize_device(ttsvd_cu_ctx* ctx, const double* A, int n, int m, const doub
     return check_launch(ctx, "jacobi_finalize_kernel");
 }
 
+// Bidiagonal path (bidiag.cuh) of svd_work: sigma now, the vectors later by
+// svd_vectors.  Returns -1 (nothing launched) when A does not fit the cluster.
+constexpr int kBdCluster = 16;
+constexpr int kBdMinM = 64;
+int bd_sigma(ttsvd_cu_ctx* ctx, double* A, int n, int m, double* sigma) {
+    const int cpc = (m + kBdCluster - 1) / kBdCluster;
+    const size_t smem = bd_smem_bytes(n, cpc);
+    static int static_smem = -1;
+    if (static_smem < 0) {
+        cudaFuncAttributes fa;
+        TT_CUDA(cudaFuncGetAttributes(&fa, bd_kernel));
+        static_smem = (int)fa.sharedSizeBytes;
+        TT_CUDA(cudaFuncSetAttribute(bd_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        TT_CUDA(cudaFuncSetAttribute(bd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit - static_smem));
+    }
+    if (n < m || smem > (size_t)(kSmemLimit - static_smem)) return -1;
+    TT_TRY(ensure(ctx->ws_bd, (size_t)3 * m * 8));
+    double* d = as<double>(ctx->ws_bd);
+    double* e = d + m;
+    double* tauL = e + m;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(kBdCluster);
+    cfg.blockDim = dim3(kBdThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = ctx->stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = kBdCluster;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    static const bool prof = std::getenv("TTSVD_PROF_BD") != nullptr;
+    long long* dprof = nullptr;
+    if (prof) {
+        TT_CUDA(cudaMalloc(&dprof, 16 * sizeof(long long)));
+        TT_CUDA(cudaMemset(dprof, 0, 16 * sizeof(long long)));
+    }
+    BdArgs ba{A, n, m, cpc, d, e, tauL, dprof};
+    TT_CUDA(cudaLaunchKernelEx(&cfg, bd_kernel, ba));
+    TT_TRY(check_launch(ctx, "bd_kernel"));
+    if (prof) {
+        long long h[16];
+        TT_CUDA(cudaMemcpy(h, dprof, sizeof(h), cudaMemcpyDeviceToHost));
+        cudaFree(dprof);
+        std::fprintf(stderr, "[bd prof] n=%d m=%d cycles per step: left+B1 %.0f ucopy %.0f lupdate %.0f rnorm+B2 %.0f refl+zpart %.0f B3 %.0f reduce %.0f B4 %.0f gather %.0f update %.0f\n",
+                     n, m, h[0] / (double)m, h[1] / (double)m, h[2] / (double)m, h[3] / (double)m, h[4] / (double)m,
+                     h[5] / (double)m, h[6] / (double)m, h[7] / (double)m, h[8] / (double)m, h[9] / (double)m);
+    }
+    const int wpb = kBisThreads / 32;
+    bd_bisect_kernel<<<(m + wpb - 1) / wpb, kBisThreads, (size_t)(2 * m) * 8, ctx->stream>>>(d, e, m, sigma);
+    TT_TRY(check_launch(ctx, "bd_bisect_kernel"));
+    ctx->bd_pending = true;
+    ctx->bd_A = A;
+    ctx->bd_n = n;
+    ctx->bd_m = m;
+    return TTSVD_OK;
+}
+
+// The leading r left singular vectors of svd_work's A (n x r, ld n) when the
+// bidiagonal path ran; no-op after the Jacobi path (its Vout is complete).
+int svd_vectors(ttsvd_cu_ctx* ctx, int64_t r, const double* sigma, double* Vout) {
+    if (!ctx->bd_pending) return TTSVD_OK;
+    ctx->bd_pending = false;
+    const int n = ctx->bd_n, m = ctx->bd_m;
+    if (r < 1) return TTSVD_OK;
+    r = std::min<int64_t>(r, m);
+    double* d = as<double>(ctx->ws_bd);
+    double* e = d + m;
+    double* tauL = e + m;
+    TT_TRY(ensure(ctx->ws_Scr, (size_t)r * (7 * 2 * (size_t)m + m) * 8));
+    double* scratch = as<double>(ctx->ws_Scr);
+    double* X = scratch + (size_t)r * 7 * 2 * m;
+    BdVecArgs va{d, e, sigma, m, (int)r, scratch, X};
+    const size_t tsm = (size_t)kTwWarps * 4 * m * 8;
+    static bool tattr = false;
+    if (!tattr) {
+        TT_CUDA(cudaFuncSetAttribute(bd_twisted_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit));
+        tattr = true;
+    }
+    bd_twisted_kernel<<<(unsigned)((r + kTwWarps - 1) / kTwWarps), kTwWarps * 32, tsm, ctx->stream>>>(va);
+    TT_TRY(check_launch(ctx, "bd_twisted_kernel"));
+    // clusters (rare): inverse iteration with modified Gram-Schmidt
+    bd_vectors_kernel<<<(unsigned)((r + 63) / 64), 64, 0, ctx->stream>>>(va);
+    TT_TRY(check_launch(ctx, "bd_vectors_kernel"));
+    const size_t smem = (size_t)kBackWarps * n * 8;
+    static bool attr = false;
+    if (!attr) {
+        TT_CUDA(cudaFuncSetAttribute(bd_back_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit));
+        attr = true;
+    }
+    bd_back_kernel<<<(unsigned)((r + kBackWarps - 1) / kBackWarps), kBackWarps * 32, smem, ctx->stream>>>(
+        ctx->bd_A, tauL, n, m, X, (int)r, Vout);
+    return check_launch(ctx, "bd_back_kernel");
+}
+
 // sigma and right singular vectors of a work matrix.
 //   accumulate == true (the small_svd / jacobi_svd API, small_svd.hpp:72-114):
 //     one-sided Jacobi on the columns of R with the rotations accumulated
@@ -766,7 +868,17 @@ int svd_work(ttsvd_cu_ctx* ctx, const double* src, int64_t src_rows, int64_t src
     } else {
         TT_CUDA(cudaMemcpy2DAsync(A, n * 8, src, src_ld * 8, n * 8, m, cudaMemcpyDeviceToDevice, ctx->stream));
     }
+    ctx->bd_pending = false;
     if (!accumulate) {
+        static const char* ssel = std::getenv("TTSVD_SVD");  // diagnostics: "jacobi" forces the sweeps
+        const bool jac = ssel && std::string(ssel) == "jacobi";
+        if (!jac && m >= kBdMinM) {
+            const int rc = bd_sigma(ctx, A, (int)n, (int)m, sigma);
+            if (rc != -1) {
+                *sweeps = 0;
+                return rc;
+            }
+        }
         TT_TRY(jacobi_device(ctx, A, (int)n, (int)m, nullptr));
         TT_TRY(jacobi_status(ctx, sweeps));
         return finalize_device(ctx, A, (int)n, (int)m, nullptr, sigma, Vout, nullptr);
@@ -964,6 +1076,7 @@ int run_chain(ttsvd_cu_ctx* ctx, WorkView cur, const std::vector<int64_t>& dims,
         const int64_t rnew = choose_rank_h(sig.data(), nsig, cur.cols, nsig, delta, r_max, cur.rows);
         st.nsig = nsig;
         st.rank = rnew;
+        TT_TRY(svd_vectors(ctx, rnew, d_sigma, d_V));
         // core_from_vt (tt_svd.hpp:121-128) from the first rnew columns of V
         Vh.resize((size_t)m * rnew);
         TT_TRY(d2h(ctx, Vh.data(), d_V, (size_t)m * rnew));
@@ -1060,7 +1173,7 @@ int ttsvd_cu_ctx_destroy(ttsvd_cu_ctx* ctx) {
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
     for (DevBuf* b : {&ctx->ws_R, &ctx->ws_R2, &ctx->ws_P, &ctx->ws_Scr, &ctx->ws_G, &ctx->ws_Gp, &ctx->ws_A, &ctx->ws_V, &ctx->ws_Vacc, &ctx->ws_U, &ctx->ws_sigma, &ctx->ws_flags, &ctx->ws_work[0],
-                      &ctx->ws_work[1], &ctx->ws_X, &ctx->ws_send, &ctx->ws_recv, &ctx->ws_thick[0], &ctx->ws_thick[1], &ctx->ws_gs})
+                      &ctx->ws_work[1], &ctx->ws_X, &ctx->ws_send, &ctx->ws_recv, &ctx->ws_thick[0], &ctx->ws_thick[1], &ctx->ws_gs, &ctx->ws_bd})
         if (b->p) cudaFree(b->p);
     if (ctx->host_stage.p) cudaFreeHost(ctx->host_stage.p);
     for (auto& e : ctx->ev)
@@ -1438,6 +1551,7 @@ int ttsvd_cu_tt_svd_distributed(ttsvd_cu_ctx* ctx, const double* const* slabs, i
         const int64_t nsig = std::min(m, global_rows);
         if (delta < 0.0) delta = eps / std::sqrt((double)(d - 1)) * sigma_norm_h(sig.data(), m);
         const int64_t rnew = choose_rank_h(sig.data(), m, m, nsig, delta, r_max, global_rows);
+        if ((rc = svd_vectors(ctx, rnew, d_sigma, d_V)) != TTSVD_OK) break;
         Vh.resize((size_t)m * rnew);
         if ((rc = d2h(ctx, Vh.data(), d_V, (size_t)m * rnew)) != TTSVD_OK) break;
         std::vector<double> core((size_t)(rnew * n_i * r));
