@@ -106,6 +106,14 @@ int ttsvd_cu_small_svd(ttsvd_cu_ctx* ctx, const double* R, int64_t m, double* si
  * completion for sigma <= n*eps*sigma_1. */
 int ttsvd_cu_jacobi_svd(ttsvd_cu_ctx* ctx, const double* A, int64_t n, int64_t m, int64_t lda, double* sigma,
                         double* V, double* U);
+/* The TT-SVD driver's SVD of a work matrix A (n x m, n >= m, device, ld lda;
+ * tt_svd.hpp:85-110 calls small_svd on R / W and keeps the leading r right
+ * singular vectors): sigma (m, non-increasing) and the leading r left
+ * singular vectors of A (V: n x r, ld n).  Bidiagonalisation + bisection +
+ * twisted factorisation when A fits a 16-CTA cluster (64 <= m), else block
+ * Jacobi.  *path_out (optional): 1 bidiagonal, 0 Jacobi. */
+int ttsvd_cu_driver_svd(ttsvd_cu_ctx* ctx, const double* A, int64_t n, int64_t m, int64_t lda, int64_t r,
+                        double* sigma, double* V, int32_t* path_out);
 /* small_svd.hpp:49 select_rank() on a device sigma; the rank is returned on the host. */
 int ttsvd_cu_select_rank(ttsvd_cu_ctx* ctx, const double* sigma, int64_t m, double delta, int64_t r_max,
                          int64_t* rank_host);

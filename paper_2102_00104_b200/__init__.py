@@ -9,7 +9,7 @@ mirror of the same interface.
 from .ttsvd import (AllocationError, BlockParams, Context, ConvergenceError, DegenerateDimension, DeviceError,
                     DimensionError, DimensionMismatch, DivergenceError, Error, IoError, LayoutError,
                     PartitionMismatch, ShapeError, SmallSVD, StepRecord, TensorTrain, ThickBoundsParams, TruncationSpec,
-                    TTCore, choose_combined_dims, combine_factors, context, derive_delta, fortran_empty, gen_uniform, jacobi_svd, padded_stride,
+                    TTCore, choose_combined_dims, combine_factors, context, derive_delta, driver_svd, fortran_empty, gen_uniform, jacobi_svd, padded_stride,
                     reduce_block, select_rank, small_svd, to_device_matrix, to_host, tsmm_reshape, tsqr,
                     tt_svd_distributed, tt_svd_thick_bounds, tt_svd_tsqr)
 

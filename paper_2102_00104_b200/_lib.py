@@ -48,6 +48,7 @@ _SIGS = {
     "ttsvd_cu_combine_factors": (C.c_int, [C.c_void_p, dptr, i64, i64, dptr]),
     "ttsvd_cu_small_svd": (C.c_int, [C.c_void_p, dptr, i64, dptr, dptr]),
     "ttsvd_cu_jacobi_svd": (C.c_int, [C.c_void_p, dptr, i64, i64, i64, dptr, dptr, dptr]),
+    "ttsvd_cu_driver_svd": (C.c_int, [C.c_void_p, dptr, i64, i64, i64, i64, dptr, dptr, C.POINTER(C.c_int32)]),
     "ttsvd_cu_select_rank": (C.c_int, [C.c_void_p, dptr, i64, C.c_double, i64, i64p]),
     "ttsvd_cu_select_rank_host": (i64, [C.c_void_p, i64, C.c_double, i64]),
     "ttsvd_cu_derive_delta": (C.c_int, [C.c_double, C.c_double, i64, C.POINTER(C.c_double)]),

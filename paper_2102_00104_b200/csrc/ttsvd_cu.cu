@@ -70,7 +70,7 @@ struct ttsvd_cu_ctx {
     // grow-only device workspaces
     DevBuf ws_R, ws_R2, ws_P, ws_Scr, ws_G, ws_Gp, ws_A, ws_V, ws_Vacc, ws_U, ws_sigma, ws_flags, ws_work[2], ws_X, ws_send, ws_recv, ws_thick[2], ws_gs, ws_bd;
     DevBuf host_stage;  // pinned
-    cudaEvent_t ev[7] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+    cudaEvent_t ev[9] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
     // svd_work's bidiagonal path leaves the vectors for svd_vectors (the
     // driver knows the rank only after the sigmas): A holds the reflectors
     bool bd_pending = false;
@@ -1076,7 +1076,9 @@ int run_chain(ttsvd_cu_ctx* ctx, WorkView cur, const std::vector<int64_t>& dims,
         const int64_t rnew = choose_rank_h(sig.data(), nsig, cur.cols, nsig, delta, r_max, cur.rows);
         st.nsig = nsig;
         st.rank = rnew;
+        tm.mark(7);
         TT_TRY(svd_vectors(ctx, rnew, d_sigma, d_V));
+        tm.mark(8);
         // core_from_vt (tt_svd.hpp:121-128) from the first rnew columns of V
         Vh.resize((size_t)m * rnew);
         TT_TRY(d2h(ctx, Vh.data(), d_V, (size_t)m * rnew));
@@ -1098,7 +1100,7 @@ int run_chain(ttsvd_cu_ctx* ctx, WorkView cur, const std::vector<int64_t>& dims,
         tm.mark(4);
         if (tm.on) {
             st.t_tsqr_ms = tm.ms(0, 1);
-            st.t_svd_ms = tm.ms(1, 2);
+            st.t_svd_ms = tm.ms(1, 2) + tm.ms(7, 8);  // sigmas + the leading vectors
             st.t_tsmm_ms = tm.ms(3, 4);
             if (tall && ctx->last_kernel) st.t_tsqr_sweep_ms = tm.ms(5, 6);
         }
@@ -1265,6 +1267,22 @@ int ttsvd_cu_jacobi_svd(ttsvd_cu_ctx* ctx, const double* A, int64_t n, int64_t m
         Uout = as<double>(ctx->ws_V);
     }
     TT_TRY(finalize_device(ctx, W, (int)n, (int)m, Vacc, sigma, Uout, V));
+    TT_CUDA(cudaStreamSynchronize(ctx->stream));
+    return TTSVD_OK;
+}
+
+int ttsvd_cu_driver_svd(ttsvd_cu_ctx* ctx, const double* A, int64_t n, int64_t m, int64_t lda, int64_t r,
+                        double* sigma, double* V, int32_t* path_out) {
+    TT_TRY(set_device(ctx));
+    if (!A || !sigma || !V || m < 1 || n < m || lda < n || r < 0 || r > m)
+        return fail(TTSVD_ERR_INVALID, "driver_svd: needs n >= m >= 1, lda >= n, 0 <= r <= m");
+    int sweeps = 0;
+    TT_TRY(ensure(ctx->ws_V, (size_t)n * m * 8));
+    double* Vw = as<double>(ctx->ws_V);
+    TT_TRY(svd_work(ctx, A, n, m, lda, false, false, sigma, Vw, &sweeps));
+    if (path_out) *path_out = ctx->bd_pending ? 1 : 0;
+    TT_TRY(svd_vectors(ctx, r, sigma, Vw));
+    if (r > 0) TT_CUDA(cudaMemcpyAsync(V, Vw, (size_t)n * r * 8, cudaMemcpyDeviceToDevice, ctx->stream));
     TT_CUDA(cudaStreamSynchronize(ctx->stream));
     return TTSVD_OK;
 }

@@ -299,6 +299,21 @@ def jacobi_svd(A) -> SmallSVD:
     return SmallSVD(n, m, U, sigma, V)
 
 
+def driver_svd(A, r: int):
+    """The TT-SVD driver's SVD of a work matrix (tt_svd.hpp:85-110): sigma
+    (non-increasing) and the leading r left singular vectors of A (n x m,
+    n >= m).  Returns (sigma, V, path) with path "bidiag" or "jacobi"."""
+    A = to_device_matrix(A)
+    p, n, m, ld = _mat(A)
+    ctx = context(A.device.index)
+    sigma = torch.empty(m, dtype=torch.float64, device=A.device)
+    V = fortran_empty(n, max(int(r), 1))
+    path = C.c_int32(-1)
+    _check(_lib.lib().ttsvd_cu_driver_svd(ctx.handle, p, n, m, ld, int(r), sigma.data_ptr(), V.data_ptr(),
+                                          C.byref(path)))
+    return sigma, V[:, :int(r)], ("bidiag" if path.value == 1 else "jacobi")
+
+
 def select_rank(sigma, delta: float, r_max: int) -> int:
     """small_svd.hpp:49"""
     s = sigma if isinstance(sigma, torch.Tensor) and sigma.is_cuda else torch.as_tensor(
