@@ -44,10 +44,16 @@ struct BdArgs {
     double* d;     // m
     double* e;     // m - 1
     double* tauL;  // m
+    double* xg;    // exchange (global, L2): u_k (2 x (n + 1), by step parity), partial z (16 x n),
+                   // row-norm partials + A[k][k+1] (2 x 2C, by step parity)
     long long* prof;  // optional (diagnostics): CTA 0 cycle sums per phase
 };
 
-inline size_t bd_smem_bytes(int n, int cpc) { return ((size_t)cpc * n + 4 * (size_t)n + (size_t)cpc + 8) * sizeof(double); }
+inline size_t bd_smem_bytes(int n, int cpc) { return ((size_t)cpc * n + 3 * (size_t)n + 3 * (size_t)cpc + 8) * sizeof(double); }
+
+// split cluster barrier (arrive.release / wait.acquire)
+__device__ __forceinline__ void bd_arrive() { asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory"); }
+__device__ __forceinline__ void bd_wait() { asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory"); }
 
 // sum over the CTA (every thread gets the same value; fixed order)
 __device__ __forceinline__ double bd_block_sum(double v, double* red) {
@@ -69,6 +75,11 @@ __device__ __forceinline__ double bd_warp_sum(double v) {
     return v;
 }
 
+constexpr int kBdCluster = 16;
+
+// CPC: compile-time columns per CTA (the row passes keep a row's CPC entries
+// in registers); a.cpc <= CPC
+template <int CPC>
 __global__ void __launch_bounds__(kBdThreads, 1) bd_kernel(BdArgs a) {
     cg::cluster_group cl = cg::this_cluster();
     extern __shared__ __align__(16) double sm[];
@@ -77,23 +88,26 @@ __global__ void __launch_bounds__(kBdThreads, 1) bd_kernel(BdArgs a) {
                                // barrier between a read and the next write), [2] row-norm partial, [3] A[k][k+1]
     __shared__ double rs[2];   // row reflector inputs, CTA-local copies
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int C = (int)cl.num_blocks(), rank = (int)cl.block_rank();
-    const int n = a.n, m = a.m, cpc = a.cpc;
+    constexpr int C = kBdCluster;
+    const int rank = (int)cl.block_rank();
+    const int n = a.n, m = a.m, cpc = CPC;
     double* As = sm;          // cpc columns, ld n
     double* ub = As + (size_t)cpc * n;
     double* zp = ub + n;      // partial z over my columns
-    double* zr = zp + n;      // reduced z, my row slice
-    double* zf = zr + n;      // full z
+    double* zf = zp + n;      // full z
     double* vl = zf + n;      // right reflector, my columns
+    double* wl = vl + cpc;    // left-reflector products w_j
+    double* rk = wl + cpc;    // row k after the left update
     const int c0 = rank * cpc;
-    const int sl = (n + C - 1) / C;
+    double* ug = a.xg;
+    double* zg = a.xg + 2 * (size_t)(n + 1);
     for (int e = tid; e < cpc * n; e += kBdThreads) {
         const int j = e / n, i = e - j * n, gj = c0 + j;
         As[e] = gj < m ? a.A[(int64_t)gj * n + i] : 0.0;
     }
     __syncthreads();
     cl.sync();
-    long long* pf = (a.prof && rank == 0 && tid == 0) ? a.prof : nullptr;
+    long long* pf = (a.prof && rank == C - 1 && tid == 0) ? a.prof : nullptr;  // the last CTA: active to the end
     long long tp = pf ? bj_clock() : 0;
 #define BD_MARK(i)                           \
     if (pf) {                                \
@@ -101,70 +115,100 @@ __global__ void __launch_bounds__(kBdThreads, 1) bd_kernel(BdArgs a) {
         pf[i] += tq - tp;                    \
         tp = tq;                             \
     }
-    for (int k = 0; k < m; ++k) {
-        const int o = k / cpc, lk = k - o * cpc;
-        // ---- left reflector of column k (owner) ----
-        if (rank == o) {
-            double* col = As + (size_t)lk * n;
-            double s = 0.0;
-            for (int i = k + 1 + tid; i < n; i += kBdThreads) s = fma(col[i], col[i], s);
-            s = bd_block_sum(s, red);
-            const double alpha = col[k];
-            double tau = 0.0, beta = alpha, scale = 0.0;
-            if (s != 0.0) {
-                const double nr = sqrt(fma(alpha, alpha, s));
-                beta = alpha >= 0.0 ? -nr : nr;
-                tau = (beta - alpha) / beta;
-                scale = 1.0 / (alpha - beta);
-            }
-            for (int i = k + 1 + tid; i < n; i += kBdThreads) col[i] *= scale;
-            __syncthreads();
-            if (tid == 0) {
-                col[k] = 1.0;
-                pub[k & 1] = tau;
-                a.d[k] = beta;
-                a.tauL[k] = tau;
-            }
+    // the owner of column k computes its left reflector at the end of step
+    // k-1 (after updating that one column), arrives at the cluster barrier and
+    // only then updates its other columns; step 0's reflector is computed here
+    auto left_reflector = [&](int k) {
+        double* col = As + (size_t)(k - c0) * n;
+        double s = 0.0;
+        for (int i = k + 1 + tid; i < n; i += kBdThreads) s = fma(col[i], col[i], s);
+        s = bd_block_sum(s, red);
+        const double alpha = col[k];
+        double tau = 0.0, beta = alpha, scale = 0.0;
+        if (s != 0.0) {
+            const double nr = sqrt(fma(alpha, alpha, s));
+            beta = alpha >= 0.0 ? -nr : nr;
+            tau = (beta - alpha) / beta;
+            scale = 1.0 / (alpha - beta);
         }
-        cl.sync();
+        double* ug_k = ug + (size_t)(k & 1) * (n + 1);
+        for (int i = k + 1 + tid; i < n; i += kBdThreads) {
+            const double u = col[i] * scale;
+            col[i] = u;
+            __stcg(ug_k + i, u);
+        }
+        if (tid == 0) {
+            col[k] = 1.0;
+            __stcg(ug_k + k, 1.0);
+            __stcg(ug_k + n, tau);
+            a.d[k] = beta;
+            a.tauL[k] = tau;
+        }
+        __syncthreads();
+    };
+    if (rank == 0) left_reflector(0);
+    bd_arrive();
+    for (int k = 0; k < m; ++k) {
+        const int lj0 = max(0, k + 1 - c0);  // first local column right of k
+        const int lj1 = min(cpc, m - c0);     // past the last real column
+        bd_wait();  // B1: u_k published
         BD_MARK(0)
         {
-            const double* ucol = cl.map_shared_rank(As, o) + (size_t)lk * n;
-            for (int i = k + tid; i < n; i += kBdThreads) ub[i] = ucol[i];
-            if (tid == 0) rs[0] = *cl.map_shared_rank(&pub[k & 1], o);
+            // u_k through L2 (16 readers of one SM's shared memory would
+            // serialise on its DSMEM port)
+            const double* ug_k = ug + (size_t)(k & 1) * (n + 1);
+            for (int i = k + tid; i < n; i += kBdThreads) ub[i] = __ldcg(ug_k + i);
+            if (tid == 0) rs[0] = __ldcg(ug_k + n);
         }
         __syncthreads();
         BD_MARK(1)
         const double tauL = rs[0];
-        if (tauL != 0.0) {
-            for (int lj = warp; lj < cpc; lj += kBdThreads / 32) {
-                const int gj = c0 + lj;
-                if (gj <= k || gj >= m) continue;
-                double* col = As + (size_t)lj * n;
-                double dot = 0.0;
-                for (int i = k + lane; i < n; i += 32) dot = fma(ub[i], col[i], dot);
-                const double w = tauL * bd_warp_sum(dot);
-                for (int i = k + lane; i < n; i += 32) col[i] = fma(-w, ub[i], col[i]);
+        // ---- pass 1: w_j = tau_L u^T a_j (warp per column); row k after the
+        // left update: a_kj - w_j (u_k = 1) ----
+        for (int la = lj0 + warp; la < lj1; la += 2 * (kBdThreads / 32)) {
+            const int lb = la + kBdThreads / 32;  // second column of this warp (if any)
+            const bool hb = lb < lj1;
+            const double* ca = As + (size_t)la * n;
+            const double* cb = As + (size_t)(hb ? lb : la) * n;
+            double da0 = 0.0, da1 = 0.0, db0 = 0.0, db1 = 0.0;
+            int i = k + lane;
+            for (; i + 32 < n; i += 64) {
+                const double u0 = ub[i], u1 = ub[i + 32];
+                da0 = fma(u0, ca[i], da0);
+                da1 = fma(u1, ca[i + 32], da1);
+                db0 = fma(u0, cb[i], db0);
+                db1 = fma(u1, cb[i + 32], db1);
+            }
+            if (i < n) {
+                da0 = fma(ub[i], ca[i], da0);
+                db0 = fma(ub[i], cb[i], db0);
+            }
+            const double wa = tauL * bd_warp_sum(da0 + da1);
+            const double wb = tauL * bd_warp_sum(db0 + db1);
+            if (lane == 0) {
+                wl[la] = wa;
+                rk[la] = ca[k] - wa;
+                if (hb) {
+                    wl[lb] = wb;
+                    rk[lb] = cb[k] - wb;
+                }
             }
         }
         __syncthreads();
         BD_MARK(2)
         if (k + 2 < m) {
             // ---- right reflector of row k (columns k+1 ..) ----
-            double s = 0.0;
-            if (tid < cpc) {
-                const int gj = c0 + tid;
-                if (gj >= k + 2 && gj < m) {
-                    const double v = As[(size_t)tid * n + k];
-                    s = v * v;
+            if (warp == 0) {
+                double s = 0.0;
+                for (int lj = max(lj0, k + 2 - c0) + lane; lj < lj1; lj += 32) s = fma(rk[lj], rk[lj], s);
+                s = bd_warp_sum(s);
+                if (lane == 0) {
+                    pub[2] = s;
+                    if ((k + 1) / cpc == rank) pub[3] = rk[k + 1 - c0];
                 }
             }
-            s = bd_block_sum(s, red);
-            if (tid == 0) {
-                pub[2] = s;
-                if ((k + 1) / cpc == rank) pub[3] = As[(size_t)(k + 1 - c0) * n + k];
-            }
-            cl.sync();
+            __syncthreads();
+            cl.sync();  // B2
             BD_MARK(3)
             if (warp == 0) {
                 double p = lane < C ? *cl.map_shared_rank(&pub[2], lane) : 0.0;
@@ -184,51 +228,325 @@ __global__ void __launch_bounds__(kBdThreads, 1) bd_kernel(BdArgs a) {
                 scaleR = 1.0 / (y0 - gamma);
             }
             if (rank == 0 && tid == 0) a.e[k] = gamma;
-            if (tid < cpc) {
-                const int gj = c0 + tid;
-                vl[tid] = (gj == k + 1) ? 1.0 : ((gj >= k + 2 && gj < m) ? As[(size_t)tid * n + k] * scaleR : 0.0);
+            for (int lj = lj0 + tid; lj < lj1; lj += kBdThreads) vl[lj] = (c0 + lj == k + 1) ? 1.0 : rk[lj] * scaleR;
+            __syncthreads();
+            // ---- pass 2 (thread per row): left update, z partial ----
+            for (int i = k + 1 + tid; i < n; i += kBdThreads) {
+                const double ui = ub[i];
+                double z = 0.0;
+                for (int lj = lj0; lj < lj1; ++lj) {
+                    double* pa = As + (size_t)lj * n + i;
+                    const double x = fma(-wl[lj], ui, *pa);
+                    *pa = x;
+                    z = fma(x, vl[lj], z);
+                }
+                zg[(size_t)rank * n + i] = z;
+            }
+            BD_MARK(4)
+            cl.sync();  // B3
+            BD_MARK(5)
+            // ---- z = tau_R sum of the partials (same order on every CTA),
+            // right update; the owner of column k+1 updates it first and
+            // publishes the next left reflector before the others ----
+            const int on = (k + 1) / cpc;
+            if (lj0 < lj1) {
+                for (int i = k + 1 + tid; i < n; i += kBdThreads) {
+                    double p[C];
+#pragma unroll
+                    for (int t = 0; t < C; ++t) p[t] = __ldcg(zg + (size_t)t * n + i);
+                    double z = 0.0;
+#pragma unroll
+                    for (int t = 0; t < C; ++t) z += p[t];
+                    zf[i] = tauR * z;
+                }
             }
             __syncthreads();
-            if (tauR != 0.0) {
-                for (int i = k + 1 + tid; i < n; i += kBdThreads) {
-                    double z = 0.0;
-                    for (int lj = 0; lj < cpc; ++lj) z = fma(As[(size_t)lj * n + i], vl[lj], z);
-                    zp[i] = z;
-                }
-                BD_MARK(4)
-                cl.sync();
-                BD_MARK(5)
-                {
-                    const int i0 = max(rank * sl, k + 1), i1 = min(n, (rank + 1) * sl);
-                    for (int i = i0 + tid; i < i1; i += kBdThreads) {
-                        double z = 0.0;
-                        for (int t = 0; t < C; ++t) z += cl.map_shared_rank(zp, t)[i];
-                        zr[i] = tauR * z;
-                    }
-                }
-                BD_MARK(6)
-                cl.sync();
-                BD_MARK(7)
-                for (int i = k + 1 + tid; i < n; i += kBdThreads) zf[i] = cl.map_shared_rank(zr, i / sl)[i];
+            BD_MARK(6)
+            if (rank == on) {
+                double* col = As + (size_t)(k + 1 - c0) * n;
+                for (int i = k + 1 + tid; i < n; i += kBdThreads) col[i] = fma(-zf[i], 1.0, col[i]);
                 __syncthreads();
-                BD_MARK(8)
+                left_reflector(k + 1);
+            }
+            bd_arrive();
+            {
+                const int skip = (rank == on) ? k + 1 - c0 : -1;  // the owner's column k+1 is done
                 for (int i = k + 1 + tid; i < n; i += kBdThreads) {
                     const double z = zf[i];
-                    for (int lj = 0; lj < cpc; ++lj) As[(size_t)lj * n + i] = fma(-z, vl[lj], As[(size_t)lj * n + i]);
+                    for (int lj = lj0; lj < lj1; ++lj)
+                        if (lj != skip) As[(size_t)lj * n + i] = fma(-z, vl[lj], As[(size_t)lj * n + i]);
                 }
             }
             __syncthreads();
-            BD_MARK(9)
-        } else if (k + 2 == m) {
-            if ((k + 1) / cpc == rank && tid == 0) a.e[k] = As[(size_t)(k + 1 - c0) * n + k];
+            BD_MARK(7)
+        } else {
+            // last two steps: left update only (no right reflector)
+            for (int i = k + 1 + tid; i < n; i += kBdThreads) {
+                const double ui = ub[i];
+                for (int lj = lj0; lj < lj1; ++lj) As[(size_t)lj * n + i] = fma(-wl[lj], ui, As[(size_t)lj * n + i]);
+            }
+            if (k + 2 == m && (k + 1) / cpc == rank && tid == 0) a.e[k] = rk[k + 1 - c0];
+            __syncthreads();
+            if (k + 1 < m && (k + 1) / cpc == rank) left_reflector(k + 1);
+            bd_arrive();
         }
     }
+    bd_wait();
 #undef BD_MARK
-    cl.sync();
     for (int e = tid; e < cpc * n; e += kBdThreads) {
         const int j = e / n, i = e - j * n, gj = c0 + j;
         if (gj < m) a.A[(int64_t)gj * n + i] = As[e];
     }
+}
+
+// Register-resident variant (n <= kBdThreads): thread i keeps row i of the
+// CTA's CPC columns in registers, so the rank-1 updates and z = A v never
+// touch shared memory; the column products w = u^T A are a transpose-reduce
+// of CPC values inside each warp (lane L ends with column L) plus a 16-way
+// sum over the warps.  Inactive columns (j <= k) carry w_j = v_j = 0 and
+// inactive rows u_i = z_i = 0, so every thread runs the same unrolled code.
+// The exchange (u_k, partial z) goes through L2 as in bd_kernel.
+// mbarrier + st.async: a point-to-point exchange inside the cluster (the
+// receiver's mbarrier counts the bytes that landed in its shared memory), in
+// place of a cluster barrier whose release has to drain the remote stores
+__device__ __forceinline__ unsigned bd_smem_addr(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void bd_mbar_init(unsigned bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void bd_mbar_expect(unsigned bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bd_mbar_wait(unsigned bar, unsigned parity) {
+    asm volatile(
+        "{\n .reg .pred p;\n BD_WAIT_%=:\n"
+        " mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra BD_WAIT_%=;\n}" ::"r"(bar),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ unsigned bd_mapa(unsigned addr, int rank) {
+    unsigned r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void bd_st_async(unsigned raddr, double v, unsigned rbar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(raddr),
+                 "l"(__double_as_longlong(v)), "r"(rbar)
+                 : "memory");
+}
+
+template <int CPC>
+__device__ __forceinline__ double bd_transpose_reduce(double (&p)[CPC], int lane) {
+#pragma unroll
+    for (int o = 16; o >= CPC; o >>= 1)
+#pragma unroll
+        for (int t = 0; t < CPC; ++t) p[t] += __shfl_xor_sync(0xffffffffu, p[t], o);
+#pragma unroll
+    for (int o = CPC / 2; o >= 1; o >>= 1) {
+        const bool up = (lane & o) != 0;
+#pragma unroll
+        for (int t = 0; t < o; ++t) {
+            const double send = up ? p[t] : p[t + o];
+            const double keep = up ? p[t + o] : p[t];
+            p[t] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+        }
+    }
+    return p[0];  // column lane % CPC
+}
+
+template <int CPC>
+__global__ void __launch_bounds__(kBdThreads, 1) bd_reg_kernel(BdArgs a) {
+    cg::cluster_group cl = cg::this_cluster();
+    constexpr int C = kBdCluster;
+    constexpr int W = kBdThreads / 32;
+    __shared__ double wred[W][CPC], sred[W];
+    __shared__ double wl[CPC], rowa[CPC], rowk[CPC];
+    __shared__ double pnorm[2][C + 1];  // row-norm partials of all CTAs + A[k][k+1], by step parity
+    __shared__ double rs[2];
+    __shared__ __align__(8) unsigned long long e1bar;  // E1 arrivals (C + 1 doubles per step)
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int rank = (int)cl.block_rank();
+    const int n = a.n, m = a.m;
+    const int c0 = rank * CPC;
+    const int i = tid;  // my row
+    double* colg = a.xg;                        // column k+1 after the left update (its owner), 2 x n by parity
+    double* zg = a.xg + 2 * (size_t)(n + 1);    // partial z, C x n
+    double x[CPC];
+#pragma unroll
+    for (int j = 0; j < CPC; ++j) x[j] = (i < n && c0 + j < m) ? a.A[(int64_t)(c0 + j) * n + i] : 0.0;
+    long long* pf = (a.prof && rank == C - 1 && tid == 0) ? a.prof : nullptr;
+    long long tp = pf ? bj_clock() : 0;
+#define BD_MARK(q)                           \
+    if (pf) {                                \
+        const long long tq = bj_clock();     \
+        pf[q] += tq - tp;                    \
+        tp = tq;                             \
+    }
+    const unsigned bar = bd_smem_addr(&e1bar);
+    if (tid == 0) {
+        bd_mbar_init(bar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    // Left reflector of column k from its entries ck (every CTA computes it
+    // from the same bits) fused with the next products w_j = tau u^T x_j:
+    // one reduction of (ck^2, ck x_ij) over the rows below k; u_k = 1 adds
+    // row k.  Returns u_i; the owner keeps u in its column.
+    double tauL = 0.0;
+    auto reflect = [&](int k, double ck) -> double {
+        const bool below = i > k && i < n;
+        double p[CPC];
+#pragma unroll
+        for (int j = 0; j < CPC; ++j) p[j] = below ? ck * x[j] : 0.0;
+        const double cs = bd_transpose_reduce<CPC>(p, lane);
+        const double ss = bd_warp_sum(below ? ck * ck : 0.0);
+        if (lane < CPC) wred[warp][lane] = cs;
+        if (lane == 0) sred[warp] = ss;
+        if (i == k) {
+            rs[0] = ck;
+#pragma unroll
+            for (int j = 0; j < CPC; ++j) rowa[j] = x[j];
+        }
+        __syncthreads();
+        double s = 0.0;
+#pragma unroll
+        for (int q = 0; q < W; ++q) s += sred[q];
+        const double alpha = rs[0];
+        double tau = 0.0, beta = alpha, scale = 0.0;
+        if (s != 0.0) {
+            const double x2 = fma(alpha, alpha, s), inv = fast_rsqrt(x2), nr = x2 * inv;
+            beta = alpha >= 0.0 ? -nr : nr;
+            tau = 1.0 + fabs(alpha) * inv;  // (beta - alpha) / beta
+            scale = fast_rcp(alpha - beta);
+        }
+        if (tid < CPC) {
+            double sj = 0.0;
+#pragma unroll
+            for (int q = 0; q < W; ++q) sj += wred[q][tid];
+            const int gj = c0 + tid;
+            wl[tid] = (gj > k && gj < m) ? tau * fma(scale, sj, rowa[tid]) : 0.0;
+        }
+        const double u = below ? ck * scale : (i == k ? 1.0 : 0.0);
+        if (k / CPC == rank) {
+#pragma unroll
+            for (int j = 0; j < CPC; ++j)
+                if (c0 + j == k && i >= k) x[j] = u;
+        }
+        if (rank == 0 && tid == 0) {
+            a.d[k] = beta;
+            a.tauL[k] = tau;
+        }
+        tauL = tau;
+        __syncthreads();  // wl visible; rs / rowa / wred free
+        return u;
+    };
+    // column 0 to everyone
+    if (rank == 0 && i < n) __stcg(colg + i, x[0]);
+    bd_arrive();
+    bd_wait();
+    double ui = reflect(0, i < n ? __ldcg(colg + i) : 0.0);
+    for (int k = 0; k < m; ++k) {
+        BD_MARK(0)
+#pragma unroll
+        for (int j = 0; j < CPC; ++j) x[j] = fma(-wl[j], ui, x[j]);
+        const int on = (k + 1) / CPC;  // owner of column k+1
+        double* colg_k = colg + (size_t)((k + 1) & 1) * n;
+        if (k + 2 < m) {
+            // ---- E1: row k's norm partials (+ A[k][k+1]) stored into every
+            // CTA's shared memory by st.async; each CTA waits on its mbarrier.
+            // Meanwhile every row forms T_i = sum_j x_ij rowk_j (the right
+            // reflector's product up to its scale) ----
+            double* pn = pnorm[k & 1];
+            if (tid == 0) bd_mbar_expect(bar, (C + 1) * 8);
+            if (i == k) {
+                double s = 0.0, y = 0.0;
+#pragma unroll
+                for (int j = 0; j < CPC; ++j) {
+                    const int gj = c0 + j;
+                    const bool act = gj >= k + 2 && gj < m;
+                    rowk[j] = act ? x[j] : 0.0;
+                    if (act) s = fma(x[j], x[j], s);
+                    if (gj == k + 1) y = x[j];
+                }
+                const unsigned ps = bd_smem_addr(pn + rank), py = bd_smem_addr(pn + C);
+#pragma unroll
+                for (int t = 0; t < C; ++t) {
+                    const unsigned rb = bd_mapa(bar, t);
+                    bd_st_async(bd_mapa(ps, t), s, rb);
+                    if (rank == on) bd_st_async(bd_mapa(py, t), y, rb);
+                }
+            }
+            __syncthreads();  // rowk
+            double T = 0.0, xk1 = 0.0;
+#pragma unroll
+            for (int j = 0; j < CPC; ++j) {
+                T = fma(x[j], rowk[j], T);
+                if (c0 + j == k + 1) xk1 = x[j];
+            }
+            BD_MARK(1)
+            bd_mbar_wait(bar, (unsigned)(k & 1));
+            BD_MARK(2)
+            double st = 0.0;
+#pragma unroll
+            for (int t = 0; t < C; ++t) st += pn[t];
+            const double y0 = pn[C];
+            double tauR = 0.0, gamma = y0, scaleR = 0.0;
+            if (st != 0.0) {
+                const double x2 = fma(y0, y0, st), inv = fast_rsqrt(x2), nr = x2 * inv;
+                gamma = y0 >= 0.0 ? -nr : nr;
+                tauR = 1.0 + fabs(y0) * inv;  // (gamma - y0) / gamma
+                scaleR = fast_rcp(y0 - gamma);
+            }
+            if (rank == 0 && tid == 0) a.e[k] = gamma;
+            // ---- E2: partial z (rows > k) and, at the owner, column k+1 ----
+            const double z = fma(scaleR, T, xk1);
+            if (i < n) {
+                zg[(size_t)rank * n + i] = (i > k) ? z : 0.0;
+                if (rank == on) __stcg(colg_k + i, xk1);
+            }
+            BD_MARK(3)
+            bd_arrive();  // B3
+            bd_wait();
+            BD_MARK(4)
+            double zt = 0.0, ck = 0.0;
+            if (i < n) {
+                double q[C];
+#pragma unroll
+                for (int t = 0; t < C; ++t) q[t] = __ldcg(zg + (size_t)t * n + i);
+                ck = __ldcg(colg_k + i);
+                if (i > k) {
+#pragma unroll
+                    for (int t = 0; t < C; ++t) zt += q[t];
+                    zt *= tauR;
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < CPC; ++j) {
+                const int gj = c0 + j;
+                const double v = (gj == k + 1) ? 1.0 : rowk[j] * scaleR;
+                x[j] = fma(-zt, v, x[j]);
+            }
+            BD_MARK(5)
+            ui = reflect(k + 1, ck - zt);
+            BD_MARK(6)
+        } else if (k + 1 < m) {
+            // k = m-2: no right reflector; e_k = A[k][k+1]; column k+1 to everyone
+            if (rank == on && i < n) {
+#pragma unroll
+                for (int j = 0; j < CPC; ++j)
+                    if (c0 + j == k + 1) {
+                        __stcg(colg_k + i, x[j]);
+                        if (i == k) a.e[k] = x[j];
+                    }
+            }
+            bd_arrive();
+            bd_wait();
+            ui = reflect(k + 1, i < n ? __ldcg(colg_k + i) : 0.0);
+        }
+    }
+#undef BD_MARK
+#pragma unroll
+    for (int j = 0; j < CPC; ++j)
+        if (i < n && c0 + j < m) a.A[(int64_t)(c0 + j) * n + i] = x[j];
 }
 
 // off-diagonal t (0..2m-2) of the Golub-Kahan tridiagonal: d0 e0 d1 e1 ... d_{m-1}
@@ -530,6 +848,67 @@ __global__ void __launch_bounds__(kTwWarps * 32) bd_twisted_kernel(BdVecArgs a) 
         const double z = t < kb ? dp[t] : (t == kb ? 1.0 : dm[t]);
         a.X[(size_t)v * m + k] = z * ix;
     }
+}
+
+// V = U_B [X; 0] for n <= 32 NPL: a warp applies the reflectors to 4
+// vectors at once (lane: rows lane + 32 q), the next reflector's entries are
+// loaded while the current one is applied
+constexpr int kBack4Warps = 4;
+
+template <int NPL>
+__global__ void __launch_bounds__(kBack4Warps * 32) bd_back4_kernel(const double* A, const double* tauL, int n, int m,
+                                                                    const double* X, int r, double* V) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int v0 = (blockIdx.x * kBack4Warps + warp) * 4;
+    if (v0 >= r) return;
+    double x[4][NPL];
+#pragma unroll
+    for (int v = 0; v < 4; ++v)
+#pragma unroll
+        for (int q = 0; q < NPL; ++q) {
+            const int row = lane + 32 * q;
+            x[v][q] = (v0 + v < r && row < m) ? X[(size_t)(v0 + v) * m + row] : 0.0;
+        }
+    double un[NPL];
+    auto load = [&](int k) {
+        const double* u = A + (size_t)k * n;
+#pragma unroll
+        for (int q = 0; q < NPL; ++q) {
+            const int row = lane + 32 * q;
+            un[q] = (row > k && row < n) ? __ldg(u + row) : (row == k ? 1.0 : 0.0);
+        }
+    };
+    load(m - 1);
+    for (int k = m - 1; k >= 0; --k) {
+        double u[NPL];
+#pragma unroll
+        for (int q = 0; q < NPL; ++q) u[q] = un[q];
+        if (k > 0) load(k - 1);
+        const double tau = tauL[k];
+        double d[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+        for (int q = 0; q < NPL; ++q)
+#pragma unroll
+            for (int v = 0; v < 4; ++v) d[v] = fma(u[q], x[v][q], d[v]);
+#pragma unroll
+        for (int o = 16; o >= 1; o >>= 1)
+#pragma unroll
+            for (int v = 0; v < 4; ++v) d[v] += __shfl_xor_sync(0xffffffffu, d[v], o);
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+            const double w = tau * d[v];
+#pragma unroll
+            for (int q = 0; q < NPL; ++q) x[v][q] = fma(-w, u[q], x[v][q]);
+        }
+    }
+#pragma unroll
+    for (int v = 0; v < 4; ++v)
+        if (v0 + v < r)
+#pragma unroll
+            for (int q = 0; q < NPL; ++q) {
+                const int row = lane + 32 * q;
+                if (row < n) V[(size_t)(v0 + v) * n + row] = x[v][q];
+            }
 }
 
 // V (n x r, ld n) = U_B [X; 0]: the left reflectors of bd_kernel applied in

@@ -747,24 +747,31 @@ int finalize_device(ttsvd_cu_ctx* ctx, const double* A, int n, int m, const doub
 
 // Bidiagonal path (bidiag.cuh) of svd_work: sigma now, the vectors later by
 // svd_vectors.  Returns -1 (nothing launched) when A does not fit the cluster.
-constexpr int kBdCluster = 16;
 constexpr int kBdMinM = 64;
 int bd_sigma(ttsvd_cu_ctx* ctx, double* A, int n, int m, double* sigma) {
-    const int cpc = (m + kBdCluster - 1) / kBdCluster;
-    const size_t smem = bd_smem_bytes(n, cpc);
-    static int static_smem = -1;
-    if (static_smem < 0) {
+    const int need = (m + kBdCluster - 1) / kBdCluster;
+    const int cpc = need <= 8 ? 8 : (need <= 16 ? 16 : 32);
+    if (need > 32 || n < m) return -1;
+    static const char* bsel = std::getenv("TTSVD_BD");  // diagnostics: "smem" forces the shared-memory kernel
+    const bool reg = n <= kBdThreads && !(bsel && std::string(bsel) == "smem");
+    void (*kern)(BdArgs) = reg ? (cpc == 8 ? bd_reg_kernel<8> : (cpc == 16 ? bd_reg_kernel<16> : bd_reg_kernel<32>))
+                               : (cpc == 8 ? bd_kernel<8> : (cpc == 16 ? bd_kernel<16> : bd_kernel<32>));
+    const size_t smem = reg ? 0 : bd_smem_bytes(n, cpc);
+    static int static_smem[6] = {-1, -1, -1, -1, -1, -1};
+    int& ss = static_smem[(cpc == 8 ? 0 : (cpc == 16 ? 1 : 2)) + (reg ? 3 : 0)];
+    if (ss < 0) {
         cudaFuncAttributes fa;
-        TT_CUDA(cudaFuncGetAttributes(&fa, bd_kernel));
-        static_smem = (int)fa.sharedSizeBytes;
-        TT_CUDA(cudaFuncSetAttribute(bd_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-        TT_CUDA(cudaFuncSetAttribute(bd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit - static_smem));
+        TT_CUDA(cudaFuncGetAttributes(&fa, kern));
+        ss = (int)fa.sharedSizeBytes;
+        TT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        TT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit - ss));
     }
-    if (n < m || smem > (size_t)(kSmemLimit - static_smem)) return -1;
-    TT_TRY(ensure(ctx->ws_bd, (size_t)3 * m * 8));
+    if (smem > (size_t)(kSmemLimit - ss)) return -1;
+    TT_TRY(ensure(ctx->ws_bd, ((size_t)3 * m + 2 * (size_t)(n + 1) + (size_t)kBdCluster * n + 32 * (kBdCluster + 1)) * 8));
     double* d = as<double>(ctx->ws_bd);
     double* e = d + m;
     double* tauL = e + m;
+    double* xg = tauL + m;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(kBdCluster);
     cfg.blockDim = dim3(kBdThreads);
@@ -783,16 +790,16 @@ int bd_sigma(ttsvd_cu_ctx* ctx, double* A, int n, int m, double* sigma) {
         TT_CUDA(cudaMalloc(&dprof, 16 * sizeof(long long)));
         TT_CUDA(cudaMemset(dprof, 0, 16 * sizeof(long long)));
     }
-    BdArgs ba{A, n, m, cpc, d, e, tauL, dprof};
-    TT_CUDA(cudaLaunchKernelEx(&cfg, bd_kernel, ba));
+    BdArgs ba{A, n, m, cpc, d, e, tauL, xg, dprof};
+    TT_CUDA(cudaLaunchKernelEx(&cfg, kern, ba));
     TT_TRY(check_launch(ctx, "bd_kernel"));
     if (prof) {
         long long h[16];
         TT_CUDA(cudaMemcpy(h, dprof, sizeof(h), cudaMemcpyDeviceToHost));
         cudaFree(dprof);
-        std::fprintf(stderr, "[bd prof] n=%d m=%d cycles per step: left+B1 %.0f ucopy %.0f lupdate %.0f rnorm+B2 %.0f refl+zpart %.0f B3 %.0f reduce %.0f B4 %.0f gather %.0f update %.0f\n",
-                     n, m, h[0] / (double)m, h[1] / (double)m, h[2] / (double)m, h[3] / (double)m, h[4] / (double)m,
-                     h[5] / (double)m, h[6] / (double)m, h[7] / (double)m, h[8] / (double)m, h[9] / (double)m);
+        std::fprintf(stderr, "[bd prof] n=%d m=%d cycles per step: update+E1 send+T %.0f E1 wait %.0f refl-R+zpart %.0f E2 %.0f zpull+update %.0f reflect+dots %.0f\n",
+                     n, m, (h[0] + h[1]) / (double)m, h[2] / (double)m, h[3] / (double)m, h[4] / (double)m,
+                     h[5] / (double)m, h[6] / (double)m);
     }
     const int wpb = kBisThreads / 32;
     bd_bisect_kernel<<<(m + wpb - 1) / wpb, kBisThreads, (size_t)(2 * m) * 8, ctx->stream>>>(d, e, m, sigma);
@@ -830,6 +837,14 @@ int svd_vectors(ttsvd_cu_ctx* ctx, int64_t r, const double* sigma, double* Vout)
     // clusters (rare): inverse iteration with modified Gram-Schmidt
     bd_vectors_kernel<<<(unsigned)((r + 63) / 64), 64, 0, ctx->stream>>>(va);
     TT_TRY(check_launch(ctx, "bd_vectors_kernel"));
+    if (n <= 512) {
+        const unsigned g = (unsigned)((r + 4 * kBack4Warps - 1) / (4 * kBack4Warps));
+        if (n <= 256)
+            bd_back4_kernel<8><<<g, kBack4Warps * 32, 0, ctx->stream>>>(ctx->bd_A, tauL, n, m, X, (int)r, Vout);
+        else
+            bd_back4_kernel<16><<<g, kBack4Warps * 32, 0, ctx->stream>>>(ctx->bd_A, tauL, n, m, X, (int)r, Vout);
+        return check_launch(ctx, "bd_back4_kernel");
+    }
     const size_t smem = (size_t)kBackWarps * n * 8;
     static bool attr = false;
     if (!attr) {
