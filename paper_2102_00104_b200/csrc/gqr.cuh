@@ -35,6 +35,7 @@ struct GqrArgs {
     double* part;    // reduction partials: 2 x G x 33 (reflectors), G x 32 x 32 (S), G x 32 x M (W)
     double* piv;     // 2 x 32: the pivot row of the current reflector
     double* Wfin;    // 32 x M: W' = T^T W of the current panel
+    double* Sfin;    // 1024: S = Y^T Y of the current panel
     long long* prof; // optional (diagnostics): CTA 0 cycle sums [stage, reflectors, writeback+S+T, W partial, W reduce, update]
 };
 
@@ -76,6 +77,24 @@ __device__ __forceinline__ double gqr_strided_sum(const double* base, int64_t qs
     }
     for (; q < G; q += step) a0 += __ldcg(base + (int64_t)q * qstride);
     return (a0 + a1) + (a2 + a3);
+}
+
+// the same fixed-order sum with CH loads in flight per chunk (one L2 round
+// trip per chunk instead of one per four values)
+template <int CH>
+__device__ __forceinline__ double gqr_sum_inflight(const double* base, int64_t qstride, int G, int first, int step) {
+    double s = 0.0;
+    for (int q0 = first; q0 < G; q0 += CH * step) {
+        double v[CH];
+#pragma unroll
+        for (int u = 0; u < CH; ++u) {
+            const int q = q0 + u * step;
+            v[u] = q < G ? __ldcg(base + (int64_t)q * qstride) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < CH; ++u) s += v[u];
+    }
+    return s;
 }
 
 __host__ __device__ inline int gqr_ldy(int rows) { return ((((rows + 3) & ~3) + 7) & ~7) + 4; }
@@ -167,7 +186,7 @@ __global__ void __launch_bounds__(kGqrThreads, 1) gqr_kernel(GqrArgs a) {
             {
                 const int k = tid & 31, sl = tid >> 5;
                 const double pv = (sl == 0) ? __ldcg(&a.piv[buf * 32 + k]) : 0.0;  // in flight with the sums
-                red[8 * 33 + sl * 33 + k] = gqr_strided_sum(part + (int64_t)buf * G * 33 + k, 33, G, sl, kGqrThreads / 32);
+                red[8 * 33 + sl * 33 + k] = gqr_sum_inflight<20>(part + (int64_t)buf * G * 33 + k, 33, G, sl, kGqrThreads / 32);
                 if (sl == 0) red[33 + k] = pv;
             }
             __syncthreads();
@@ -255,8 +274,33 @@ __global__ void __launch_bounds__(kGqrThreads, 1) gqr_kernel(GqrArgs a) {
         }
         __threadfence();
         grid.sync();
-        for (int e = tid; e < 1024; e += kGqrThreads) {
-            Sm[(e >> 5) * 33 + (e & 31)] = gqr_strided_sum(part + (int64_t)2 * G * 33 + e, 1024, G, 0, 1);
+        // S = sum of the G partials, distributed: CTA c reduces entries
+        // [c E, (c+1) E) (warp per entry, lanes over the CTAs, fixed butterfly
+        // order), one grid barrier, then every CTA reads the 1024 totals
+        {
+            const int E = (1024 + G - 1) / G;
+            const double* ps = part + (int64_t)2 * G * 33;
+            for (int el = warp; el < E; el += kGqrThreads / 32) {
+                const int e = c * E + el;
+                if (e < 1024) {
+                    double s = gqr_sum_inflight<8>(ps + e, 1024, G, lane, 32);
+#pragma unroll
+                    for (int o = 16; o >= 1; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+                    if (lane == 0) a.Sfin[e] = s;
+                }
+            }
+        }
+        __threadfence();
+        grid.sync();
+        {
+            double sv[1024 / kGqrThreads];
+#pragma unroll
+            for (int r = 0; r < 1024 / kGqrThreads; ++r) sv[r] = __ldcg(a.Sfin + tid + r * kGqrThreads);
+#pragma unroll
+            for (int r = 0; r < 1024 / kGqrThreads; ++r) {
+                const int e = tid + r * kGqrThreads;
+                Sm[(e >> 5) * 33 + (e & 31)] = sv[r];
+            }
         }
         __syncthreads();
         if (warp == 0) {
@@ -330,13 +374,22 @@ __global__ void __launch_bounds__(kGqrThreads, 1) gqr_kernel(GqrArgs a) {
             const int64_t ncols = M - t0;
             const int64_t chunk = (ncols + G - 1) / G;
             const int64_t ca = t0 + c * chunk, cb = (ca + chunk < M) ? ca + chunk : M;
-            for (int64_t col = ca + warp; col < cb; col += kGqrThreads / 32) {
-                // lane k: W(k, col) summed over CTAs in order
-                const double w = gqr_strided_sum(pw + (int64_t)lane * M + col, (int64_t)32 * M, G, 0, 1);
-                // W'(i, col) = sum_k T(k, i) W(k, col)
-                double wp = 0.0;
-                for (int k = 0; k < 32; ++k) wp = fma(Tm[k * 33 + lane], __shfl_sync(0xffffffffu, w, k), wp);
-                a.Wfin[(int64_t)lane * M + col] = wp;
+            // per column: thread (k = lane, slice = warp) sums CTAs q = warp,
+            // warp + 8, ... (loads in flight), then warp 0 adds the 8 slices
+            // in order and forms W'(:, col) = T^T W(:, col)
+            double* wsl = Wsc;  // 8 x 33
+            for (int64_t col = ca; col < cb; ++col) {
+                wsl[warp * 33 + lane] = gqr_sum_inflight<20>(pw + (int64_t)lane * M + col, (int64_t)32 * M, G, warp, kGqrThreads / 32);
+                __syncthreads();
+                if (warp == 0) {
+                    double w = 0.0;
+#pragma unroll
+                    for (int sl = 0; sl < kGqrThreads / 32; ++sl) w += wsl[sl * 33 + lane];
+                    double wp = 0.0;
+                    for (int k = 0; k < 32; ++k) wp = fma(Tm[k * 33 + lane], __shfl_sync(0xffffffffu, w, k), wp);
+                    a.Wfin[(int64_t)lane * M + col] = wp;
+                }
+                __syncthreads();
             }
         }
         __threadfence();

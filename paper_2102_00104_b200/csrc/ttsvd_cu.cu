@@ -293,7 +293,7 @@ int gqr_device(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t ld,
     if (per_sm < 1 || Gq > (int64_t)per_sm * ctx->num_sms) return -1;
     TT_TRY(ensure(ctx->ws_G, (size_t)n * M * 8));
     const size_t np = (size_t)2 * Gq * 33 + (size_t)Gq * 1024 + (size_t)Gq * 32 * M;
-    TT_TRY(ensure(ctx->ws_Gp, (np + 64 + (size_t)32 * M) * 8));
+    TT_TRY(ensure(ctx->ws_Gp, (np + 64 + (size_t)32 * M + 1024) * 8));
     double* Aw = as<double>(ctx->ws_G);
     if (X != Aw) {
         TT_CUDA(cudaMemcpy2DAsync(Aw, (size_t)n * 8, X, (size_t)ld * 8, (size_t)n * 8, m, cudaMemcpyDeviceToDevice,
@@ -307,7 +307,7 @@ int gqr_device(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t ld,
         TT_CUDA(cudaMalloc(&dprof, 8 * sizeof(long long)));
         TT_CUDA(cudaMemset(dprof, 0, 8 * sizeof(long long)));
     }
-    GqrArgs ga{Aw, n, n, m, M, pp, pp + np, pp + np + 64, dprof};
+    GqrArgs ga{Aw, n, n, m, M, pp, pp + np, pp + np + 64, pp + np + 64 + (size_t)32 * M, dprof};
     void* args[] = {&ga};
     TT_CUDA(cudaLaunchCooperativeKernel((const void*)gqr_kernel, dim3((unsigned)Gq), dim3(kGqrThreads), args, smem,
                                         ctx->stream));
