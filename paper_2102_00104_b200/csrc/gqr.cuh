@@ -204,11 +204,11 @@ __global__ void __launch_bounds__(kGqrThreads, 1) gqr_kernel(GqrArgs a) {
             const double sp = red[0];
             const double u0 = red[33 + jj];
             const double nrm2 = u0 * u0 + sp;
-            const double inv = rsqrt(nrm2);
+            const double inv = fast_rsqrt(nrm2);
             const double nr = nrm2 * inv;
             const double au = fabs(u0);
             const double sg = (u0 > 0.0) ? 1.0 : -1.0;
-            double alpha = -sg * nr, tj = 1.0 + au * inv, scale = sg * __drcp_rn(au + nr);
+            double alpha = -sg * nr, tj = 1.0 + au * inv, scale = sg * fast_rcp(au + nr);
             if (sp == 0.0 && u0 != 0.0) {
                 alpha = u0;
                 tj = 0.0;

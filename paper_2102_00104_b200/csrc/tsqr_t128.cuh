@@ -25,9 +25,11 @@
 
 namespace ttsvd_b200 {
 
-constexpr int kT2Rows = 128;
-constexpr int kT2Threads = 384;  // 4 panel warps + 8 update warps
+constexpr int kT2Rows = 128;     // rows per tile of the 128-row variant
+constexpr int kT2Threads = 384;  // ROWS / 32 panel warps + the rest update warps
 constexpr int kT2Pld = 132;  // smem ld of a panel buffer (128 rows + 4)
+// smem ld of a panel buffer of a ROWS-row tile
+__host__ __device__ constexpr int t2_pld(int rows) { return rows + 4; }
 
 struct T2Args {
     const double* X;
@@ -38,22 +40,30 @@ struct T2Args {
     long long* prof;  // optional per-CTA phase cycle counters (8 per CTA), diagnostics
 };
 
-inline size_t t2_smem_bytes() {
-    return ((size_t)2 * 32 * kT2Pld + 32 * kLaRld + 32 * kTld + 2 * 32 * kLaTld + 32 + 4 * 32 + 2 * 4 * 32) *
+inline size_t t2_smem_bytes(int rows = kT2Rows) {
+    const int pw = rows / 32;
+    return ((size_t)2 * 32 * t2_pld(rows) + 32 * kLaRld + 32 * kTld + 2 * 32 * kLaTld + 32 + pw * 32 + 2 * pw * 32) *
            sizeof(double);
 }
 
-__device__ __forceinline__ void t2_bar_panel() { asm volatile("bar.sync 2, 128;" ::: "memory"); }
+template <int PW>
+__device__ __forceinline__ void t2_bar_panel() {
+    asm volatile("bar.sync 2, %0;" ::"n"(PW * 32) : "memory");
+}
+// T build: panel warps 0..3 only
+__device__ __forceinline__ void t2_bar_t() { asm volatile("bar.sync 3, 128;" ::: "memory"); }
 
 // panel warps 0..3: factor the 128 x 32 panel in P (ld kT2Pld) against the
 // diagonal R block Rp; leaves V in P, the new block in Rp, tau, striu(S) in Sm.
+template <int PW>
 __device__ __forceinline__ void t2_panel(double* P, double* Rp, double* tau, double* pvall, double* dpart, double* Sm,
                                          int warp, int lane) {
+    constexpr int Pld = 32 * PW + 4;
     double* pv = pvall + 32 * warp;
     double x[32];
 #pragma unroll
     for (int i = 0; i < 32; i += 2) {
-        const double2 t = *reinterpret_cast<const double2*>(P + lane * kT2Pld + 32 * warp + i);
+        const double2 t = *reinterpret_cast<const double2*>(P + lane * Pld + 32 * warp + i);
         x[i] = t.x;
         x[i + 1] = t.y;
     }
@@ -90,27 +100,45 @@ __device__ __forceinline__ void t2_panel(double* P, double* Rp, double* tau, dou
             }
         }
         const double dk = ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
-        sts1_if(true, s_dp + 8 * (par * 128 + warp * 32 + lane), dk);
-        t2_bar_panel();
+        sts1_if(true, s_dp + 8 * (par * 32 * PW + warp * 32 + lane), dk);
+        t2_bar_panel<PW>();
         if (w0 && pend_j >= 0) {  // everyone is past reflector j-1: publish its R row
             sts1_if(pend_upd, s_rcol + 8 * pend_j, pend_r);
             sts1_if(lane == pend_j, s_rp + 8 * pend_j * (kLaRld + 1), pend_alpha);
             sts1_if(lane == pend_j, s_tau + 8 * pend_j, pend_tau);
         }
-        const double d = (lds1(s_dp + 8 * (par * 128 + lane)) + lds1(s_dp + 8 * (par * 128 + 32 + lane))) +
-                         (lds1(s_dp + 8 * (par * 128 + 64 + lane)) + lds1(s_dp + 8 * (par * 128 + 96 + lane)));
-        const double sp = (lds1(s_dp + 8 * (par * 128 + j)) + lds1(s_dp + 8 * (par * 128 + 32 + j))) +
-                          (lds1(s_dp + 8 * (par * 128 + 64 + j)) + lds1(s_dp + 8 * (par * 128 + 96 + j)));
+        double dv[PW], sv[PW];
+#pragma unroll
+        for (int w = 0; w < PW; ++w) {
+            dv[w] = lds1(s_dp + 8 * (par * 32 * PW + 32 * w + lane));
+            sv[w] = lds1(s_dp + 8 * (par * 32 * PW + 32 * w + j));
+        }
+        if constexpr ((PW & (PW - 1)) == 0) {
+#pragma unroll
+            for (int h = PW / 2; h >= 1; h >>= 1)
+#pragma unroll
+                for (int w = 0; w < h; ++w) {
+                    dv[w] = dv[w] + dv[w + h];
+                    sv[w] = sv[w] + sv[w + h];
+                }
+        } else {
+#pragma unroll
+            for (int w = 1; w < PW; ++w) {
+                dv[0] += dv[w];
+                sv[0] += sv[w];
+            }
+        }
+        const double d = dv[0], sp = sv[0];
         const double u0 = lds1(s_rp + 8 * j * (kLaRld + 1));
         const double rjc = lds1(s_rcol + 8 * j);
         const double nrm2 = u0 * u0 + sp;
-        const double inv = rsqrt(nrm2);
+        const double inv = fast_rsqrt(nrm2);
         const double nr = nrm2 * inv;
         const double au = fabs(u0);
         const double sg = (u0 > 0.0) ? 1.0 : -1.0;
         double alpha = -sg * nr;
         double tj = 1.0 + au * inv;
-        double scale = sg * __drcp_rn(au + nr);
+        double scale = sg * fast_rcp(au + nr);
         if (sp == 0.0 && u0 != 0.0) {  // H = I
             alpha = u0;
             tj = 0.0;
@@ -141,7 +169,7 @@ __device__ __forceinline__ void t2_panel(double* P, double* Rp, double* tau, dou
         }
         __syncwarp();
     }
-    t2_bar_panel();
+    t2_bar_panel<PW>();
     if (w0) {
         sts1_if(pend_upd, s_rcol + 8 * pend_j, pend_r);
         sts1_if(lane == pend_j, s_rp + 8 * pend_j * (kLaRld + 1), pend_alpha);
@@ -149,8 +177,8 @@ __device__ __forceinline__ void t2_panel(double* P, double* Rp, double* tau, dou
     }
 #pragma unroll
     for (int i = 0; i < 32; i += 2)
-        *reinterpret_cast<double2*>(P + lane * kT2Pld + 32 * warp + i) = make_double2(my_scale * x[i], my_scale * x[i + 1]);
-    t2_bar_panel();
+        *reinterpret_cast<double2*>(P + lane * Pld + 32 * warp + i) = make_double2(my_scale * x[i], my_scale * x[i + 1]);
+    t2_bar_panel<PW>();
 }
 
 // panel warps 0..3: T = (diag(1/tau) + striu(S))^{-1} (row-major, ld kLaTld)
@@ -180,7 +208,7 @@ __device__ __forceinline__ void t2_build_t(const double* Sm, const double* tau, 
                 for (int i = 0; i < 8; ++i) Tm[(b0 + i) * kLaTld + c] = 0.0;
         }
     }
-    t2_bar_panel();
+    t2_bar_t();
     // level 1: blocks (0,1) by warp 0, (2,3) by warp 1: T_ab = -T_aa (S_ab T_bb)
     if (warp < 2) {
         const int a0 = 16 * warp, b0 = a0 + 8;
@@ -203,7 +231,7 @@ __device__ __forceinline__ void t2_build_t(const double* Sm, const double* tau, 
             Tm[(a0 + i) * kLaTld + b0 + j] = -acc;
         }
     }
-    t2_bar_panel();
+    t2_bar_t();
     // level 2: T[0:16, 16:32] = -T[0:16, 0:16] (S[0:16, 16:32] T[16:32, 16:32])
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
@@ -213,7 +241,7 @@ __device__ __forceinline__ void t2_build_t(const double* Sm, const double* tau, 
         for (int l = 0; l < 16; ++l) acc = fma(Sm[i * kTld + 16 + l], Tm[(16 + l) * kLaTld + 16 + j], acc);
         X[i * 16 + j] = acc;
     }
-    t2_bar_panel();
+    t2_bar_t();
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
         const int e = 64 * warp + lane + 32 * h, i = e >> 4, j = e & 15;
@@ -222,14 +250,14 @@ __device__ __forceinline__ void t2_build_t(const double* Sm, const double* tau, 
         for (int l = 0; l < 16; ++l) acc = fma(Tm[i * kLaTld + l], X[l * 16 + j], acc);
         Tm[i * kLaTld + 16 + j] = -acc;
     }
-    t2_bar_panel();
+    t2_bar_t();
 }
 
 // one warp: apply panel p's block reflector (V: 128 x 32 in smem, ld kT2Pld;
 // T) to tile columns g..g+7 (source: input X or the scratch; destination:
 // scratch or a panel buffer) and to R(p, g..g+7).
 //   W^T = R(p, c)^T + B(:, c)^T V;  W'^T = W^T T;  R(p, c) -= W';  B(:, c) -= V W'.
-template <bool SRC_X, bool DST_SMEM>
+template <bool SRC_X, bool DST_SMEM, int ROWS>
 __device__ __forceinline__ void t2_group(const double* src, int64_t lds, int rows, int mcols, double* dst, int64_t ldd,
                                          const double* V, const double* Tm, double* Rrow, int c0, int g, int gd,
                                          int lane, uint64_t pol_x, uint64_t pol_r) {
@@ -245,7 +273,7 @@ __device__ __forceinline__ void t2_group(const double* src, int64_t lds, int row
     }
     const double* scol = src + (int64_t)(g + r) * lds;
 #pragma unroll
-    for (int kc = 0; kc < 32; kc += 8) {
+    for (int kc = 0; kc < ROWS / 4; kc += 8) {
         double av[8];
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
@@ -257,7 +285,7 @@ __device__ __forceinline__ void t2_group(const double* src, int64_t lds, int row
         for (int u = 0; u < 8; ++u)
 #pragma unroll
             for (int nt = 0; nt < 4; ++nt)
-                dmma884(acc[nt], av[u], V[(8 * nt + r) * kT2Pld + 4 * (kc + u) + q]);
+                dmma884(acc[nt], av[u], V[(8 * nt + r) * t2_pld(ROWS) + 4 * (kc + u) + q]);
     }
     double w2[4][2];
 #pragma unroll
@@ -286,7 +314,7 @@ __device__ __forceinline__ void t2_group(const double* src, int64_t lds, int row
     }
     const double* s0c = src + (int64_t)(g + 2 * q) * lds;
 #pragma unroll 2
-    for (int mc = 0; mc < 16; mc += 4) {
+    for (int mc = 0; mc < ROWS / 8; mc += 4) {
         double cb[4][2];
 #pragma unroll
         for (int u = 0; u < 4; ++u)
@@ -300,7 +328,7 @@ __device__ __forceinline__ void t2_group(const double* src, int64_t lds, int row
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk)
 #pragma unroll
-            for (int u = 0; u < 4; ++u) dmma884(cb[u], -V[(4 * kk + q) * kT2Pld + 8 * (mc + u) + r], bv[kk]);
+            for (int u = 0; u < 4; ++u) dmma884(cb[u], -V[(4 * kk + q) * t2_pld(ROWS) + 8 * (mc + u) + r], bv[kk]);
 #pragma unroll
         for (int u = 0; u < 4; ++u)
 #pragma unroll
@@ -312,17 +340,19 @@ __device__ __forceinline__ void t2_group(const double* src, int64_t lds, int row
     }
 }
 
+template <int ROWS>
 __global__ void __launch_bounds__(kT2Threads, 1) tsqr_t128_kernel(T2Args a) {
+    constexpr int PW = ROWS / 32, Pld = t2_pld(ROWS), NUW = kT2Threads / 32 - PW;
     extern __shared__ __align__(16) double sm[];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int M = a.M, m = a.m;
-    double* Pb = sm;                           // 2 panel buffers, 32 columns x 128 rows (ld kT2Pld)
-    double* Rp = Pb + 2 * 32 * kT2Pld;         // diagonal R block (ld kLaRld)
+    double* Pb = sm;                           // 2 panel buffers, 32 columns x 128 rows (ld Pld)
+    double* Rp = Pb + 2 * 32 * Pld;         // diagonal R block (ld kLaRld)
     double* Sm = Rp + 32 * kLaRld;             // striu(V^T V) (ld kTld)
     double* Tm0 = Sm + 32 * kTld;              // 2 x T (ld kLaTld)
     double* tau = Tm0 + 2 * 32 * kLaTld;       // 32
     double* pvall = tau + 32;                  // 4 x 32 pivot parts
-    double* dpart = pvall + 4 * 32;            // 2 x 4 x 32 partial dots
+    double* dpart = pvall + PW * 32;           // 2 x PW x 32 partial dots
 
     const int64_t job = blockIdx.x, G = gridDim.x;
     const int64_t base = a.n / G, rem = a.n % G;
@@ -330,12 +360,12 @@ __global__ void __launch_bounds__(kT2Threads, 1) tsqr_t128_kernel(T2Args a) {
     const int64_t row1 = row0 + base + (job < rem ? 1 : 0);
     const int64_t RS = blk_rsize(M);
     double* R = a.Rws + job * RS;
-    double* Scr = a.Scr + job * (int64_t)kT2Rows * M;
+    double* Scr = a.Scr + job * (int64_t)ROWS * M;
     const uint64_t pol_x = l2_policy_evict_first(), pol_r = l2_policy_evict_last();
     for (int64_t e = tid; e < RS; e += kT2Threads) st_hint(R + e, 0.0, pol_r);
     __syncthreads();
     const int npan = M / 32;
-    const bool panel_warp = warp < 4;
+    const bool panel_warp = warp < PW;
     long long t_prev = 0, t_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 #define T2_PROF(ph)                                   \
     if (a.prof && tid == 0) {                         \
@@ -344,57 +374,57 @@ __global__ void __launch_bounds__(kT2Threads, 1) tsqr_t128_kernel(T2Args a) {
         t_prev = t_now;                               \
     }
     T2_PROF(7);
-    const int uw = warp - 4;  // update warp index 0..11
-    for (int64_t r0 = row0; r0 < row1; r0 += kT2Rows) {
-        const int rows = (int)((row1 - r0) < kT2Rows ? (row1 - r0) : kT2Rows);
+    const int uw = warp - PW;  // update warp index
+    for (int64_t r0 = row0; r0 < row1; r0 += ROWS) {
+        const int rows = (int)((row1 - r0) < ROWS ? (row1 - r0) : ROWS);
         const double* Xt = a.X + r0;  // column c at Xt + c * ld
         // panel 0 of the tile straight from the input
         if (warp == 0) la_fetch_rdiag(Rp, R, lane);
-        for (int e = tid; e < 32 * kT2Rows; e += kT2Threads) {
-            const int c = e >> 7, i = e & 127;
-            Pb[c * kT2Pld + i] = (i < rows && c < m) ? ld_hint(Xt + (int64_t)c * a.ld + i, pol_x) : 0.0;
+        for (int e = tid; e < 32 * ROWS; e += kT2Threads) {
+            const int c = e / ROWS, i = e % ROWS;
+            Pb[c * Pld + i] = (i < rows && c < m) ? ld_hint(Xt + (int64_t)c * a.ld + i, pol_x) : 0.0;
         }
         if (warp == 0) cp_async_wait_all();
         __syncthreads();
         T2_PROF(0);
         if (panel_warp) {
-            t2_panel(Pb, Rp, tau, pvall, dpart, Sm, warp, lane);
+            t2_panel<PW>(Pb, Rp, tau, pvall, dpart, Sm, warp, lane);
             if (warp == 0) la_store_rdiag(Rp, R, lane, pol_r);
-            if (npan > 1) t2_build_t(Sm, tau, Tm0, dpart, warp, lane);
+            if (npan > 1 && warp < 4) t2_build_t(Sm, tau, Tm0, dpart, warp, lane);
         }
         __syncthreads();
         T2_PROF(0);
         for (int p = 0; p + 1 < npan; ++p) {
             const int c0 = 32 * p, nxt = c0 + 32;
-            const double* V = Pb + (p & 1) * 32 * kT2Pld;
-            double* Pn = Pb + ((p + 1) & 1) * 32 * kT2Pld;
+            const double* V = Pb + (p & 1) * 32 * Pld;
+            double* Pn = Pb + ((p + 1) & 1) * 32 * Pld;
             const double* Tp = Tm0 + (p & 1) * 32 * kLaTld;
             double* Rrow = R + blk_roff(p, M);
             if (warp == 0) la_fetch_rdiag(Rp, R + blk_roff(p + 1, M), lane);
             // phase A: panel p+1's columns, alone on the tensor pipes
             if (uw >= 0 && uw < 4) {
                 if (p == 0)
-                    t2_group<true, true>(Xt, a.ld, rows, m, Pn, kT2Pld, V, Tp, Rrow, c0, nxt + 8 * uw, 8 * uw, lane, pol_x,
+                    t2_group<true, true, ROWS>(Xt, a.ld, rows, m, Pn, Pld, V, Tp, Rrow, c0, nxt + 8 * uw, 8 * uw, lane, pol_x,
                                          pol_r);
                 else
-                    t2_group<false, true>(Scr, kT2Rows, rows, m, Pn, kT2Pld, V, Tp, Rrow, c0, nxt + 8 * uw, 8 * uw, lane,
+                    t2_group<false, true, ROWS>(Scr, ROWS, rows, m, Pn, Pld, V, Tp, Rrow, c0, nxt + 8 * uw, 8 * uw, lane,
                                           pol_x, pol_r);
             }
             if (warp == 0) cp_async_wait_all();
             __syncthreads();
             T2_PROF(1);
             if (panel_warp) {
-                t2_panel(Pn, Rp, tau, pvall, dpart, Sm, warp, lane);
+                t2_panel<PW>(Pn, Rp, tau, pvall, dpart, Sm, warp, lane);
                 T2_PROF(2);
                 if (warp == 0) la_store_rdiag(Rp, R + blk_roff(p + 1, M), lane, pol_r);
-                if (p + 2 < npan) t2_build_t(Sm, tau, Tm0 + ((p + 1) & 1) * 32 * kLaTld, dpart, warp, lane);
+                if (p + 2 < npan && warp < 4) t2_build_t(Sm, tau, Tm0 + ((p + 1) & 1) * 32 * kLaTld, dpart, warp, lane);
                 T2_PROF(3);
             } else {
-                for (int g = nxt + 32 + 8 * uw; g < M; g += 8 * (kT2Threads / 32 - 4)) {
+                for (int g = nxt + 32 + 8 * uw; g < M; g += 8 * NUW) {
                     if (p == 0)
-                        t2_group<true, false>(Xt, a.ld, rows, m, Scr, kT2Rows, V, Tp, Rrow, c0, g, g, lane, pol_x, pol_r);
+                        t2_group<true, false, ROWS>(Xt, a.ld, rows, m, Scr, ROWS, V, Tp, Rrow, c0, g, g, lane, pol_x, pol_r);
                     else
-                        t2_group<false, false>(Scr, kT2Rows, rows, m, Scr, kT2Rows, V, Tp, Rrow, c0, g, g, lane, pol_x,
+                        t2_group<false, false, ROWS>(Scr, ROWS, rows, m, Scr, ROWS, V, Tp, Rrow, c0, g, g, lane, pol_x,
                                                pol_r);
                 }
             }

@@ -499,15 +499,27 @@ int tsqr_device(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t ld
         static const char* tsel = std::getenv("TTSVD_TSQR");  // diagnostics: "t128", "la"
         const bool force_t128 = tsel && std::string(tsel) == "t128";
         const bool want_t128 = tsel ? force_t128 : true;
+        // 192-row tiles (6 panel + 6 update warps) when every CTA gets >= 4
+        // of them: the reflector chain per row is 2/3 of the 128-row tile's
+        // (config 2 step 2: 27.1 -> 24.3 M cycles per CTA; 256-row tiles with
+        // 4 update warps leave the trailing update on the critical path,
+        // 25.6 M).  TTSVD_T2ROWS=128|192|256 selects one for A/B timing.
+        static const char* t2sel = std::getenv("TTSVD_T2ROWS");
+        const int t2want = t2sel ? std::atoi(t2sel) : 192;
+        const int t2rows = (t2want == 192 || t2want == 256) && n >= (int64_t)ctx->num_sms * 4 * t2want ? t2want : 128;
         if (!R_init && want_t128 && (n >= (int64_t)ctx->num_sms * 4 * kT2Rows || (force_t128 && n >= 4 * kT2Rows))) {
             const int64_t Gt = ctx->num_sms;
             TT_TRY(ensure(ctx->ws_R, (size_t)Gt * RS * 8));
-            TT_TRY(ensure(ctx->ws_Scr, (size_t)Gt * kT2Rows * M * 8));
+            TT_TRY(ensure(ctx->ws_Scr, (size_t)Gt * t2rows * M * 8));
             double* parts = as<double>(ctx->ws_R);
             static bool tattr = false;
             if (!tattr) {
-                TT_CUDA(cudaFuncSetAttribute(tsqr_t128_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)t2_smem_bytes()));
+                TT_CUDA(cudaFuncSetAttribute(tsqr_t128_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)t2_smem_bytes(128)));
+                TT_CUDA(cudaFuncSetAttribute(tsqr_t128_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)t2_smem_bytes(256)));
+                TT_CUDA(cudaFuncSetAttribute(tsqr_t128_kernel<192>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)t2_smem_bytes(192)));
                 tattr = true;
             }
             static const bool tprof = std::getenv("TTSVD_PROF_BLK") != nullptr;
@@ -515,7 +527,12 @@ int tsqr_device(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t ld
             if (tprof) TT_CUDA(cudaMalloc(&dprof, (size_t)Gt * 8 * sizeof(long long)));
             T2Args ta{X, n, ld, parts, as<double>(ctx->ws_Scr), m, M, dprof};
             kmark(ctx, 0, TTSVD_K_T128);
-            tsqr_t128_kernel<<<(unsigned)Gt, kT2Threads, t2_smem_bytes(), ctx->stream>>>(ta);
+            if (t2rows == 256)
+                tsqr_t128_kernel<256><<<(unsigned)Gt, kT2Threads, t2_smem_bytes(256), ctx->stream>>>(ta);
+            else if (t2rows == 192)
+                tsqr_t128_kernel<192><<<(unsigned)Gt, kT2Threads, t2_smem_bytes(192), ctx->stream>>>(ta);
+            else
+                tsqr_t128_kernel<128><<<(unsigned)Gt, kT2Threads, t2_smem_bytes(128), ctx->stream>>>(ta);
             TT_TRY(check_launch(ctx, "tsqr_t128_kernel"));
             kmark(ctx, 1, TTSVD_K_T128);
             if (tprof) {
@@ -525,9 +542,9 @@ int tsqr_device(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t ld
                 double ph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
                 for (int64_t g = 0; g < Gt; ++g)
                     for (int q = 0; q < 8; ++q) ph[q] += (double)hp[g * 8 + q] / Gt;
-                const double tiles = (double)n / Gt / kT2Rows;
-                std::fprintf(stderr, "[t128 prof] n=%lld m=%d tiles/CTA=%.1f per tile kcyc: load+panel0 %.1f, phaseA %.1f, panel %.1f, T+store %.1f, trailing wait %.1f\n",
-                             (long long)n, m, tiles, ph[0] / tiles / 1e3, ph[1] / tiles / 1e3, ph[2] / tiles / 1e3,
+                const double tiles = (double)n / Gt / t2rows;
+                std::fprintf(stderr, "[t128 prof] n=%lld m=%d rows/tile=%d tiles/CTA=%.1f per tile kcyc: load+panel0 %.1f, phaseA %.1f, panel %.1f, T+store %.1f, trailing wait %.1f\n",
+                             (long long)n, m, t2rows, tiles, ph[0] / tiles / 1e3, ph[1] / tiles / 1e3, ph[2] / tiles / 1e3,
                              ph[3] / tiles / 1e3, ph[4] / tiles / 1e3);
             }
             static const bool prof = std::getenv("TTSVD_PROF_BLK") != nullptr;
