@@ -18,13 +18,23 @@ from .ttsvd import fortran_empty, gen_uniform, padded_stride
 
 def tt_contract_flat(cores: list[torch.Tensor]) -> torch.Tensor:
     """Flat Fortran-order contraction of TT cores (each (r_l, n, r_r), float64,
-    on the device) — tensor_train.hpp:80-110 done with device GEMMs."""
-    M = cores[0][0].t().contiguous()  # (r1, n1): M[a, L]
+    on the device) — tensor_train.hpp:80-110 done with device GEMMs.  The
+    running factor is kept row-major as (N, r): rows x*N .. x*N + N - 1 of the
+    next factor are M @ G[:, x, :], so every GEMM has leading dimension r and
+    row chunks below 2^31 (cuBLAS int32 dimensions; config 4 has N = 2^32)."""
+    M = cores[0][0].contiguous()  # (n1, r1): M[L, a]
+    chunk = 1 << 30
     for c in cores[1:]:
         rl, n, rr = c.shape
-        Gp = c.permute(2, 1, 0).reshape(rr * n, rl)  # row b*n + x
-        T = Gp @ M  # (rr*n, N): row (b, x), col L
-        M = T.reshape(rr, n * M.shape[1])  # col x*N + L  == Fortran index of (L, x)
+        N = M.shape[0]
+        out = torch.empty((n * N, rr), dtype=M.dtype, device=M.device)
+        for x in range(n):
+            Gx = c[:, x, :].contiguous()  # rl x rr
+            for c0 in range(0, N, chunk):
+                c1 = min(N, c0 + chunk)
+                torch.matmul(M[c0:c1], Gx, out=out[x * N + c0:x * N + c1])
+        del M
+        M = out
     return M.reshape(-1)
 
 
@@ -41,17 +51,28 @@ def config1(seed: int = 1):
     return gen_uniform(seed, dims), dims, 16, 0.0
 
 
-def exact_tt(dims, ranks, seed: int, noise_rel: float, noise_seed: int, device: int = 0):
+def gaussian_cores(dims, ranks, seed: int, device: int = 0) -> list[torch.Tensor]:
+    """N(0,1) TT cores r_{j-1} x n_j x r_j from one seeded host stream (SURVEY
+    §8 d: Gaussian cores on the host, then copied to the device)."""
     rng = np.random.default_rng(seed)
-    cores = [torch.from_numpy(rng.standard_normal((ranks[j], dims[j], ranks[j + 1]))).to(f"cuda:{device}")
-             for j in range(len(dims))]
-    flat = tt_contract_flat(cores)
-    del cores
+    return [torch.from_numpy(rng.standard_normal((ranks[j], dims[j], ranks[j + 1]))).to(f"cuda:{device}")
+            for j in range(len(dims))]
+
+
+def _add_noise(flat: torch.Tensor, sigma: float, noise_seed: int, chunk: int = 1 << 27) -> None:
+    """flat += sigma N(0,1), generated chunk-wise (no N-sized temporary)."""
+    g = torch.Generator(device=flat.device)
+    g.manual_seed(noise_seed)
+    for c0 in range(0, flat.numel(), chunk):
+        n = min(chunk, flat.numel() - c0)
+        flat[c0:c0 + n].add_(torch.randn(n, dtype=torch.float64, device=flat.device, generator=g), alpha=sigma)
+
+
+def exact_tt(dims, ranks, seed: int, noise_rel: float, noise_seed: int, device: int = 0):
+    flat = tt_contract_flat(gaussian_cores(dims, ranks, seed, device))
     if noise_rel > 0:
-        g = torch.Generator(device=flat.device)
-        g.manual_seed(noise_seed)
         sigma = noise_rel * float(torch.linalg.vector_norm(flat)) / np.sqrt(flat.numel())
-        flat.add_(torch.randn(flat.numel(), dtype=torch.float64, device=flat.device, generator=g), alpha=sigma)
+        _add_noise(flat, sigma, noise_seed)
     X = to_padded(flat, dims)
     del flat
     torch.cuda.empty_cache()
@@ -69,3 +90,29 @@ def config2(scale_modes: int = 7, device: int = 0):
 def config3_matrix(k: int, device: int = 0, total: int = 1 << 30):
     n = total // k
     return gen_uniform(3, [n, k]), n, k
+
+
+def config4(d: int = 32, device: int = 0):
+    """2^d entries as d modes of 2 (d = 32: 2^32, 32 GiB), exact TT with
+    r_j = min(64, 2^j, 2^(d-j)), N(0,1) cores (seed 4), plus N(0, s^2) noise
+    with s = 1e-10 ||X|| / sqrt(N) (seed 104); TT-SVD r_max = 64, eps = 0."""
+    dims = [2] * d
+    ranks = [min(64, 2 ** j, 2 ** (d - j)) for j in range(d + 1)]
+    return exact_tt(dims, ranks, 4, 1e-10, 104, device), dims, 64, 0.0
+
+
+def config5(d: int = 11, device: int = 0):
+    """8^d entries (d = 11: 2^33, 64 GiB): E uniform[-1,1] (seed 5) plus a TT
+    signal S with N(0,1) cores, r_j = min(50, 8^j, 8^(d-j)) (seed 105), scaled
+    so ||S|| = 100 ||E||; TT-SVD r_max = 50, eps = 1e-4."""
+    dims = [8] * d
+    ranks = [min(50, 8 ** j, 8 ** (d - j)) for j in range(d + 1)]
+    X = gen_uniform(5, dims)
+    rows = int(np.prod(dims)) // dims[-1]
+    S = tt_contract_flat(gaussian_cores(dims, ranks, 105, device)).view(dims[-1], rows).t()
+    e2 = float(sum(torch.sum(X[:rows, j] ** 2) for j in range(dims[-1])))
+    s2 = float(sum(torch.sum(S[:, j] ** 2) for j in range(dims[-1])))
+    X[:rows].add_(S, alpha=100.0 * np.sqrt(e2 / s2))
+    del S
+    torch.cuda.empty_cache()
+    return X, dims, 50, 1e-4
