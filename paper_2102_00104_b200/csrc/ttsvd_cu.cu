@@ -279,18 +279,35 @@ int merge_tree(ttsvd_cu_ctx* ctx, double* parts, int64_t count, int m, double* R
 int gqr_device(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t ld, double* R) {
     const int M = (m + 31) / 32 * 32;
     if (n < M || n > (int64_t)kGqrMaxRows * ctx->num_sms) return -1;
-    int64_t Gq = std::max<int64_t>(1, std::min<int64_t>(ctx->num_sms, n / 128));
+    // a cooperative grid of up to one CTA per SM.  TTSVD_GQR=cluster runs
+    // short steps (n <= 16 x 512) as one cluster of <= 16 CTAs with cluster
+    // barriers instead — measured slower on config 2 step 4 (3.77 vs 3.37 ms:
+    // 8.5k vs 9.1k cycles per reflector, but half the SMs for the blocked
+    // updates), kept for A/B timing
+    static const char* gsel = std::getenv("TTSVD_GQR");
+    const bool cl = n <= (int64_t)kGqrCluster * kGqrMaxRows && gsel && std::string(gsel) == "cluster";
+    int64_t Gq = std::max<int64_t>(1, std::min<int64_t>(cl ? kGqrCluster : ctx->num_sms, n / 128));
+    if (cl) {  // a power-of-two cluster
+        int64_t g = 1;
+        while (2 * g <= Gq) g *= 2;
+        Gq = g;
+        while ((n + Gq - 1) / Gq > kGqrMaxRows) Gq *= 2;
+    }
     while ((n + Gq - 1) / Gq > kGqrMaxRows) ++Gq;
     const int rows_max = (int)((n + Gq - 1) / Gq);
     const size_t smem = gqr_smem_bytes(rows_max);
     static bool gattr = false;
     if (!gattr) {
-        TT_CUDA(cudaFuncSetAttribute(gqr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit));
+        TT_CUDA(cudaFuncSetAttribute(gqr_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit));
+        TT_CUDA(cudaFuncSetAttribute(gqr_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit));
+        TT_CUDA(cudaFuncSetAttribute(gqr_kernel<true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
         gattr = true;
     }
-    int per_sm = 0;
-    TT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gqr_kernel, kGqrThreads, smem));
-    if (per_sm < 1 || Gq > (int64_t)per_sm * ctx->num_sms) return -1;
+    if (!cl) {
+        int per_sm = 0;
+        TT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gqr_kernel<false>, kGqrThreads, smem));
+        if (per_sm < 1 || Gq > (int64_t)per_sm * ctx->num_sms) return -1;
+    }
     TT_TRY(ensure(ctx->ws_G, (size_t)n * M * 8));
     const size_t np = (size_t)2 * Gq * 33 + (size_t)Gq * 1024 + (size_t)Gq * 32 * M;
     TT_TRY(ensure(ctx->ws_Gp, (np + 64 + (size_t)32 * M + 1024) * 8));
@@ -308,9 +325,25 @@ int gqr_device(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t ld,
         TT_CUDA(cudaMemset(dprof, 0, 8 * sizeof(long long)));
     }
     GqrArgs ga{Aw, n, n, m, M, pp, pp + np, pp + np + 64, pp + np + 64 + (size_t)32 * M, dprof};
-    void* args[] = {&ga};
-    TT_CUDA(cudaLaunchCooperativeKernel((const void*)gqr_kernel, dim3((unsigned)Gq), dim3(kGqrThreads), args, smem,
-                                        ctx->stream));
+    if (cl) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((unsigned)Gq);
+        cfg.blockDim = dim3(kGqrThreads);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = ctx->stream;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = (unsigned)Gq;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        TT_CUDA(cudaLaunchKernelEx(&cfg, gqr_kernel<true>, ga));
+    } else {
+        void* args[] = {&ga};
+        TT_CUDA(cudaLaunchCooperativeKernel((const void*)gqr_kernel<false>, dim3((unsigned)Gq), dim3(kGqrThreads), args,
+                                            smem, ctx->stream));
+    }
     TT_TRY(check_launch(ctx, "gqr_kernel"));
     if (prof) {
         long long h[8];
