@@ -335,6 +335,17 @@ __device__ __forceinline__ void bd_st_async(unsigned raddr, double v, unsigned r
                  : "memory");
 }
 
+// fixed-order pairwise sum of N values (N a power of two): log2(N) dependent
+// adds instead of N - 1
+template <int N>
+__device__ __forceinline__ double bd_tree_sum(double (&v)[N]) {
+#pragma unroll
+    for (int h = N / 2; h >= 1; h >>= 1)
+#pragma unroll
+        for (int t = 0; t < h; ++t) v[t] += v[t + h];
+    return v[0];
+}
+
 template <int CPC>
 __device__ __forceinline__ double bd_transpose_reduce(double (&p)[CPC], int lane) {
 #pragma unroll
@@ -407,9 +418,10 @@ __global__ void __launch_bounds__(kBdThreads, 1) bd_reg_kernel(BdArgs a) {
             for (int j = 0; j < CPC; ++j) rowa[j] = x[j];
         }
         __syncthreads();
-        double s = 0.0;
+        double sv[W];
 #pragma unroll
-        for (int q = 0; q < W; ++q) s += sred[q];
+        for (int q = 0; q < W; ++q) sv[q] = sred[q];
+        const double s = bd_tree_sum<W>(sv);
         const double alpha = rs[0];
         double tau = 0.0, beta = alpha, scale = 0.0;
         if (s != 0.0) {
@@ -419,9 +431,10 @@ __global__ void __launch_bounds__(kBdThreads, 1) bd_reg_kernel(BdArgs a) {
             scale = fast_rcp(alpha - beta);
         }
         if (tid < CPC) {
-            double sj = 0.0;
+            double wv[W];
 #pragma unroll
-            for (int q = 0; q < W; ++q) sj += wred[q][tid];
+            for (int q = 0; q < W; ++q) wv[q] = wred[q][tid];
+            const double sj = bd_tree_sum<W>(wv);
             const int gj = c0 + tid;
             wl[tid] = (gj > k && gj < m) ? tau * fma(scale, sj, rowa[tid]) : 0.0;
         }
@@ -457,37 +470,43 @@ __global__ void __launch_bounds__(kBdThreads, 1) bd_reg_kernel(BdArgs a) {
             // reflector's product up to its scale) ----
             double* pn = pnorm[k & 1];
             if (tid == 0) bd_mbar_expect(bar, (C + 1) * 8);
-            if (i == k) {
-                double s = 0.0, y = 0.0;
+            if (warp == (k >> 5)) {  // the warp holding row k
+                double s4[4] = {0.0, 0.0, 0.0, 0.0}, y = 0.0;
+                if (i == k) {
 #pragma unroll
-                for (int j = 0; j < CPC; ++j) {
-                    const int gj = c0 + j;
-                    const bool act = gj >= k + 2 && gj < m;
-                    rowk[j] = act ? x[j] : 0.0;
-                    if (act) s = fma(x[j], x[j], s);
-                    if (gj == k + 1) y = x[j];
+                    for (int j = 0; j < CPC; ++j) {
+                        const int gj = c0 + j;
+                        const bool act = gj >= k + 2 && gj < m;
+                        rowk[j] = act ? x[j] : 0.0;
+                        if (act) s4[j & 3] = fma(x[j], x[j], s4[j & 3]);
+                        if (gj == k + 1) y = x[j];
+                    }
                 }
-                const unsigned ps = bd_smem_addr(pn + rank), py = bd_smem_addr(pn + C);
-#pragma unroll
-                for (int t = 0; t < C; ++t) {
-                    const unsigned rb = bd_mapa(bar, t);
-                    bd_st_async(bd_mapa(ps, t), s, rb);
-                    if (rank == on) bd_st_async(bd_mapa(py, t), y, rb);
+                // lane t sends the row-norm partial (and A[k][k+1]) to CTA t:
+                // C sends in parallel instead of one thread's 2C in a row
+                const double s = __shfl_sync(0xffffffffu, bd_tree_sum<4>(s4), k & 31);
+                y = __shfl_sync(0xffffffffu, y, k & 31);
+                if (lane < C) {
+                    const unsigned rb = bd_mapa(bar, lane);
+                    bd_st_async(bd_mapa(bd_smem_addr(pn + rank), lane), s, rb);
+                    if (rank == on) bd_st_async(bd_mapa(bd_smem_addr(pn + C), lane), y, rb);
                 }
             }
             __syncthreads();  // rowk
-            double T = 0.0, xk1 = 0.0;
+            double T4[4] = {0.0, 0.0, 0.0, 0.0}, xk1 = 0.0;
 #pragma unroll
             for (int j = 0; j < CPC; ++j) {
-                T = fma(x[j], rowk[j], T);
+                T4[j & 3] = fma(x[j], rowk[j], T4[j & 3]);
                 if (c0 + j == k + 1) xk1 = x[j];
             }
+            const double T = bd_tree_sum<4>(T4);
             BD_MARK(1)
             bd_mbar_wait(bar, (unsigned)(k & 1));
             BD_MARK(2)
-            double st = 0.0;
+            double pv[C];
 #pragma unroll
-            for (int t = 0; t < C; ++t) st += pn[t];
+            for (int t = 0; t < C; ++t) pv[t] = pn[t];
+            const double st = bd_tree_sum<C>(pv);
             const double y0 = pn[C];
             double tauR = 0.0, gamma = y0, scaleR = 0.0;
             if (st != 0.0) {
@@ -513,11 +532,7 @@ __global__ void __launch_bounds__(kBdThreads, 1) bd_reg_kernel(BdArgs a) {
 #pragma unroll
                 for (int t = 0; t < C; ++t) q[t] = __ldcg(zg + (size_t)t * n + i);
                 ck = __ldcg(colg_k + i);
-                if (i > k) {
-#pragma unroll
-                    for (int t = 0; t < C; ++t) zt += q[t];
-                    zt *= tauR;
-                }
+                if (i > k) zt = bd_tree_sum<C>(q) * tauR;
             }
 #pragma unroll
             for (int j = 0; j < CPC; ++j) {
