@@ -22,6 +22,32 @@ int main(int argc, char** argv) {
     if (choose_combined_dims({4, 4, 4, 4, 4, 4, 4, 4, 4, 4}, ThickBoundsParams{}, 16) != std::make_pair<index_t, index_t>(3, 64))
         return 6;
     if (argc > 1 && std::strcmp(argv[1], "host") == 0) {
+        // wire formats: "host <dir>" writes a tensor and a train for the
+        // reference's loaders to read (tests/test_wire.py) and reads them back
+        if (argc > 2) {
+            const std::string dir = argv[2];
+            DenseTensor T({3, 5, 4});
+            for (index_t l = 0; l < T.total(); ++l) T.at_flat(l) = 0.25 * l - 3.0;
+            dump_tensor(T, dir + "/cpp_tensor.bin");
+            const DenseTensor U = load_tensor(dir + "/cpp_tensor.bin");
+            for (index_t l = 0; l < T.total(); ++l)
+                if (U.at_flat(l) != T.at_flat(l)) return 7;
+            TensorTrain tt;
+            const index_t ranks[] = {1, 2, 3, 1}, dims[] = {3, 5, 4};
+            for (int j = 0; j < 3; ++j) {
+                TTCore c(ranks[j], dims[j], ranks[j + 1]);
+                for (std::size_t e = 0; e < c.data.size(); ++e) c.data[e] = 0.5 * (double)e - j;
+                tt.cores.push_back(c);
+            }
+            save_tt(tt, dir + "/cpp_tt.bin");
+            const TensorTrain back = load_tt(dir + "/cpp_tt.bin");
+            if (back.ranks() != tt.ranks() || back.cores[2].data != tt.cores[2].data) return 8;
+            try {
+                load_tensor(dir + "/missing.bin");
+                return 9;
+            } catch (const IoError&) {
+            }
+        }
         std::printf("host entry points ok\n");
         return 0;
     }

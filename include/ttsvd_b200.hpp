@@ -21,6 +21,8 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdio>
+#include <memory>
 #include <utility>
 #include <limits>
 #include <stdexcept>
@@ -253,6 +255,92 @@ struct TensorTrain {
         return r;
     }
 };
+
+inline void validate(const TensorTrain& tt) {  // tensor_train.hpp:60-77
+    if (tt.cores.empty()) throw DegenerateDimension("TensorTrain: no cores");
+    if (tt.cores.front().r_left != 1 || tt.cores.back().r_right != 1)
+        throw DimensionMismatch("TensorTrain: boundary ranks must be 1");
+    for (std::size_t j = 0; j + 1 < tt.cores.size(); ++j)
+        if (tt.cores[j].r_right != tt.cores[j + 1].r_left) throw DimensionMismatch("TensorTrain: rank chain broken");
+}
+
+// ---- wire formats (storage.hpp:214-278, tensor_train.hpp:157-191) ---------
+// Little-endian 64-bit integers and IEEE doubles, byte-identical to the
+// reference's dump_tensor / load_tensor (header d, dims..., stride; then the
+// padded buffer) and save_tt / load_tt (header d, ranks r_0..r_d, dims; then
+// the core buffers), written and read in bulk.
+namespace wire {
+static_assert(__BYTE_ORDER__ == __ORDER_LITTLE_ENDIAN__, "the wire formats are little-endian");
+struct Closer {
+    void operator()(std::FILE* f) const {
+        if (f) std::fclose(f);
+    }
+};
+using File = std::unique_ptr<std::FILE, Closer>;
+inline void put(std::FILE* f, const void* p, std::size_t bytes) {
+    if (std::fwrite(p, 1, bytes, f) != bytes) throw IoError("dump: short write");
+}
+inline void get(std::FILE* f, void* p, std::size_t bytes) {
+    if (std::fread(p, 1, bytes, f) != bytes) throw IoError("load: short read");
+}
+inline void put_u64(std::FILE* f, std::uint64_t v) { put(f, &v, 8); }
+inline std::uint64_t get_u64(std::FILE* f) {
+    std::uint64_t v;
+    get(f, &v, 8);
+    return v;
+}
+}  // namespace wire
+
+inline void dump_tensor(const DenseTensor& t, const std::string& path) {
+    wire::File f(std::fopen(path.c_str(), "wb"));
+    if (!f) throw IoError("dump_tensor: cannot open " + path);
+    wire::put_u64(f.get(), static_cast<std::uint64_t>(t.dims().size()));
+    for (index_t n : t.dims()) wire::put_u64(f.get(), static_cast<std::uint64_t>(n));
+    wire::put_u64(f.get(), static_cast<std::uint64_t>(t.leading_stride()));
+    wire::put(f.get(), t.data(), static_cast<std::size_t>(t.buffer_size()) * 8);
+}
+
+inline DenseTensor load_tensor(const std::string& path) {
+    wire::File f(std::fopen(path.c_str(), "rb"));
+    if (!f) throw IoError("load_tensor: cannot open " + path);
+    const index_t d = static_cast<index_t>(wire::get_u64(f.get()));
+    if (d < 1 || d > 64) throw IoError("load_tensor: bad header");
+    std::vector<index_t> dims(static_cast<std::size_t>(d));
+    for (auto& n : dims) n = static_cast<index_t>(wire::get_u64(f.get()));
+    const index_t stride = static_cast<index_t>(wire::get_u64(f.get()));
+    DenseTensor t(dims);
+    if (stride != t.leading_stride()) throw IoError("load_tensor: stride mismatch");
+    wire::get(f.get(), t.data(), static_cast<std::size_t>(t.buffer_size()) * 8);
+    return t;
+}
+
+inline void save_tt(const TensorTrain& tt, const std::string& path) {
+    validate(tt);
+    wire::File f(std::fopen(path.c_str(), "wb"));
+    if (!f) throw IoError("save_tt: cannot open " + path);
+    wire::put_u64(f.get(), static_cast<std::uint64_t>(tt.d()));
+    for (index_t r : tt.ranks()) wire::put_u64(f.get(), static_cast<std::uint64_t>(r));
+    for (const auto& c : tt.cores) wire::put_u64(f.get(), static_cast<std::uint64_t>(c.n));
+    for (const auto& c : tt.cores) wire::put(f.get(), c.data.data(), c.data.size() * 8);
+}
+
+inline TensorTrain load_tt(const std::string& path) {
+    wire::File f(std::fopen(path.c_str(), "rb"));
+    if (!f) throw IoError("load_tt: cannot open " + path);
+    const index_t d = static_cast<index_t>(wire::get_u64(f.get()));
+    if (d < 1 || d > 64) throw IoError("load_tt: bad header");
+    std::vector<index_t> ranks(static_cast<std::size_t>(d + 1)), dims(static_cast<std::size_t>(d));
+    for (auto& r : ranks) r = static_cast<index_t>(wire::get_u64(f.get()));
+    for (auto& n : dims) n = static_cast<index_t>(wire::get_u64(f.get()));
+    TensorTrain tt;
+    for (index_t j = 0; j < d; ++j) {
+        TTCore c(ranks[static_cast<std::size_t>(j)], dims[static_cast<std::size_t>(j)], ranks[static_cast<std::size_t>(j + 1)]);
+        wire::get(f.get(), c.data.data(), c.data.size() * 8);
+        tt.cores.push_back(std::move(c));
+    }
+    validate(tt);
+    return tt;
+}
 
 struct ExecContext {  // tt_svd.hpp:39-52; threads / l2 budget have no device meaning
     int threads = 1;

@@ -399,3 +399,70 @@ def split_cores(flat: np.ndarray, dims, ranks) -> list[np.ndarray]:
         out.append(flat[off:off + sz].reshape((rl, int(n), rr), order="F").copy())
         off += sz
     return out
+
+
+# ---- wire formats through the reference's own writers/readers ---------------
+class RefWire:
+    """save_tt / load_tt / dump_tensor / load_tensor of the compiled reference
+    (storage.hpp:214-278, tensor_train.hpp:157-191), for cross-reading files
+    written by the package."""
+
+    def __init__(self):
+        path = LIBS["reference"]
+        if not os.path.exists(path):
+            build()
+        self.lib = C.CDLL(path)
+        L = self.lib
+        L.ref_save_tt.argtypes = [C.c_char_p, i64, i64ptr, i64ptr, dptr]
+        L.ref_load_tt.argtypes = [C.c_char_p, i64ptr, i64ptr, i64ptr, dptr, i64, i64ptr]
+        L.ref_dump_tensor.argtypes = [C.c_char_p, dptr, i64ptr, i64, i64]
+        L.ref_load_tensor.argtypes = [C.c_char_p, i64ptr, i64ptr, i64ptr, dptr, i64]
+
+    def save_tt(self, path: str, cores: list) -> None:
+        d = len(cores)
+        ranks = np.array([cores[0].shape[0]] + [c.shape[2] for c in cores], dtype=np.int64)
+        dims = np.array([c.shape[1] for c in cores], dtype=np.int64)
+        flat = np.concatenate([np.asarray(c).reshape(-1, order="F") for c in cores])
+        rc = self.lib.ref_save_tt(path.encode(), d, _pi(ranks), _pi(dims), _p(flat))
+        if rc:
+            raise OracleError(rc, "ref_save_tt")
+
+    def load_tt(self, path: str) -> list:
+        d = np.zeros(1, dtype=np.int64)
+        ranks = np.zeros(65, dtype=np.int64)
+        dims = np.zeros(64, dtype=np.int64)
+        need = np.zeros(1, dtype=np.int64)
+        buf = np.zeros(1)
+        rc = self.lib.ref_load_tt(path.encode(), _pi(d), _pi(ranks), _pi(dims), _p(buf), 0, _pi(need))
+        if rc not in (0, 11):
+            raise OracleError(rc, "ref_load_tt")
+        buf = np.zeros(int(need[0]))
+        rc = self.lib.ref_load_tt(path.encode(), _pi(d), _pi(ranks), _pi(dims), _p(buf), buf.size, _pi(need))
+        if rc:
+            raise OracleError(rc, "ref_load_tt")
+        cores, off = [], 0
+        for j in range(int(d[0])):
+            rl, n, rr = int(ranks[j]), int(dims[j]), int(ranks[j + 1])
+            cores.append(buf[off:off + rl * n * rr].reshape((rl, n, rr), order="F"))
+            off += rl * n * rr
+        return cores
+
+    def dump_tensor(self, path: str, X: np.ndarray, dims, ld: int) -> None:
+        dv = np.asarray(dims, dtype=np.int64)
+        Xf = np.asfortranarray(X)
+        rc = self.lib.ref_dump_tensor(path.encode(), _p(Xf), _pi(dv), dv.size, ld)
+        if rc:
+            raise OracleError(rc, "ref_dump_tensor")
+
+    def load_tensor(self, path: str):
+        """-> (padded buffer as a Fortran (ld x n_d) array, dims)"""
+        d = np.zeros(1, dtype=np.int64)
+        dims = np.zeros(64, dtype=np.int64)
+        ld = np.zeros(1, dtype=np.int64)
+        cap = os.path.getsize(path) // 8
+        buf = np.zeros(cap)
+        rc = self.lib.ref_load_tensor(path.encode(), _pi(d), _pi(dims), _pi(ld), _p(buf), cap)
+        if rc:
+            raise OracleError(rc, "ref_load_tensor")
+        dd = [int(x) for x in dims[:int(d[0])]]
+        return buf[:int(ld[0]) * dd[-1]].reshape((int(ld[0]), dd[-1]), order="F"), dd

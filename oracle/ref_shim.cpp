@@ -24,6 +24,7 @@ int code_of(const std::exception& e) {
     if (dynamic_cast<const AllocationError*>(&e)) return 5;
     if (dynamic_cast<const DegenerateDimension*>(&e)) return 6;
     if (dynamic_cast<const PartitionMismatch*>(&e)) return 7;
+    if (dynamic_cast<const IoError*>(&e)) return 9;
     if (dynamic_cast<const LayoutError*>(&e)) return 10;
     return 12;
 }
@@ -261,6 +262,58 @@ void ref_gaussian(int64_t rows, int64_t cols, uint64_t seed, double* out) {
 void ref_uniform(int64_t rows, int64_t cols, uint64_t seed, double* out) {
     oracles::Dense m = oracles::uniform(rows, cols, seed);
     std::memcpy(out, m.a.data(), rows * cols * 8);
+}
+
+// wire formats (storage.hpp:214-278, tensor_train.hpp:157-191): the
+// reference's own writers/readers, for cross-reading files with the package
+int ref_save_tt(const char* path, int64_t d, const int64_t* ranks, const int64_t* dims, const double* cores) {
+    try {
+        TensorTrain tt;
+        int64_t off = 0;
+        for (int64_t j = 0; j < d; ++j) {
+            TTCore c(ranks[j], dims[j], ranks[j + 1]);
+            std::memcpy(c.data.data(), cores + off, c.data.size() * 8);
+            off += static_cast<int64_t>(c.data.size());
+            tt.cores.push_back(std::move(c));
+        }
+        save_tt(tt, path);
+        return 0;
+    } catch (const std::exception& e) {
+        return code_of(e);
+    }
+}
+int ref_load_tt(const char* path, int64_t* d, int64_t* ranks, int64_t* dims, double* cores, int64_t cap,
+                int64_t* needed) {
+    try {
+        const TensorTrain tt = load_tt(path);
+        *d = tt.d();
+        for (int64_t j = 0; j < tt.d(); ++j) dims[j] = tt.cores[static_cast<std::size_t>(j)].n;
+        return export_tt(tt, ranks, cores, cap, needed);
+    } catch (const std::exception& e) {
+        return code_of(e);
+    }
+}
+int ref_dump_tensor(const char* path, const double* X, const int64_t* dims, int64_t d, int64_t ldx) {
+    try {
+        dump_tensor(tensor_from(X, dims, d, ldx), path);
+        return 0;
+    } catch (const std::exception& e) {
+        return code_of(e);
+    }
+}
+// buf: the padded buffer (stride x n_d); cap in doubles
+int ref_load_tensor(const char* path, int64_t* d, int64_t* dims, int64_t* ld, double* buf, int64_t cap) {
+    try {
+        const DenseTensor t = load_tensor(path);
+        *d = t.shape().d();
+        for (int64_t j = 0; j < *d; ++j) dims[j] = t.shape().dims()[static_cast<std::size_t>(j)];
+        *ld = t.leading_stride();
+        if (t.buffer_size() > cap) return 11;
+        std::memcpy(buf, t.data(), static_cast<std::size_t>(t.buffer_size()) * 8);
+        return 0;
+    } catch (const std::exception& e) {
+        return code_of(e);
+    }
 }
 
 } // extern "C"

@@ -73,3 +73,29 @@ def test_config5_reduced_vs_oracle(tt, orc):
     X, dims, r_max, eps = inputs.config5(7)
     T, e_gpu, e_ref = parity_vs_oracle(tt, orc, X, dims, r_max, eps)
     assert T.max_rank() == 50
+
+
+def test_wire_device_round_trip(tt, tmp_path):
+    """dump a device tensor, load it back onto the device, decompose, save the
+    train: the reference's loaders read both files (wire formats, §8 f-3)."""
+    import os
+    from oracle.oracle import LIBS, RefWire
+    from paper_2102_00104_b200 import wire
+    X = tt.gen_uniform(1, [4] * 8)
+    dims = [4] * 8
+    p = str(tmp_path / "x.bin")
+    wire.dump_tensor(X, dims, p)
+    Y, d2 = wire.load_tensor(p, device=0)
+    assert d2 == dims
+    T1 = tt.tt_svd_tsqr(X, dims, tt.TruncationSpec(r_max=8))
+    T2 = tt.tt_svd_tsqr(Y, dims, tt.TruncationSpec(r_max=8))
+    for a, b in zip(T1.cores, T2.cores):
+        assert np.array_equal(a.data, b.data)
+    q = str(tmp_path / "t.tt")
+    wire.save_tt(T2, q)
+    if os.path.exists(LIBS["reference"]):
+        rw = RefWire()
+        for a, b in zip(T2.cores, rw.load_tt(q)):
+            assert np.array_equal(a.data, b)
+        Xr, dr = rw.load_tensor(p)
+        assert dr == dims and np.array_equal(Xr, host_copy(X, dims))
