@@ -410,7 +410,9 @@ __global__ void __launch_bounds__(kT2Threads, 1) tsqr_t128_kernel(T2Args a) {
                     t2_group<false, true, ROWS>(Scr, ROWS, rows, m, Pn, Pld, V, Tp, Rrow, c0, nxt + 8 * uw, 8 * uw, lane,
                                           pol_x, pol_r);
             }
+            T2_PROF(5);
             if (warp == 0) cp_async_wait_all();
+            T2_PROF(6);
             __syncthreads();
             T2_PROF(1);
             if (panel_warp) {

@@ -576,8 +576,9 @@ int tsqr_device(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t ld
                 for (int64_t g = 0; g < Gt; ++g)
                     for (int q = 0; q < 8; ++q) ph[q] += (double)hp[g * 8 + q] / Gt;
                 const double tiles = (double)n / Gt / t2rows;
-                std::fprintf(stderr, "[t128 prof] n=%lld m=%d rows/tile=%d tiles/CTA=%.1f per tile kcyc: load+panel0 %.1f, phaseA %.1f, panel %.1f, T+store %.1f, trailing wait %.1f\n",
-                             (long long)n, m, t2rows, tiles, ph[0] / tiles / 1e3, ph[1] / tiles / 1e3, ph[2] / tiles / 1e3,
+                std::fprintf(stderr, "[t128 prof] n=%lld m=%d rows/tile=%d tiles/CTA=%.1f per tile kcyc: load+panel0 %.1f, phaseA %.1f (warp 0 work %.1f, rdiag wait %.1f, barrier %.1f), panel %.1f, T+store %.1f, trailing wait %.1f\n",
+                             (long long)n, m, t2rows, tiles, ph[0] / tiles / 1e3, (ph[1] + ph[5] + ph[6]) / tiles / 1e3,
+                             ph[5] / tiles / 1e3, ph[6] / tiles / 1e3, ph[1] / tiles / 1e3, ph[2] / tiles / 1e3,
                              ph[3] / tiles / 1e3, ph[4] / tiles / 1e3);
             }
             static const bool prof = std::getenv("TTSVD_PROF_BLK") != nullptr;
