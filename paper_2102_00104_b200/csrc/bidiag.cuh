@@ -926,6 +926,112 @@ __global__ void __launch_bounds__(kBack4Warps * 32) bd_back4_kernel(const double
             }
 }
 
+// bd_back4_kernel with the reflectors staged in shared memory: chunks of
+// kB4sChunk columns of A are copied by cp.async (double buffered, all threads)
+// while the previous chunk is applied, so a reflector costs its arithmetic
+// and reductions instead of an L2 round trip (the register prefetch of
+// bd_back4_kernel looks one reflector ahead, less than the L2 latency).
+constexpr int kB4sChunk = 16;
+constexpr int kB4sWarps = 8;  // warps per CTA
+constexpr int kB4sVpw = 2;    // vectors per warp
+
+__device__ __forceinline__ void bd_cp_async16(void* smem_dst, const void* gsrc) {
+    const unsigned sd = (unsigned)__cvta_generic_to_shared(smem_dst);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sd), "l"(gsrc) : "memory");
+}
+
+inline size_t bd_back4s_smem(int npl) { return (size_t)2 * kB4sChunk * 32 * npl * sizeof(double); }
+
+template <int NPL>
+__global__ void __launch_bounds__(kB4sWarps * 32) bd_back4s_kernel(const double* A, const double* tauL, int n, int m,
+                                                                     const double* X, int r, double* V) {
+    extern __shared__ __align__(16) double us[];  // 2 x kB4sChunk x (32 NPL): raw columns k of A
+    __shared__ double taus[2 * kB4sChunk];
+    constexpr int LD = 32 * NPL;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int v0 = (blockIdx.x * kB4sWarps + warp) * kB4sVpw;
+    const int nchunks = (m + kB4sChunk - 1) / kB4sChunk;
+    // chunk c: reflectors k = m-1-c*CH down to max(0, m-CH-c*CH)
+    auto stage = [&](int c) {
+        double* dst = us + (c & 1) * kB4sChunk * LD;
+        const int khi = m - 1 - c * kB4sChunk;
+        const int cnt = min(kB4sChunk, khi + 1);
+        if (tid < cnt) taus[(c & 1) * kB4sChunk + tid] = tauL[khi - tid];
+        // warp per column, lane per 16-byte pair (no index division)
+        for (int kk = warp; kk < cnt; kk += kB4sWarps) {
+            const double* src = A + (size_t)(khi - kk) * n;
+            double* d = dst + kk * LD;
+            if ((n & 1) == 0) {
+                for (int p2 = 2 * lane; p2 < n; p2 += 64) bd_cp_async16(d + p2, src + p2);
+            } else {  // odd n: columns are not 16-byte aligned
+                for (int i = lane; i < n; i += 32) d[i] = src[i];
+            }
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    double x[kB4sVpw][NPL];
+#pragma unroll
+    for (int v = 0; v < kB4sVpw; ++v)
+#pragma unroll
+        for (int q = 0; q < NPL; ++q) {
+            const int row = lane + 32 * q;
+            x[v][q] = (v0 + v < r && row < m) ? X[(size_t)(v0 + v) * m + row] : 0.0;
+        }
+    stage(0);
+    for (int c = 0; c < nchunks; ++c) {
+        if (c + 1 < nchunks) {
+            stage(c + 1);
+            asm volatile("cp.async.wait_group 1;" ::: "memory");
+        } else {
+            asm volatile("cp.async.wait_group 0;" ::: "memory");
+        }
+        __syncthreads();
+        const double* ub = us + (c & 1) * kB4sChunk * LD;
+        const int khi = m - 1 - c * kB4sChunk;
+        const int cnt = min(kB4sChunk, khi + 1);
+        for (int kk = 0; kk < cnt; ++kk) {
+            const int k = khi - kk;
+            double u[NPL];
+#pragma unroll
+            for (int q = 0; q < NPL; ++q) {
+                const int row = lane + 32 * q;
+                u[q] = (row > k && row < n) ? ub[kk * LD + row] : (row == k ? 1.0 : 0.0);
+            }
+            const double tau = taus[(c & 1) * kB4sChunk + kk];
+            double d[kB4sVpw][2];
+#pragma unroll
+            for (int v = 0; v < kB4sVpw; ++v) d[v][0] = d[v][1] = 0.0;
+#pragma unroll
+            for (int q = 0; q < NPL; ++q)
+#pragma unroll
+                for (int v = 0; v < kB4sVpw; ++v) d[v][q & 1] = fma(u[q], x[v][q], d[v][q & 1]);
+            double dd[kB4sVpw];
+#pragma unroll
+            for (int v = 0; v < kB4sVpw; ++v) dd[v] = d[v][0] + d[v][1];
+#pragma unroll
+            for (int o = 16; o >= 1; o >>= 1)
+#pragma unroll
+                for (int v = 0; v < kB4sVpw; ++v) dd[v] += __shfl_xor_sync(0xffffffffu, dd[v], o);
+#pragma unroll
+            for (int v = 0; v < kB4sVpw; ++v) {
+                const double w = tau * dd[v];
+#pragma unroll
+                for (int q = 0; q < NPL; ++q) x[v][q] = fma(-w, u[q], x[v][q]);
+            }
+        }
+        __syncthreads();  // the buffer is restaged two chunks later
+    }
+    if (v0 >= r) return;
+#pragma unroll
+    for (int v = 0; v < kB4sVpw; ++v)
+        if (v0 + v < r)
+#pragma unroll
+            for (int q = 0; q < NPL; ++q) {
+                const int row = lane + 32 * q;
+                if (row < n) V[(size_t)(v0 + v) * n + row] = x[v][q];
+            }
+}
+
 // V (n x r, ld n) = U_B [X; 0]: the left reflectors of bd_kernel applied in
 // reverse; warp per vector
 constexpr int kBackWarps = 4;

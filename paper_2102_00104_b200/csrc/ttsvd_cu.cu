@@ -890,11 +890,30 @@ int svd_vectors(ttsvd_cu_ctx* ctx, int64_t r, const double* sigma, double* Vout)
     TT_TRY(check_launch(ctx, "bd_vectors_kernel"));
     if (n <= 512) {
         const unsigned g = (unsigned)((r + 4 * kBack4Warps - 1) / (4 * kBack4Warps));
+        static const char* bsel = std::getenv("TTSVD_BACK");  // diagnostics: "reg" = the register-prefetch kernel
+        if (bsel && std::string(bsel) == "reg") {
+            if (n <= 256)
+                bd_back4_kernel<8><<<g, kBack4Warps * 32, 0, ctx->stream>>>(ctx->bd_A, tauL, n, m, X, (int)r, Vout);
+            else
+                bd_back4_kernel<16><<<g, kBack4Warps * 32, 0, ctx->stream>>>(ctx->bd_A, tauL, n, m, X, (int)r, Vout);
+            return check_launch(ctx, "bd_back4_kernel");
+        }
+        static bool b4attr = false;
+        if (!b4attr) {
+            TT_CUDA(cudaFuncSetAttribute(bd_back4s_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)bd_back4s_smem(8)));
+            TT_CUDA(cudaFuncSetAttribute(bd_back4s_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)bd_back4s_smem(16)));
+            b4attr = true;
+        }
+        const unsigned gs = (unsigned)((r + kB4sVpw * kB4sWarps - 1) / (kB4sVpw * kB4sWarps));
         if (n <= 256)
-            bd_back4_kernel<8><<<g, kBack4Warps * 32, 0, ctx->stream>>>(ctx->bd_A, tauL, n, m, X, (int)r, Vout);
+            bd_back4s_kernel<8><<<gs, kB4sWarps * 32, bd_back4s_smem(8), ctx->stream>>>(ctx->bd_A, tauL, n, m, X,
+                                                                                        (int)r, Vout);
         else
-            bd_back4_kernel<16><<<g, kBack4Warps * 32, 0, ctx->stream>>>(ctx->bd_A, tauL, n, m, X, (int)r, Vout);
-        return check_launch(ctx, "bd_back4_kernel");
+            bd_back4s_kernel<16><<<gs, kB4sWarps * 32, bd_back4s_smem(16), ctx->stream>>>(ctx->bd_A, tauL, n, m, X,
+                                                                                          (int)r, Vout);
+        return check_launch(ctx, "bd_back4s_kernel");
     }
     const size_t smem = (size_t)kBackWarps * n * 8;
     static bool attr = false;
