@@ -28,6 +28,15 @@ def tt_contract_flat(cores: list[torch.Tensor]) -> torch.Tensor:
         rl, n, rr = c.shape
         N = M.shape[0]
         out = torch.empty((n * N, rr), dtype=M.dtype, device=M.device)
+        if rr == 1:  # last core: out (n x N, row-major) = G[:, :, 0]^T M^T, one GEMM per chunk
+            Gt = c[:, :, 0].t().contiguous()  # n x rl
+            o2 = out.view(n, N)
+            for c0 in range(0, N, chunk):
+                c1 = min(N, c0 + chunk)
+                torch.matmul(Gt, M[c0:c1].t(), out=o2[:, c0:c1])
+            del M
+            M = out
+            continue
         for x in range(n):
             Gx = c[:, x, :].contiguous()  # rl x rr
             for c0 in range(0, N, chunk):
