@@ -538,7 +538,9 @@ int tsqr_device(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t ld
         // 4 update warps leave the trailing update on the critical path,
         // 25.6 M).  TTSVD_T2ROWS=128|192|256 selects one for A/B timing.
         static const char* t2sel = std::getenv("TTSVD_T2ROWS");
-        const int t2want = t2sel ? std::atoi(t2sel) : 192;
+        // (M <= 128: the update is small and four update warps keep up, so
+        // 256-row tiles win: config 3 k = 64 / 128 34.2 -> 32.8 / 38.8 -> 37.4 ms)
+        const int t2want = t2sel ? std::atoi(t2sel) : (M <= 128 ? 256 : 192);
         const int t2rows = (t2want == 192 || t2want == 256) && n >= (int64_t)ctx->num_sms * 4 * t2want ? t2want : 128;
         if (!R_init && want_t128 && (n >= (int64_t)ctx->num_sms * 4 * kT2Rows || (force_t128 && n >= 4 * kT2Rows))) {
             const int64_t Gt = ctx->num_sms;

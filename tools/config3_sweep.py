@@ -8,7 +8,11 @@ import numpy as np
 import torch
 import paper_2102_00104_b200 as tt
 
-HBM = 6461.2  # GB/s, MEASURED_PEAKS.json
+try:  # GB/s, the driver-written MEASURED_PEAKS.json (copy bandwidth)
+    _pk = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "MEASURED_PEAKS.json")))
+    HBM = float(_pk.get("hbm_copy_gbs") or _pk.get("hbm_gbs") or 6461.2)
+except Exception:
+    HBM = 6461.2
 FP64 = 37.1   # TF/s, DMMA probe
 
 
