@@ -46,16 +46,17 @@ inline size_t t2_smem_bytes(int rows = kT2Rows) {
            sizeof(double);
 }
 
-template <int PW>
+template <int PW, int ID = 2>
 __device__ __forceinline__ void t2_bar_panel() {
-    asm volatile("bar.sync 2, %0;" ::"n"(PW * 32) : "memory");
+    asm volatile("bar.sync %0, %1;" ::"n"(ID), "n"(PW * 32) : "memory");
 }
-// T build: panel warps 0..3 only
-__device__ __forceinline__ void t2_bar_t() { asm volatile("bar.sync 3, 128;" ::: "memory"); }
+// T build: four warps (the panel warps 0..3 of a stream)
+template <int ID = 3>
+__device__ __forceinline__ void t2_bar_t() { asm volatile("bar.sync %0, 128;" ::"n"(ID) : "memory"); }
 
 // panel warps 0..3: factor the 128 x 32 panel in P (ld kT2Pld) against the
 // diagonal R block Rp; leaves V in P, the new block in Rp, tau, striu(S) in Sm.
-template <int PW>
+template <int PW, int BAR = 2>
 __device__ __forceinline__ void t2_panel(double* P, double* Rp, double* tau, double* pvall, double* dpart, double* Sm,
                                          int warp, int lane) {
     constexpr int Pld = 32 * PW + 4;
@@ -101,7 +102,7 @@ __device__ __forceinline__ void t2_panel(double* P, double* Rp, double* tau, dou
         }
         const double dk = ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
         sts1_if(true, s_dp + 8 * (par * 32 * PW + warp * 32 + lane), dk);
-        t2_bar_panel<PW>();
+        t2_bar_panel<PW, BAR>();
         if (w0 && pend_j >= 0) {  // everyone is past reflector j-1: publish its R row
             sts1_if(pend_upd, s_rcol + 8 * pend_j, pend_r);
             sts1_if(lane == pend_j, s_rp + 8 * pend_j * (kLaRld + 1), pend_alpha);
@@ -169,7 +170,7 @@ __device__ __forceinline__ void t2_panel(double* P, double* Rp, double* tau, dou
         }
         __syncwarp();
     }
-    t2_bar_panel<PW>();
+    t2_bar_panel<PW, BAR>();
     if (w0) {
         sts1_if(pend_upd, s_rcol + 8 * pend_j, pend_r);
         sts1_if(lane == pend_j, s_rp + 8 * pend_j * (kLaRld + 1), pend_alpha);
@@ -178,13 +179,14 @@ __device__ __forceinline__ void t2_panel(double* P, double* Rp, double* tau, dou
 #pragma unroll
     for (int i = 0; i < 32; i += 2)
         *reinterpret_cast<double2*>(P + lane * Pld + 32 * warp + i) = make_double2(my_scale * x[i], my_scale * x[i + 1]);
-    t2_bar_panel<PW>();
+    t2_bar_panel<PW, BAR>();
 }
 
 // panel warps 0..3: T = (diag(1/tau) + striu(S))^{-1} (row-major, ld kLaTld)
 // by 8 x 8 diagonal blocks (warp k back-substitutes block k, lane j < 8 one
 // column) and two levels of [[A, B], [0, C]]^{-1} = [[A^-1, -A^-1 B C^-1],
 // [0, C^-1]]; X (16 x 16 scratch) holds the B C^-1 products.
+template <int BAR = 3>
 __device__ __forceinline__ void t2_build_t(const double* Sm, const double* tau, double* Tm, double* X, int warp,
                                            int lane) {
     {
@@ -208,7 +210,7 @@ __device__ __forceinline__ void t2_build_t(const double* Sm, const double* tau, 
                 for (int i = 0; i < 8; ++i) Tm[(b0 + i) * kLaTld + c] = 0.0;
         }
     }
-    t2_bar_t();
+    t2_bar_t<BAR>();
     // level 1: blocks (0,1) by warp 0, (2,3) by warp 1: T_ab = -T_aa (S_ab T_bb)
     if (warp < 2) {
         const int a0 = 16 * warp, b0 = a0 + 8;
@@ -231,7 +233,7 @@ __device__ __forceinline__ void t2_build_t(const double* Sm, const double* tau, 
             Tm[(a0 + i) * kLaTld + b0 + j] = -acc;
         }
     }
-    t2_bar_t();
+    t2_bar_t<BAR>();
     // level 2: T[0:16, 16:32] = -T[0:16, 0:16] (S[0:16, 16:32] T[16:32, 16:32])
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
@@ -241,7 +243,7 @@ __device__ __forceinline__ void t2_build_t(const double* Sm, const double* tau, 
         for (int l = 0; l < 16; ++l) acc = fma(Sm[i * kTld + 16 + l], Tm[(16 + l) * kLaTld + 16 + j], acc);
         X[i * 16 + j] = acc;
     }
-    t2_bar_t();
+    t2_bar_t<BAR>();
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
         const int e = 64 * warp + lane + 32 * h, i = e >> 4, j = e & 15;
@@ -250,7 +252,7 @@ __device__ __forceinline__ void t2_build_t(const double* Sm, const double* tau, 
         for (int l = 0; l < 16; ++l) acc = fma(Tm[i * kLaTld + l], X[l * 16 + j], acc);
         Tm[i * kLaTld + 16 + j] = -acc;
     }
-    t2_bar_t();
+    t2_bar_t<BAR>();
 }
 
 // one warp: apply panel p's block reflector (V: 128 x 32 in smem, ld kT2Pld;
