@@ -800,7 +800,8 @@ int finalize_device(ttsvd_cu_ctx* ctx, const double* A, int n, int m, const doub
 
 // Bidiagonal path (bidiag.cuh) of svd_work: sigma now, the vectors later by
 // svd_vectors.  Returns -1 (nothing launched) when A does not fit the cluster.
-constexpr int kBdMinM = 64;
+// the bidiagonal path from m = 16 (config 2 steps 1 and 6: 0.17 -> 0.10 ms, 0.21 -> 0.12 ms)
+static const int kBdMinM = std::getenv("TTSVD_BDMIN") ? std::atoi(std::getenv("TTSVD_BDMIN")) : 16;
 int bd_sigma(ttsvd_cu_ctx* ctx, double* A, int n, int m, double* sigma) {
     const int need = (m + kBdCluster - 1) / kBdCluster;
     const int cpc = need <= 8 ? 8 : (need <= 16 ? 16 : 32);

@@ -107,10 +107,18 @@ def test_driver_svd_wide_work_matrix(tt):
 
 
 def test_driver_svd_small_uses_jacobi(tt):
-    # below the bidiagonal threshold (m < 64) the Jacobi path runs; same contract
+    # below the bidiagonal threshold (m < 16) the Jacobi path runs; same contract
     rng = np.random.default_rng(2)
-    A = np.asfortranarray(rng.standard_normal((80, 40)))
-    check(tt, A, 10, path="jacobi", ang_tol=1e-9)
+    A = np.asfortranarray(rng.standard_normal((80, 12)))
+    check(tt, A, 6, path="jacobi", ang_tol=1e-9)
+
+
+@pytest.mark.parametrize("n,m,r", [(80, 40, 10), (16, 16, 16), (512, 16, 16), (300, 17, 5)])
+def test_driver_svd_narrow_bidiag(tt, n, m, r):
+    # from m = 16 the bidiagonal path runs (config 2 steps 1 and 6 have m = 16)
+    rng = np.random.default_rng(n + m)
+    A = np.asfortranarray(rng.standard_normal((n, m)))
+    check(tt, A, r, path="bidiag", ang_tol=1e-9)
 
 
 def test_driver_svd_matches_reference_jacobi(tt):
