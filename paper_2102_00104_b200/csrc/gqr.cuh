@@ -25,7 +25,7 @@
 
 namespace ttsvd_b200 {
 
-constexpr int kGqrThreads = 256;
+constexpr int kGqrThreads = 256;  // threads of the 256-thread variant (rows per CTA <= 256)
 constexpr int kGqrMaxRows = 512;  // rows per CTA (panel rows in shared memory)
 constexpr int kGqrCluster = 16;   // CTAs of the cluster variant
 
@@ -100,9 +100,9 @@ __device__ __forceinline__ double gqr_sum_inflight(const double* base, int64_t q
 
 __host__ __device__ inline int gqr_ldy(int rows) { return ((((rows + 3) & ~3) + 7) & ~7) + 4; }
 
-inline size_t gqr_smem_bytes(int rows_max) {
+inline size_t gqr_smem_bytes(int rows_max, int nt = kGqrThreads) {
     const int ldy = gqr_ldy(rows_max);
-    return ((size_t)32 * ldy + 2 * 32 * 33 + 32 + 16 * 33 + (kGqrThreads / 32) * 32 * 9) * sizeof(double);
+    return ((size_t)32 * ldy + 2 * 32 * 33 + 32 + 2 * (nt / 32) * 33 + (nt / 32) * 32 * 9) * sizeof(double);
 }
 
 // CL = false: one cooperative grid (grid.sync); CL = true: the grid is one
@@ -110,8 +110,8 @@ inline size_t gqr_smem_bytes(int rows_max) {
 // barrier (arrive.release / wait.acquire orders the global-memory partials
 // at cluster scope) — ~0.2 us instead of ~2 us per barrier for the short
 // steps (n <= 16 x 512)
-template <bool CL>
-__global__ void __launch_bounds__(kGqrThreads, 1) gqr_kernel(GqrArgs a) {
+template <bool CL, int NT>
+__global__ void __launch_bounds__(NT, 1) gqr_kernel(GqrArgs a) {
     namespace cg = cooperative_groups;
     auto gsync = [&]() {
         if constexpr (CL) {
@@ -139,8 +139,8 @@ __global__ void __launch_bounds__(kGqrThreads, 1) gqr_kernel(GqrArgs a) {
     double* Sm = Ys + 32 * ldy;              // 32 x 33
     double* Tm = Sm + 32 * 33;               // 32 x 33
     double* tau = Tm + 32 * 33;              // 32
-    double* red = tau + 32;                  // 16 x 33 (warp totals, then slice totals)
-    double* Wsc = red + 16 * 33;             // per-warp 32 x 8 (ld 9)
+    double* red = tau + 32;                  // 2 NW x 33 (warp totals, then slice totals)
+    double* Wsc = red + 2 * (NT / 32) * 33;  // per-warp 32 x 8 (ld 9)
     double* part = a.part;
     double* A = a.A;
     const int lr = lane >> 2, lc = lane & 3;
@@ -156,7 +156,7 @@ __global__ void __launch_bounds__(kGqrThreads, 1) gqr_kernel(GqrArgs a) {
     for (int p = 0; p < M / 32; ++p) {
         const int64_t c0 = 32 * (int64_t)p;
         // ---- stage my rows of the panel ----
-        for (int e = tid; e < 32 * ldy; e += kGqrThreads) {
+        for (int e = tid; e < 32 * ldy; e += NT) {
             const int k = e / ldy, i = e - k * ldy;
             Ys[e] = i < rows ? A[(c0 + k) * lda + r0 + i] : 0.0;
         }
@@ -171,7 +171,7 @@ __global__ void __launch_bounds__(kGqrThreads, 1) gqr_kernel(GqrArgs a) {
             double v[32];
 #pragma unroll
             for (int k = 0; k < 32; ++k) v[k] = 0.0;
-            for (int i = tid; i < rows; i += kGqrThreads) {
+            for (int i = tid; i < rows; i += NT) {
                 const int64_t gi = r0 + i;
                 if (gi <= j) {
                     if (gi == j)  // pivot row -> broadcast slot
@@ -191,7 +191,7 @@ __global__ void __launch_bounds__(kGqrThreads, 1) gqr_kernel(GqrArgs a) {
             __syncthreads();
             if (tid < 32) {
                 double t = 0.0;
-                for (int w = 0; w < kGqrThreads / 32; ++w) t += red[w * 33 + tid];
+                for (int w = 0; w < NT / 32; ++w) t += red[w * 33 + tid];
                 part[((int64_t)buf * G + c) * 33 + tid] = t;
             }
             long long tq0 = pf ? gqr_clock() : 0;
@@ -204,14 +204,14 @@ __global__ void __launch_bounds__(kGqrThreads, 1) gqr_kernel(GqrArgs a) {
             {
                 const int k = tid & 31, sl = tid >> 5;
                 const double pv = (sl == 0) ? __ldcg(&a.piv[buf * 32 + k]) : 0.0;  // in flight with the sums
-                red[8 * 33 + sl * 33 + k] = gqr_sum_inflight<20>(part + (int64_t)buf * G * 33 + k, 33, G, sl, kGqrThreads / 32);
+                red[(NT / 32) * 33 + sl * 33 + k] = gqr_sum_inflight<20>(part + (int64_t)buf * G * 33 + k, 33, G, sl, NT / 32);
                 if (sl == 0) red[33 + k] = pv;
             }
             __syncthreads();
             if (tid < 32) {
                 double t = 0.0;
 #pragma unroll
-                for (int sl = 0; sl < kGqrThreads / 32; ++sl) t += red[8 * 33 + sl * 33 + tid];
+                for (int sl = 0; sl < NT / 32; ++sl) t += red[(NT / 32) * 33 + sl * 33 + tid];
                 red[tid] = t;
             }
             __syncthreads();
@@ -241,7 +241,7 @@ __global__ void __launch_bounds__(kGqrThreads, 1) gqr_kernel(GqrArgs a) {
             double gam[32];
 #pragma unroll
             for (int k = 0; k < 32; ++k) gam[k] = (k > jj) ? tj * (red[33 + k] + scale * red[k]) : 0.0;
-            for (int i = tid; i < rows; i += kGqrThreads) {
+            for (int i = tid; i < rows; i += NT) {
                 const int64_t gi = r0 + i;
                 if (gi < j) continue;
                 if (gi == j) {
@@ -263,7 +263,7 @@ __global__ void __launch_bounds__(kGqrThreads, 1) gqr_kernel(GqrArgs a) {
         }
         GQR_PROF(1);
         // ---- write back the panel (R rows and v), then the structured Y in smem ----
-        for (int e = tid; e < 32 * ldy; e += kGqrThreads) {
+        for (int e = tid; e < 32 * ldy; e += NT) {
             const int k = e / ldy, i = e - k * ldy;
             if (i < rows) {
                 A[(c0 + k) * lda + r0 + i] = Ys[e];
@@ -298,7 +298,7 @@ __global__ void __launch_bounds__(kGqrThreads, 1) gqr_kernel(GqrArgs a) {
         {
             const int E = (1024 + G - 1) / G;
             const double* ps = part + (int64_t)2 * G * 33;
-            for (int el = warp; el < E; el += kGqrThreads / 32) {
+            for (int el = warp; el < E; el += NT / 32) {
                 const int e = c * E + el;
                 if (e < 1024) {
                     double s = gqr_sum_inflight<8>(ps + e, 1024, G, lane, 32);
@@ -311,12 +311,12 @@ __global__ void __launch_bounds__(kGqrThreads, 1) gqr_kernel(GqrArgs a) {
         gfence();
         gsync();
         {
-            double sv[1024 / kGqrThreads];
+            double sv[1024 / NT];
 #pragma unroll
-            for (int r = 0; r < 1024 / kGqrThreads; ++r) sv[r] = __ldcg(a.Sfin + tid + r * kGqrThreads);
+            for (int r = 0; r < 1024 / NT; ++r) sv[r] = __ldcg(a.Sfin + tid + r * NT);
 #pragma unroll
-            for (int r = 0; r < 1024 / kGqrThreads; ++r) {
-                const int e = tid + r * kGqrThreads;
+            for (int r = 0; r < 1024 / NT; ++r) {
+                const int e = tid + r * NT;
                 Sm[(e >> 5) * 33 + (e & 31)] = sv[r];
             }
         }
@@ -335,7 +335,7 @@ __global__ void __launch_bounds__(kGqrThreads, 1) gqr_kernel(GqrArgs a) {
         for (int lev = 8; lev <= 16; lev *= 2) {
             double* Xs = Wsc;
             const int nblk = 32 / (2 * lev);
-            for (int e = tid; e < nblk * lev * lev; e += kGqrThreads) {
+            for (int e = tid; e < nblk * lev * lev; e += NT) {
                 const int q = e / (lev * lev), i = (e / lev) % lev, jx = e % lev;
                 const int o = q * 2 * lev;
                 double acc = 0.0;
@@ -343,7 +343,7 @@ __global__ void __launch_bounds__(kGqrThreads, 1) gqr_kernel(GqrArgs a) {
                 Xs[q * 17 * 17 + i * 17 + jx] = acc;
             }
             __syncthreads();
-            for (int e = tid; e < nblk * lev * lev; e += kGqrThreads) {
+            for (int e = tid; e < nblk * lev * lev; e += NT) {
                 const int q = e / (lev * lev), i = (e / lev) % lev, jx = e % lev;
                 const int o = q * 2 * lev;
                 double acc = 0.0;
@@ -357,7 +357,7 @@ __global__ void __launch_bounds__(kGqrThreads, 1) gqr_kernel(GqrArgs a) {
         const int64_t t0 = c0 + 32;
         const int ngr = (int)((M - t0) / 8);
         double* pw = part + (int64_t)2 * G * 33 + (int64_t)G * 1024;  // G x 32 x M (cols t0..M used)
-        for (int gq = warp; gq < ngr; gq += kGqrThreads / 32) {
+        for (int gq = warp; gq < ngr; gq += NT / 32) {
             const int64_t g = t0 + 8 * gq;
             double acc[4][2];
 #pragma unroll
@@ -397,12 +397,12 @@ __global__ void __launch_bounds__(kGqrThreads, 1) gqr_kernel(GqrArgs a) {
             // in order and forms W'(:, col) = T^T W(:, col)
             double* wsl = Wsc;  // 8 x 33
             for (int64_t col = ca; col < cb; ++col) {
-                wsl[warp * 33 + lane] = gqr_sum_inflight<20>(pw + (int64_t)lane * M + col, (int64_t)32 * M, G, warp, kGqrThreads / 32);
+                wsl[warp * 33 + lane] = gqr_sum_inflight<20>(pw + (int64_t)lane * M + col, (int64_t)32 * M, G, warp, NT / 32);
                 __syncthreads();
                 if (warp == 0) {
                     double w = 0.0;
 #pragma unroll
-                    for (int sl = 0; sl < kGqrThreads / 32; ++sl) w += wsl[sl * 33 + lane];
+                    for (int sl = 0; sl < NT / 32; ++sl) w += wsl[sl * 33 + lane];
                     double wp = 0.0;
                     for (int k = 0; k < 32; ++k) wp = fma(Tm[k * 33 + lane], __shfl_sync(0xffffffffu, w, k), wp);
                     a.Wfin[(int64_t)lane * M + col] = wp;
@@ -414,7 +414,7 @@ __global__ void __launch_bounds__(kGqrThreads, 1) gqr_kernel(GqrArgs a) {
         gsync();
         GQR_PROF(4);
         // ---- A(rows_c, trail) -= Y_c W': DMMA per 8-column group, 64-row chunks ----
-        for (int gq = warp; gq < ngr; gq += kGqrThreads / 32) {
+        for (int gq = warp; gq < ngr; gq += NT / 32) {
             const int64_t g = t0 + 8 * gq;
             double* Ws = Wsc + warp * 32 * 9;
             for (int e = lane; e < 256; e += 32) Ws[(e >> 3) * 9 + (e & 7)] = __ldcg(&a.Wfin[(int64_t)(e >> 3) * M + g + (e & 7)]);

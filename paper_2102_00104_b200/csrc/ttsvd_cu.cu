@@ -295,17 +295,24 @@ int gqr_device(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t ld,
     }
     while ((n + Gq - 1) / Gq > kGqrMaxRows) ++Gq;
     const int rows_max = (int)((n + Gq - 1) / Gq);
-    const size_t smem = gqr_smem_bytes(rows_max);
+    // more than 256 rows per CTA: 512 threads (one row each; the blocked
+    // updates gain more than the reflector chain loses — config 2 step 3
+    // 6.31 -> 5.74 ms); otherwise 256 (steps with <= 256 rows per CTA are
+    // slower with 512)
+    const int gnt = (rows_max > 256 && !cl) ? 512 : 256;
+    const size_t smem = gqr_smem_bytes(rows_max, gnt);
     static bool gattr = false;
     if (!gattr) {
-        TT_CUDA(cudaFuncSetAttribute(gqr_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit));
-        TT_CUDA(cudaFuncSetAttribute(gqr_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit));
-        TT_CUDA(cudaFuncSetAttribute(gqr_kernel<true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        TT_CUDA(cudaFuncSetAttribute(gqr_kernel<false, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit));
+        TT_CUDA(cudaFuncSetAttribute(gqr_kernel<false, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit));
+        TT_CUDA(cudaFuncSetAttribute(gqr_kernel<true, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit));
+        TT_CUDA(cudaFuncSetAttribute(gqr_kernel<true, 256>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
         gattr = true;
     }
     if (!cl) {
         int per_sm = 0;
-        TT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gqr_kernel<false>, kGqrThreads, smem));
+        TT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gnt == 512 ? gqr_kernel<false, 512> : gqr_kernel<false, 256>,
+                                                              gnt, smem));
         if (per_sm < 1 || Gq > (int64_t)per_sm * ctx->num_sms) return -1;
     }
     TT_TRY(ensure(ctx->ws_G, (size_t)n * M * 8));
@@ -338,11 +345,11 @@ int gqr_device(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t ld,
         at[0].val.clusterDim.z = 1;
         cfg.attrs = at;
         cfg.numAttrs = 1;
-        TT_CUDA(cudaLaunchKernelEx(&cfg, gqr_kernel<true>, ga));
+        TT_CUDA(cudaLaunchKernelEx(&cfg, gqr_kernel<true, 256>, ga));
     } else {
         void* args[] = {&ga};
-        TT_CUDA(cudaLaunchCooperativeKernel((const void*)gqr_kernel<false>, dim3((unsigned)Gq), dim3(kGqrThreads), args,
-                                            smem, ctx->stream));
+        TT_CUDA(cudaLaunchCooperativeKernel(gnt == 512 ? (const void*)gqr_kernel<false, 512> : (const void*)gqr_kernel<false, 256>,
+                                            dim3((unsigned)Gq), dim3(gnt), args, smem, ctx->stream));
     }
     TT_TRY(check_launch(ctx, "gqr_kernel"));
     if (prof) {
