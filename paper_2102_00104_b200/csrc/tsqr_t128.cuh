@@ -26,7 +26,7 @@
 namespace ttsvd_b200 {
 
 constexpr int kT2Rows = 128;     // rows per tile of the 128-row variant
-constexpr int kT2Threads = 384;  // ROWS / 32 panel warps + the rest update warps
+constexpr int kT2Threads = 512;  // ROWS / 32 panel warps + the rest update warps
 constexpr int kT2Pld = 132;  // smem ld of a panel buffer (128 rows + 4)
 // smem ld of a panel buffer of a ROWS-row tile
 __host__ __device__ constexpr int t2_pld(int rows) { return rows + 4; }

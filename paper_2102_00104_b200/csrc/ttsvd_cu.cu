@@ -539,16 +539,17 @@ int tsqr_device(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t ld
         static const char* tsel = std::getenv("TTSVD_TSQR");  // diagnostics: "t128", "la"
         const bool force_t128 = tsel && std::string(tsel) == "t128";
         const bool want_t128 = tsel ? force_t128 : true;
-        // 192-row tiles (6 panel + 6 update warps) when every CTA gets >= 4
-        // of them: the reflector chain per row is 2/3 of the 128-row tile's
-        // (config 2 step 2: 27.1 -> 24.3 M cycles per CTA; 256-row tiles with
-        // 4 update warps leave the trailing update on the critical path,
-        // 25.6 M).  TTSVD_T2ROWS=128|192|256 selects one for A/B timing.
+        // 256-row tiles (8 panel + 8 update warps of a 512-thread CTA) when
+        // every CTA gets >= 4 of them: the reflector chain per row is half the
+        // 128-row tile's (config 2 step 2 sweep: 13.7 ms at 128 rows / 384
+        // threads, 12.35 at 192 / 384, 11.8 at 256 / 512; 12.8 at 320 / 512).
+        // TTSVD_T2ROWS=128|192|256|320 selects one for A/B timing.
         static const char* t2sel = std::getenv("TTSVD_T2ROWS");
-        // (M <= 128: the update is small and four update warps keep up, so
-        // 256-row tiles win: config 3 k = 64 / 128 34.2 -> 32.8 / 38.8 -> 37.4 ms)
-        const int t2want = t2sel ? std::atoi(t2sel) : (M <= 128 ? 256 : 192);
-        const int t2rows = (t2want == 192 || t2want == 256) && n >= (int64_t)ctx->num_sms * 4 * t2want ? t2want : 128;
+        const int t2want = t2sel ? std::atoi(t2sel) : 256;
+        const int t2rows = (t2want == 192 || t2want == 256 || t2want == 320) &&
+                                   n >= (int64_t)ctx->num_sms * 4 * t2want
+                               ? t2want
+                               : 128;
         if (!R_init && want_t128 && (n >= (int64_t)ctx->num_sms * 4 * kT2Rows || (force_t128 && n >= 4 * kT2Rows))) {
             const int64_t Gt = ctx->num_sms;
             TT_TRY(ensure(ctx->ws_R, (size_t)Gt * RS * 8));
@@ -562,6 +563,8 @@ int tsqr_device(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t ld
                                              (int)t2_smem_bytes(256)));
                 TT_CUDA(cudaFuncSetAttribute(tsqr_t128_kernel<192>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)t2_smem_bytes(192)));
+                TT_CUDA(cudaFuncSetAttribute(tsqr_t128_kernel<320>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)t2_smem_bytes(320)));
                 tattr = true;
             }
             static const bool tprof = std::getenv("TTSVD_PROF_BLK") != nullptr;
@@ -573,6 +576,8 @@ int tsqr_device(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t ld
                 tsqr_t128_kernel<256><<<(unsigned)Gt, kT2Threads, t2_smem_bytes(256), ctx->stream>>>(ta);
             else if (t2rows == 192)
                 tsqr_t128_kernel<192><<<(unsigned)Gt, kT2Threads, t2_smem_bytes(192), ctx->stream>>>(ta);
+            else if (t2rows == 320)
+                tsqr_t128_kernel<320><<<(unsigned)Gt, kT2Threads, t2_smem_bytes(320), ctx->stream>>>(ta);
             else
                 tsqr_t128_kernel<128><<<(unsigned)Gt, kT2Threads, t2_smem_bytes(128), ctx->stream>>>(ta);
             TT_TRY(check_launch(ctx, "tsqr_t128_kernel"));
