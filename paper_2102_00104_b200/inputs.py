@@ -31,9 +31,10 @@ def tt_contract_flat(cores: list[torch.Tensor]) -> torch.Tensor:
         if rr == 1:  # last core: out (n x N, row-major) = G[:, :, 0]^T M^T, one GEMM per chunk
             Gt = c[:, :, 0].t().contiguous()  # n x rl
             o2 = out.view(n, N)
-            for c0 in range(0, N, chunk):
-                c1 = min(N, c0 + chunk)
-                torch.matmul(Gt, M[c0:c1].t(), out=o2[:, c0:c1])
+            ck = 1 << 27  # the (n x ck) product is staged: o2's row stride N may exceed int32
+            for c0 in range(0, N, ck):
+                c1 = min(N, c0 + ck)
+                o2[:, c0:c1].copy_(Gt @ M[c0:c1].t())
             del M
             M = out
             continue
