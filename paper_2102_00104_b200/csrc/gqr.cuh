@@ -102,7 +102,7 @@ __host__ __device__ inline int gqr_ldy(int rows) { return ((((rows + 3) & ~3) + 
 
 inline size_t gqr_smem_bytes(int rows_max, int nt = kGqrThreads) {
     const int ldy = gqr_ldy(rows_max);
-    return ((size_t)32 * ldy + 2 * 32 * 33 + 32 + 2 * (nt / 32) * 33 + (nt / 32) * 32 * 9) * sizeof(double);
+    return ((size_t)32 * ldy + 2 * 32 * 33 + 32 + 2 * (nt / 32) * 33 + (nt / 32) * 32 * 9 + 40) * sizeof(double);
 }
 
 // CL = false: one cooperative grid (grid.sync); CL = true: the grid is one
@@ -141,6 +141,7 @@ __global__ void __launch_bounds__(NT, 1) gqr_kernel(GqrArgs a) {
     double* tau = Tm + 32 * 33;              // 32
     double* red = tau + 32;                  // 2 NW x 33 (warp totals, then slice totals)
     double* Wsc = red + 2 * (NT / 32) * 33;  // per-warp 32 x 8 (ld 9)
+    double* gsm = Wsc + (NT / 32) * 32 * 9;  // 32 gamma + scale, alpha
     double* part = a.part;
     double* A = a.A;
     const int lr = lane >> 2, lc = lane & 3;
@@ -208,46 +209,52 @@ __global__ void __launch_bounds__(NT, 1) gqr_kernel(GqrArgs a) {
                 if (sl == 0) red[33 + k] = pv;
             }
             __syncthreads();
+            // warp 0: the totals, the reflector (every CTA derives the same
+            // bits) and gamma_k = tau (A(j,k) + scale d_k) for the columns
+            // k > jj, once per CTA instead of once per thread
             if (tid < 32) {
                 double t = 0.0;
 #pragma unroll
                 for (int sl = 0; sl < NT / 32; ++sl) t += red[(NT / 32) * 33 + sl * 33 + tid];
-                red[tid] = t;
+                const double pk = red[33 + tid];
+                const double sp = __shfl_sync(0xffffffffu, t, 0);
+                const double u0 = __shfl_sync(0xffffffffu, pk, jj);
+                const double nrm2 = u0 * u0 + sp;
+                const double inv = fast_rsqrt(nrm2);
+                const double nr = nrm2 * inv;
+                const double au = fabs(u0);
+                const double sg = (u0 > 0.0) ? 1.0 : -1.0;
+                double alpha = -sg * nr, tj = 1.0 + au * inv, scale = sg * fast_rcp(au + nr);
+                if (sp == 0.0 && u0 != 0.0) {
+                    alpha = u0;
+                    tj = 0.0;
+                    scale = 0.0;
+                }
+                if (nrm2 == 0.0) {
+                    alpha = sqrt(2.0 * DBL_MIN);
+                    tj = 2.0;
+                    scale = 0.0;
+                }
+                gsm[tid] = (tid > jj) ? tj * (pk + scale * t) : 0.0;
+                if (tid == 0) {
+                    gsm[32] = scale;
+                    gsm[33] = alpha;
+                    tau[jj] = tj;
+                }
             }
             __syncthreads();
             if (pf) {
                 const long long tq1 = gqr_clock();
                 a.prof[7] += tq1 - tq0;
             }
-            const double sp = red[0];
-            const double u0 = red[33 + jj];
-            const double nrm2 = u0 * u0 + sp;
-            const double inv = fast_rsqrt(nrm2);
-            const double nr = nrm2 * inv;
-            const double au = fabs(u0);
-            const double sg = (u0 > 0.0) ? 1.0 : -1.0;
-            double alpha = -sg * nr, tj = 1.0 + au * inv, scale = sg * fast_rcp(au + nr);
-            if (sp == 0.0 && u0 != 0.0) {
-                alpha = u0;
-                tj = 0.0;
-                scale = 0.0;
-            }
-            if (nrm2 == 0.0) {
-                alpha = sqrt(2.0 * DBL_MIN);
-                tj = 2.0;
-                scale = 0.0;
-            }
-            // gamma_k = tau (A(j,k) + scale d_k): column k > jj
-            double gam[32];
-#pragma unroll
-            for (int k = 0; k < 32; ++k) gam[k] = (k > jj) ? tj * (red[33 + k] + scale * red[k]) : 0.0;
+            const double scale = gsm[32], alpha = gsm[33];
             for (int i = tid; i < rows; i += NT) {
                 const int64_t gi = r0 + i;
                 if (gi < j) continue;
                 if (gi == j) {
 #pragma unroll
                     for (int k = 0; k < 32; ++k)
-                        if (k > jj) Ys[k * ldy + i] -= gam[k];
+                        if (k > jj) Ys[k * ldy + i] -= gsm[k];
                     Ys[jj * ldy + i] = alpha;
                     continue;
                 }
@@ -255,10 +262,9 @@ __global__ void __launch_bounds__(NT, 1) gqr_kernel(GqrArgs a) {
                 const double f = xj * scale;
 #pragma unroll
                 for (int k = 0; k < 32; ++k)
-                    if (k > jj) Ys[k * ldy + i] = fma(-gam[k], f, Ys[k * ldy + i]);
+                    if (k > jj) Ys[k * ldy + i] = fma(-gsm[k], f, Ys[k * ldy + i]);
                 Ys[jj * ldy + i] = f;  // v
             }
-            if (tid == 0) tau[jj] = tj;
             __syncthreads();
         }
         GQR_PROF(1);
