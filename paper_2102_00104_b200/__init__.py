@@ -12,5 +12,7 @@ from .ttsvd import (AllocationError, BlockParams, Context, ConvergenceError, Deg
                     TTCore, choose_combined_dims, combine_factors, context, derive_delta, driver_svd, fortran_empty, gen_uniform, jacobi_svd, padded_stride,
                     reduce_block, select_rank, small_svd, to_device_matrix, to_host, tsmm_reshape, tsqr,
                     tt_svd_distributed, tt_svd_thick_bounds, tt_svd_tsqr)
+from .wire import dump_tensor, emit_csv, load_tensor, load_tt, parse_csv, report_rows, save_tt
+from . import verify  # noqa: F401  (device tt_error / check_orthonormality)
 
 __all__ = [n for n in dir() if not n.startswith("_")]
