@@ -286,7 +286,10 @@ int gqr_device(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t ld,
     // updates), kept for A/B timing
     static const char* gsel = std::getenv("TTSVD_GQR");
     const bool cl = n <= (int64_t)kGqrCluster * kGqrMaxRows && gsel && std::string(gsel) == "cluster";
-    int64_t Gq = std::max<int64_t>(1, std::min<int64_t>(cl ? kGqrCluster : ctx->num_sms, n / 128));
+    // target rows per CTA (more CTAs: the blocked updates spread wider; config 2
+    // step 4, 4096 x 512: 3.30 ms at 128 rows, 3.07 at 64); TTSVD_GQR_ROWS overrides
+    static const int64_t gq_rows = std::getenv("TTSVD_GQR_ROWS") ? std::atoll(std::getenv("TTSVD_GQR_ROWS")) : 64;
+    int64_t Gq = std::max<int64_t>(1, std::min<int64_t>(cl ? kGqrCluster : ctx->num_sms, n / gq_rows));
     if (cl) {  // a power-of-two cluster
         int64_t g = 1;
         while (2 * g <= Gq) g *= 2;
