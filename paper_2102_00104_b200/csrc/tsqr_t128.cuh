@@ -259,7 +259,7 @@ __device__ __forceinline__ void t2_build_t(const double* Sm, const double* tau, 
 // T) to tile columns g..g+7 (source: input X or the scratch; destination:
 // scratch or a panel buffer) and to R(p, g..g+7).
 //   W^T = R(p, c)^T + B(:, c)^T V;  W'^T = W^T T;  R(p, c) -= W';  B(:, c) -= V W'.
-template <bool SRC_X, bool DST_SMEM, int ROWS>
+template <bool SRC_X, bool DST_SMEM, int ROWS, bool SRC_SMEM = false>
 __device__ __forceinline__ void t2_group(const double* src, int64_t lds, int rows, int mcols, double* dst, int64_t ldd,
                                          const double* V, const double* Tm, double* Rrow, int c0, int g, int gd,
                                          int lane, uint64_t pol_x, uint64_t pol_r) {
@@ -281,6 +281,7 @@ __device__ __forceinline__ void t2_group(const double* src, int64_t lds, int row
         for (int u = 0; u < 8; ++u) {
             const int row = 4 * (kc + u) + q;
             if (SRC_X) av[u] = (row < rows && g + r < mcols) ? ld_hint(scol + row, pol_x) : 0.0;
+            else if (SRC_SMEM) av[u] = scol[row];
             else av[u] = __ldcg(scol + row);
         }
 #pragma unroll
@@ -325,6 +326,7 @@ __device__ __forceinline__ void t2_group(const double* src, int64_t lds, int row
                 const int row = 8 * (mc + u) + r;
                 if (SRC_X)
                     cb[u][e] = (row < rows && g + 2 * q + e < mcols) ? ld_stream_hint(s0c + e * lds + row, pol_x) : 0.0;
+                else if (SRC_SMEM) cb[u][e] = s0c[e * lds + row];
                 else cb[u][e] = __ldcg(s0c + e * lds + row);
             }
 #pragma unroll
@@ -403,14 +405,25 @@ __global__ void __launch_bounds__(kT2Threads, 1) tsqr_t128_kernel(T2Args a) {
             const double* Tp = Tm0 + (p & 1) * 32 * kLaTld;
             double* Rrow = R + blk_roff(p, M);
             if (warp == 0) la_fetch_rdiag(Rp, R + blk_roff(p + 1, M), lane);
+            if (p > 0) {
+                // panel p+1's columns from the scratch into the next panel
+                // buffer (cp.async, all threads), so phase A runs from shared
+                // memory instead of waiting on L2 round trips
+                for (int e = tid; e < 32 * (ROWS / 2); e += kT2Threads) {
+                    const int c = e / (ROWS / 2), i2 = 2 * (e % (ROWS / 2));
+                    cp_async16(Pn + c * Pld + i2, Scr + (int64_t)(nxt + c) * ROWS + i2);
+                }
+                cp_async_wait_all();
+                __syncthreads();
+            }
             // phase A: panel p+1's columns, alone on the tensor pipes
             if (uw >= 0 && uw < 4) {
                 if (p == 0)
                     t2_group<true, true, ROWS>(Xt, a.ld, rows, m, Pn, Pld, V, Tp, Rrow, c0, nxt + 8 * uw, 8 * uw, lane, pol_x,
                                          pol_r);
                 else
-                    t2_group<false, true, ROWS>(Scr, ROWS, rows, m, Pn, Pld, V, Tp, Rrow, c0, nxt + 8 * uw, 8 * uw, lane,
-                                          pol_x, pol_r);
+                    t2_group<false, true, ROWS, true>(Pn - (int64_t)nxt * Pld, Pld, rows, m, Pn, Pld, V, Tp, Rrow, c0,
+                                                      nxt + 8 * uw, 8 * uw, lane, pol_x, pol_r);
             }
             T2_PROF(5);
             if (warp == 0) cp_async_wait_all();
