@@ -84,8 +84,11 @@ def test_tsqr_gram_property(tt, n, m):
 # The wide-factor kernels: 32-row look-ahead tiles (tsqr_la_kernel, n below
 # 4 x 128 rows per SM) and 128-row tiles (tsqr_t128_kernel), including partial
 # tiles, m not a multiple of 32, zero and duplicated columns and low rank.
+# (40000, 150) and (50000, 200): the cooperative short-fat kernel with more
+# than 256 rows per CTA (512 threads, a row each).
 @pytest.mark.parametrize("n,m,kind", [(40000, 96, "dense"), (30011, 45, "dup"), (80000, 64, "dense"),
-                                      (90001, 45, "dup"), (77777, 130, "lowrank"), (160000, 256, "dense")])
+                                      (90001, 45, "dup"), (77777, 130, "lowrank"), (160000, 256, "dense"),
+                                      (40000, 150, "dense"), (40000, 150, "dup"), (50000, 200, "lowrank")])
 def test_tsqr_wide_kernels(tt, n, m, kind):
     from oracle.oracle import gaussian
     X = gaussian(n, m, 31 + m).copy(order="F")
