@@ -1012,6 +1012,25 @@ int launch_tsmm(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t ld
     return check_launch(ctx, "tsmm_kernel");
 }
 
+template <int KC>
+int launch_tsmm_async(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t ldx, const double* V, int64_t ldv,
+                      int k, double* Y, int64_t out_rows, int64_t ldy) {
+    const size_t smem = ((size_t)((m * KC + 1) & ~1) + (size_t)2 * m * 256) * 8;
+    static bool attr = false;
+    static int per_sm = 1;
+    if (!attr) {
+        TT_CUDA(cudaFuncSetAttribute(tsmm_async_kernel<KC>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit));
+        attr = true;
+    }
+    TT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tsmm_async_kernel<KC>, 256, smem));
+    const int64_t chunks = (n + 255) / 256;
+    const int64_t blocks = std::min<int64_t>(chunks, (int64_t)std::max(1, per_sm) * ctx->num_sms);
+    const int ychunks = (k + KC - 1) / KC;
+    tsmm_async_kernel<KC><<<dim3((unsigned)blocks, (unsigned)ychunks), 256, smem, ctx->stream>>>(X, n, m, ldx, V, ldv,
+                                                                                              k, Y, out_rows, ldy);
+    return check_launch(ctx, "tsmm_async_kernel");
+}
+
 template <int NT>
 int launch_tsmm_dmma(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t ldx, const double* V, int64_t ldv,
                      int k, double* Y, int64_t out_rows, int64_t ldy) {
@@ -1048,7 +1067,13 @@ int tsmm_device(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t ld
         }
         return TTSVD_OK;
     }
-    if (k <= 1) rc = launch_tsmm<1>(ctx, X, n, m, ldx, V, ldv, k, Y, out_rows, ldy);
+    static const bool tsmm_async = !(tsel && std::string(tsel) == "ffma");
+    if (tsmm_async && k > 1 && k <= 16 && m <= 32 && n >= (int64_t)1 << 18) {
+        // narrow X: rows staged by cp.async (tsmm_async_kernel)
+        rc = k <= 4 ? launch_tsmm_async<4>(ctx, X, n, m, ldx, V, ldv, k, Y, out_rows, ldy)
+                    : (k <= 8 ? launch_tsmm_async<8>(ctx, X, n, m, ldx, V, ldv, k, Y, out_rows, ldy)
+                              : launch_tsmm_async<16>(ctx, X, n, m, ldx, V, ldv, k, Y, out_rows, ldy));
+    } else if (k <= 1) rc = launch_tsmm<1>(ctx, X, n, m, ldx, V, ldv, k, Y, out_rows, ldy);
     else if (k <= 2) rc = launch_tsmm<2>(ctx, X, n, m, ldx, V, ldv, k, Y, out_rows, ldy);
     else if (k <= 4) rc = launch_tsmm<4>(ctx, X, n, m, ldx, V, ldv, k, Y, out_rows, ldy);
     else if (k <= 8) rc = launch_tsmm<8>(ctx, X, n, m, ldx, V, ldv, k, Y, out_rows, ldy);

@@ -584,6 +584,85 @@ __global__ void __launch_bounds__(256) tsmm_kernel(const double* __restrict__ X,
     }
 }
 
+// K_TSMM for narrow X (m <= 32) and few output columns: the streamed rows are
+// staged in shared memory by cp.async (each thread copies its own row's m
+// values, 8 bytes apiece, one chunk of 256 rows ahead), so the bytes in
+// flight per SM are bounded by shared memory instead of registers; a thread
+// only reads the row it copied itself, so cp.async.wait_group is the only
+// synchronisation.  Same arithmetic and output placement as tsmm_kernel.
+template <int KC>
+__global__ void __launch_bounds__(256) tsmm_async_kernel(const double* __restrict__ X, int64_t n, int m, int64_t ldx,
+                                                         const double* __restrict__ V, int64_t ldv, int k,
+                                                         double* __restrict__ Y, int64_t out_rows, int64_t ldy) {
+    extern __shared__ __align__(16) double tsm[];
+    double* Vs = tsm;                         // m x KC
+    double* xb = tsm + ((m * KC + 1) & ~1);   // 2 x m x 256
+    const int tid = threadIdx.x;
+    const int c0 = blockIdx.y * KC;
+    const int kc = min(KC, k - c0);
+    for (int e = tid; e < m * KC; e += blockDim.x) {
+        const int j = e / KC, c = e % KC;
+        Vs[e] = (c < kc) ? V[(int64_t)(c0 + c) * ldv + j] : 0.0;
+    }
+    __syncthreads();
+    const bool divisible = (n % out_rows) == 0;
+    const int64_t n_next = divisible ? n / out_rows : 0;
+    const int64_t chunks = (n + 255) / 256;
+    auto stage = [&](int64_t ch, int buf) {
+        const int64_t row = ch * 256 + tid;
+        double* dst = xb + (size_t)buf * m * 256 + tid;
+        if (row < n) {
+            for (int j = 0; j < m; ++j) {
+                const unsigned sd = (unsigned)__cvta_generic_to_shared(dst + j * 256);
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sd), "l"(X + (int64_t)j * ldx + row)
+                             : "memory");
+            }
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    int buf = 0;
+    int64_t ch = blockIdx.x;
+    if (ch < chunks) stage(ch, 0);
+    for (; ch < chunks; ch += gridDim.x) {
+        const int64_t nx = ch + gridDim.x;
+        if (nx < chunks) {
+            stage(nx, buf ^ 1);
+            asm volatile("cp.async.wait_group 1;" ::: "memory");
+        } else {
+            asm volatile("cp.async.wait_group 0;" ::: "memory");
+        }
+        const int64_t i = ch * 256 + tid;
+        if (i < n) {
+            const double* xr = xb + (size_t)buf * m * 256 + tid;
+            double acc[KC];
+#pragma unroll
+            for (int c = 0; c < KC; ++c) acc[c] = 0.0;
+#pragma unroll 4
+            for (int j = 0; j < m; ++j) {
+                const double x = xr[j * 256];
+                const double* vj = Vs + j * KC;
+#pragma unroll
+                for (int c = 0; c < KC; ++c) acc[c] = fma(vj[c], x, acc[c]);
+            }
+            if (divisible) {
+                const int64_t b = i / out_rows, ii = i - b * out_rows;
+#pragma unroll
+                for (int c = 0; c < KC; ++c)
+                    if (c < kc) Y[(b + n_next * (c0 + c)) * ldy + ii] = acc[c];
+            } else {
+#pragma unroll
+                for (int c = 0; c < KC; ++c)
+                    if (c < kc) {
+                        const int64_t p = i + n * (c0 + c);
+                        const int64_t col = p / out_rows;
+                        Y[col * ldy + (p - col * out_rows)] = acc[c];
+                    }
+            }
+        }
+        buf ^= 1;
+    }
+}
+
 // K_TSMM on the FP64 tensor cores: each warp computes a 32-row x 8NT-column
 // block of X V with DMMA m8n8k4 (A fragments loaded straight from X — for a
 // fixed fragment column the 8 rows are one contiguous 64-byte run — B
