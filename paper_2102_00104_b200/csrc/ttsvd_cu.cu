@@ -1031,6 +1031,27 @@ int launch_tsmm_async(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int6
     return check_launch(ctx, "tsmm_async_kernel");
 }
 
+template <int KC>
+int launch_tsmm_async_wide(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t ldx, const double* V,
+                           int64_t ldv, int k, double* Y, int64_t out_rows, int64_t ldy) {
+    const size_t smem = ((size_t)((m * KC + 1) & ~1) + (size_t)2 * 32 * 256) * 8;
+    if (smem > (size_t)kSmemLimit) return -1;
+    static bool attr = false;
+    if (!attr) {
+        TT_CUDA(cudaFuncSetAttribute(tsmm_async_wide_kernel<KC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     kSmemLimit));
+        attr = true;
+    }
+    int per_sm = 1;
+    TT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tsmm_async_wide_kernel<KC>, 256, smem));
+    const int64_t chunks = (n + 255) / 256;
+    const int64_t blocks = std::min<int64_t>(chunks, (int64_t)std::max(1, per_sm) * ctx->num_sms);
+    const int ychunks = (k + KC - 1) / KC;
+    tsmm_async_wide_kernel<KC><<<dim3((unsigned)blocks, (unsigned)ychunks), 256, smem, ctx->stream>>>(
+        X, n, m, ldx, V, ldv, k, Y, out_rows, ldy);
+    return check_launch(ctx, "tsmm_async_wide_kernel");
+}
+
 template <int NT>
 int launch_tsmm_dmma(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t ldx, const double* V, int64_t ldv,
                      int k, double* Y, int64_t out_rows, int64_t ldy) {
@@ -1073,6 +1094,14 @@ int tsmm_device(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t ld
         rc = k <= 4 ? launch_tsmm_async<4>(ctx, X, n, m, ldx, V, ldv, k, Y, out_rows, ldy)
                     : (k <= 8 ? launch_tsmm_async<8>(ctx, X, n, m, ldx, V, ldv, k, Y, out_rows, ldy)
                               : launch_tsmm_async<16>(ctx, X, n, m, ldx, V, ldv, k, Y, out_rows, ldy));
+    } else if (tsmm_async && k > 1 && k <= 32 && m > 32 && n >= (int64_t)1 << 16 && !dmma &&
+               (rc = k <= 4 ? launch_tsmm_async_wide<4>(ctx, X, n, m, ldx, V, ldv, k, Y, out_rows, ldy)
+                            : (k <= 8 ? launch_tsmm_async_wide<8>(ctx, X, n, m, ldx, V, ldv, k, Y, out_rows, ldy)
+                                      : (k <= 16 || (size_t)m * 32 * 8 + 2 * 32 * 256 * 8 > (size_t)kSmemLimit
+                                             ? launch_tsmm_async_wide<16>(ctx, X, n, m, ldx, V, ldv, k, Y, out_rows, ldy)
+                                             : launch_tsmm_async_wide<32>(ctx, X, n, m, ldx, V, ldv, k, Y, out_rows,
+                                                                          ldy)))) != -1) {
+        // wider X: column blocks of the row chunk staged by cp.async
     } else if (k <= 1) rc = launch_tsmm<1>(ctx, X, n, m, ldx, V, ldv, k, Y, out_rows, ldy);
     else if (k <= 2) rc = launch_tsmm<2>(ctx, X, n, m, ldx, V, ldv, k, Y, out_rows, ldy);
     else if (k <= 4) rc = launch_tsmm<4>(ctx, X, n, m, ldx, V, ldv, k, Y, out_rows, ldy);

@@ -663,6 +663,99 @@ __global__ void __launch_bounds__(256) tsmm_async_kernel(const double* __restric
     }
 }
 
+// tsmm_async_kernel for wider X (m > 32): the row chunk is streamed in
+// blocks of 32 columns (one cp.async stage per (chunk, column block), double
+// buffered across the flattened sequence), the KC accumulators persist over a
+// chunk's blocks.  V (m x KC) stays in shared memory.
+template <int KC>
+__global__ void __launch_bounds__(256) tsmm_async_wide_kernel(const double* __restrict__ X, int64_t n, int m,
+                                                              int64_t ldx, const double* __restrict__ V, int64_t ldv,
+                                                              int k, double* __restrict__ Y, int64_t out_rows,
+                                                              int64_t ldy) {
+    extern __shared__ __align__(16) double tsm[];
+    constexpr int MB = 32;
+    double* Vs = tsm;                        // m x KC
+    double* xb = tsm + ((m * KC + 1) & ~1);  // 2 x MB x 256
+    const int tid = threadIdx.x;
+    const int c0 = blockIdx.y * KC;
+    const int kc = min(KC, k - c0);
+    for (int e = tid; e < m * KC; e += blockDim.x) {
+        const int j = e / KC, c = e % KC;
+        Vs[e] = (c < kc) ? V[(int64_t)(c0 + c) * ldv + j] : 0.0;
+    }
+    __syncthreads();
+    const bool divisible = (n % out_rows) == 0;
+    const int64_t n_next = divisible ? n / out_rows : 0;
+    const int64_t chunks = (n + 255) / 256;
+    const int nb = (m + MB - 1) / MB;
+    const int64_t my_chunks = (chunks - blockIdx.x + gridDim.x - 1) / gridDim.x;  // chunks of this CTA
+    const int64_t seq = blockIdx.x < chunks ? my_chunks * nb : 0;
+    auto stage = [&](int64_t sidx, int buf) {
+        const int64_t ch = blockIdx.x + (sidx / nb) * gridDim.x;
+        const int b = (int)(sidx % nb);
+        const int64_t row = ch * 256 + tid;
+        double* dst = xb + (size_t)buf * MB * 256 + tid;
+        const int jn = min(MB, m - b * MB);
+        if (row < n) {
+            for (int jj = 0; jj < jn; ++jj) {
+                const unsigned sd = (unsigned)__cvta_generic_to_shared(dst + jj * 256);
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sd),
+                             "l"(X + (int64_t)(b * MB + jj) * ldx + row)
+                             : "memory");
+            }
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    double acc[KC];
+#pragma unroll
+    for (int c = 0; c < KC; ++c) acc[c] = 0.0;
+    if (seq > 0) stage(0, 0);
+    for (int64_t sidx = 0; sidx < seq; ++sidx) {
+        const int buf = (int)(sidx & 1);
+        if (sidx + 1 < seq) {
+            stage(sidx + 1, buf ^ 1);
+            asm volatile("cp.async.wait_group 1;" ::: "memory");
+        } else {
+            asm volatile("cp.async.wait_group 0;" ::: "memory");
+        }
+        const int64_t ch = blockIdx.x + (sidx / nb) * gridDim.x;
+        const int b = (int)(sidx % nb);
+        const int64_t i = ch * 256 + tid;
+        const int jn = min(MB, m - b * MB);
+        const double* xr = xb + (size_t)buf * MB * 256 + tid;
+        const double* vb = Vs + (size_t)b * MB * KC;
+        if (i < n) {
+#pragma unroll 4
+            for (int jj = 0; jj < jn; ++jj) {
+                const double x = xr[jj * 256];
+                const double* vj = vb + jj * KC;
+#pragma unroll
+                for (int c = 0; c < KC; ++c) acc[c] = fma(vj[c], x, acc[c]);
+            }
+        }
+        if (b == nb - 1) {
+            if (i < n) {
+                if (divisible) {
+                    const int64_t bb = i / out_rows, ii = i - bb * out_rows;
+#pragma unroll
+                    for (int c = 0; c < KC; ++c)
+                        if (c < kc) Y[(bb + n_next * (c0 + c)) * ldy + ii] = acc[c];
+                } else {
+#pragma unroll
+                    for (int c = 0; c < KC; ++c)
+                        if (c < kc) {
+                            const int64_t p = i + n * (c0 + c);
+                            const int64_t col = p / out_rows;
+                            Y[col * ldy + (p - col * out_rows)] = acc[c];
+                        }
+                }
+            }
+#pragma unroll
+            for (int c = 0; c < KC; ++c) acc[c] = 0.0;
+        }
+    }
+}
+
 // K_TSMM on the FP64 tensor cores: each warp computes a 32-row x 8NT-column
 // block of X V with DMMA m8n8k4 (A fragments loaded straight from X — for a
 // fixed fragment column the 8 rows are one contiguous 64-byte run — B
