@@ -384,9 +384,13 @@ __global__ void __launch_bounds__(kT2Threads, 1) tsqr_t128_kernel(T2Args a) {
         const double* Xt = a.X + r0;  // column c at Xt + c * ld
         // panel 0 of the tile straight from the input
         if (warp == 0) la_fetch_rdiag(Rp, R, lane);
-        for (int e = tid; e < 32 * ROWS; e += kT2Threads) {
+        // (and panel 1's raw columns into the second buffer, for phase A of
+        // p = 0 from shared memory; all loads of both panels in flight at once)
+        const int c_first = npan > 1 ? 64 : 32;
+        for (int e = tid; e < c_first * ROWS; e += kT2Threads) {
             const int c = e / ROWS, i = e % ROWS;
-            Pb[c * Pld + i] = (i < rows && c < m) ? ld_hint(Xt + (int64_t)c * a.ld + i, pol_x) : 0.0;
+            Pb[(c >> 5) * 32 * Pld + (c & 31) * Pld + i] =
+                (i < rows && c < m) ? ld_hint(Xt + (int64_t)c * a.ld + i, pol_x) : 0.0;
         }
         if (warp == 0) cp_async_wait_all();
         __syncthreads();
@@ -419,8 +423,8 @@ __global__ void __launch_bounds__(kT2Threads, 1) tsqr_t128_kernel(T2Args a) {
             // phase A: panel p+1's columns, alone on the tensor pipes
             if (uw >= 0 && uw < 4) {
                 if (p == 0)
-                    t2_group<true, true, ROWS>(Xt, a.ld, rows, m, Pn, Pld, V, Tp, Rrow, c0, nxt + 8 * uw, 8 * uw, lane, pol_x,
-                                         pol_r);
+                    t2_group<false, true, ROWS, true>(Pn - (int64_t)nxt * Pld, Pld, rows, m, Pn, Pld, V, Tp, Rrow, c0,
+                                                      nxt + 8 * uw, 8 * uw, lane, pol_x, pol_r);
                 else
                     t2_group<false, true, ROWS, true>(Pn - (int64_t)nxt * Pld, Pld, rows, m, Pn, Pld, V, Tp, Rrow, c0,
                                                       nxt + 8 * uw, 8 * uw, lane, pol_x, pol_r);
