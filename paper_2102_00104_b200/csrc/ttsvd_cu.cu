@@ -70,6 +70,7 @@ struct ttsvd_cu_ctx {
     // grow-only device workspaces
     DevBuf ws_R, ws_R2, ws_P, ws_Scr, ws_G, ws_Gp, ws_A, ws_V, ws_Vacc, ws_U, ws_sigma, ws_flags, ws_work[2], ws_X, ws_send, ws_recv, ws_thick[2], ws_gs, ws_bd;
     DevBuf host_stage;  // pinned
+    DevBuf host_cores;  // pinned arena of the steps' V blocks (core_from_vt after the chain)
     cudaEvent_t ev[9] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
     // svd_work's bidiagonal path leaves the vectors for svd_vectors (the
     // driver knows the rank only after the sigmas): A holds the reflectors
@@ -1194,7 +1195,29 @@ int run_chain(ttsvd_cu_ctx* ctx, WorkView cur, const std::vector<int64_t>& dims,
     int64_t r = 1;
     int which = 0;
     Timer tm(ctx);
-    std::vector<double> sig, Vh;
+    std::vector<double> sig;
+    struct PendingCore {
+        int64_t i;
+        size_t off;
+        int64_t m, rnew, n_i, r;
+    };
+    std::vector<PendingCore> pending;
+    size_t core_off = 0;
+    // build the cores whose V blocks have landed in the arena (stream synchronised)
+    auto flush_cores = [&]() {
+        const double* base = as<double>(ctx->host_cores);
+        for (const PendingCore& pc : pending) {
+            const double* Vh = base + pc.off;
+            std::vector<double> core((size_t)(pc.rnew * pc.n_i * pc.r));
+            for (int64_t b = 0; b < pc.r; ++b)
+                for (int64_t x = 0; x < pc.n_i; ++x)
+                    for (int64_t a = 0; a < pc.rnew; ++a)
+                        core[a + pc.rnew * (x + pc.n_i * b)] = Vh[a * pc.m + (x + pc.n_i * b)];
+            out->cores[pc.i] = std::move(core);
+        }
+        pending.clear();
+        core_off = 0;
+    };
     for (int64_t i = d - 1; i >= 1; --i) {
         const int64_t n_i = dims[i];
         const int64_t m = n_i * r;
@@ -1236,14 +1259,21 @@ int run_chain(ttsvd_cu_ctx* ctx, WorkView cur, const std::vector<int64_t>& dims,
         tm.mark(7);
         TT_TRY(svd_vectors(ctx, rnew, d_sigma, d_V));
         tm.mark(8);
-        // core_from_vt (tt_svd.hpp:121-128) from the first rnew columns of V
-        Vh.resize((size_t)m * rnew);
-        TT_TRY(d2h(ctx, Vh.data(), d_V, (size_t)m * rnew));
-        std::vector<double> core((size_t)(rnew * n_i * r));
-        for (int64_t b = 0; b < r; ++b)
-            for (int64_t x = 0; x < n_i; ++x)
-                for (int64_t a = 0; a < rnew; ++a) core[a + rnew * (x + n_i * b)] = Vh[a * m + (x + n_i * b)];
-        out->cores[i] = std::move(core);
+        // core_from_vt (tt_svd.hpp:121-128) from the first rnew columns of V:
+        // an asynchronous D2H into the pinned core arena, the core is built
+        // after the chain (one host round trip per step instead of two)
+        {
+            const size_t need = (size_t)m * rnew;
+            if (core_off + need > ctx->host_cores.bytes / 8) {
+                TT_CUDA(cudaStreamSynchronize(ctx->stream));
+                flush_cores();
+                TT_TRY(ensure_host(ctx->host_cores, std::max<size_t>(need, (size_t)1 << 20) * 8 * 2));
+            }
+            TT_CUDA(cudaMemcpyAsync(as<double>(ctx->host_cores) + core_off, d_V, need * 8, cudaMemcpyDeviceToHost,
+                                    ctx->stream));
+            pending.push_back(PendingCore{i, core_off, m, rnew, n_i, r});
+            core_off += need;
+        }
         out->ranks[i] = rnew;
         // fused TSMM + reshape into the next step's padded layout
         const int64_t n_next = dims[i - 1];
@@ -1286,6 +1316,8 @@ int run_chain(ttsvd_cu_ctx* ctx, WorkView cur, const std::vector<int64_t>& dims,
             first[l] = v;
         }
     }
+    TT_CUDA(cudaStreamSynchronize(ctx->stream));
+    flush_cores();
     out->cores[0] = std::move(first);
     out->ranks[0] = 1;
     out->ranks[1] = r;
@@ -1335,6 +1367,7 @@ int ttsvd_cu_ctx_destroy(ttsvd_cu_ctx* ctx) {
                       &ctx->ws_work[1], &ctx->ws_X, &ctx->ws_send, &ctx->ws_recv, &ctx->ws_thick[0], &ctx->ws_thick[1], &ctx->ws_gs, &ctx->ws_bd})
         if (b->p) cudaFree(b->p);
     if (ctx->host_stage.p) cudaFreeHost(ctx->host_stage.p);
+    if (ctx->host_cores.p) cudaFreeHost(ctx->host_cores.p);
     for (auto& e : ctx->ev)
         if (e) cudaEventDestroy(e);
     delete ctx;
