@@ -156,11 +156,20 @@ __global__ void __launch_bounds__(NT, 1) gqr_kernel(GqrArgs a) {
     }
     for (int p = 0; p < M / 32; ++p) {
         const int64_t c0 = 32 * (int64_t)p;
-        // ---- stage my rows of the panel ----
-        for (int e = tid; e < 32 * ldy; e += NT) {
-            const int k = e / ldy, i = e - k * ldy;
-            Ys[e] = i < rows ? A[(c0 + k) * lda + r0 + i] : 0.0;
+        // ---- stage my rows of the panel (8-byte cp.async: all loads in flight) ----
+        for (int k = warp; k < 32; k += NT / 32) {
+            const double* src = A + (c0 + k) * lda + r0;
+            double* dst = Ys + k * ldy;
+            for (int i = lane; i < ldy; i += 32) {
+                if (i < rows) {
+                    const unsigned sd = (unsigned)__cvta_generic_to_shared(dst + i);
+                    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sd), "l"(src + i) : "memory");
+                } else {
+                    dst[i] = 0.0;
+                }
+            }
         }
+        asm volatile("cp.async.wait_all;" ::: "memory");
         __syncthreads();
         // ---- 32 reflectors, one grid barrier each ----
         GQR_PROF(0);
