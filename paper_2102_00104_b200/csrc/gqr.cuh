@@ -62,26 +62,9 @@ __device__ __forceinline__ double warp_reduce_scatter32(double (&v)[32], int lan
 }
 
 // sum over q = first, first + step, ... < G of base[q * qstride] (L2 reads,
-// data of other CTAs), four independent accumulators so the loads overlap; a
-// fixed association order, so every CTA computes bit-identical totals
-__device__ __forceinline__ double gqr_strided_sum(const double* base, int64_t qstride, int G, int first, int step) {
-    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-    int q = first;
-    for (; q + 3 * step < G; q += 4 * step) {
-        const double v0 = __ldcg(base + (int64_t)q * qstride), v1 = __ldcg(base + (int64_t)(q + step) * qstride);
-        const double v2 = __ldcg(base + (int64_t)(q + 2 * step) * qstride),
-                     v3 = __ldcg(base + (int64_t)(q + 3 * step) * qstride);
-        a0 += v0;
-        a1 += v1;
-        a2 += v2;
-        a3 += v3;
-    }
-    for (; q < G; q += step) a0 += __ldcg(base + (int64_t)q * qstride);
-    return (a0 + a1) + (a2 + a3);
-}
-
-// the same fixed-order sum with CH loads in flight per chunk (one L2 round
-// trip per chunk instead of one per four values)
+// data of other CTAs) in a fixed association order, so every CTA computes
+// bit-identical totals; CH loads in flight per chunk (one L2 round trip per
+// chunk)
 template <int CH>
 __device__ __forceinline__ double gqr_sum_inflight(const double* base, int64_t qstride, int G, int first, int step) {
     double s = 0.0;
