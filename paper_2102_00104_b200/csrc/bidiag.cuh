@@ -627,17 +627,46 @@ __global__ void __launch_bounds__(kBisThreads) bd_bisect_kernel(const double* d,
     const int j = m - 1 - i;  // ascending index
     double lo = 0.0, hi = bmax * (1.0 + 4.0 * DBL_EPSILON) + pivmin;
     const double floor_tol = 1e-18 * hi;
-    for (int it = 0; it < 40; ++it) {
+    // 16-way multisection; each shift's inertia from a twisted factorisation
+    // split in the middle (Sylvester): the even lane of a pair runs the
+    // forward recurrence over the first half, the odd lane the backward one
+    // over the second half, so a count costs N/2 dependent steps instead of N.
+    // #{eigenvalues < s} = #{d+_t < 0, t < h} + #{d-_t < 0, t > h} + [gamma_h < 0],
+    // gamma_h = d+_h + d-_h - (T_hh - s) (T_hh = 0 on the Golub-Kahan form).
+    const int h = N / 2;
+    const int pi = lane >> 1;
+    const bool fwd = (lane & 1) == 0;
+    for (int it = 0; it < 60; ++it) {
         if (hi - lo <= fmax(2.0 * DBL_EPSILON * hi, floor_tol)) break;
-        const double s = lo + (hi - lo) * (double)(lane + 1) * (1.0 / 33.0);
-        const int cnt = bd_sturm(b2, N, s, pivmin) - m;
-        const unsigned above = __ballot_sync(0xffffffffu, cnt > j);
-        const double s_f = __shfl_sync(0xffffffffu, s, above ? __ffs(above) - 1 : 31);
-        const double s_b = __shfl_sync(0xffffffffu, s, above ? max(__ffs(above) - 2, 0) : 31);
-        if (above) {
-            const int f = __ffs(above) - 1;
+        const double sft = lo + (hi - lo) * (double)(pi + 1) * (1.0 / 17.0);
+        double q = -sft;
+        if (fabs(q) < pivmin) q = -pivmin;
+        int c = 0;
+        // one instruction stream for both lanes (no divergence): step u uses
+        // b2[u-1] forward (d+_u from d+_{u-1}) and b2[N-1-u] backward (d-_{N-1-u}
+        // from d-_{N-u}); the backward half is one step shorter
+        for (int u = 1; u < h; ++u) {
+            c += q < 0.0;
+            q = -sft - b2[fwd ? u - 1 : N - 1 - u] * fast_rcp(q);
+            if (fabs(q) < pivmin) q = -pivmin;
+        }
+        if (fwd) {
+            c += q < 0.0;
+            q = -sft - b2[h - 1] * fast_rcp(q);
+            if (fabs(q) < pivmin) q = -pivmin;
+        }
+        const double qo = __shfl_xor_sync(0xffffffffu, q, 1);
+        const int co = __shfl_xor_sync(0xffffffffu, c, 1);
+        double gam = q + qo + sft;
+        if (fabs(gam) < pivmin) gam = -pivmin;
+        const int cnt = c + co + (gam < 0.0) - m;
+        const unsigned above = __ballot_sync(0xffffffffu, cnt > j) & 0x55555555u;  // one lane per shift
+        const int f2 = above ? (__ffs(above) - 1) >> 1 : 16;  // first shift index with count > j
+        const double s_f = __shfl_sync(0xffffffffu, sft, 2 * min(f2, 15));
+        const double s_b = __shfl_sync(0xffffffffu, sft, 2 * max(f2 - 1, 0));
+        if (f2 < 16) {
             hi = s_f;
-            if (f > 0) lo = s_b;
+            if (f2 > 0) lo = s_b;
         } else {
             lo = s_f;
         }
