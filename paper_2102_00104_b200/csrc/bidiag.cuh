@@ -961,8 +961,8 @@ __global__ void __launch_bounds__(kBack4Warps * 32) bd_back4_kernel(const double
 // and reductions instead of an L2 round trip (the register prefetch of
 // bd_back4_kernel looks one reflector ahead, less than the L2 latency).
 constexpr int kB4sChunk = 16;
-constexpr int kB4sWarps = 8;  // warps per CTA
-constexpr int kB4sVpw = 2;    // vectors per warp
+constexpr int kB4sWarps = 16;  // warps per CTA
+constexpr int kB4sVpw = 1;    // vectors per warp
 
 __device__ __forceinline__ void bd_cp_async16(void* smem_dst, const void* gsrc) {
     const unsigned sd = (unsigned)__cvta_generic_to_shared(smem_dst);
