@@ -408,7 +408,9 @@ int tsqr_ws_levels(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t
     int64_t rows = n, sld = ld;
     int flip = 0;
     for (;;) {
-        int64_t S = std::min<int64_t>(rows / 128, max_streams);  // >= 4 tiles per stream
+        // >= 2 tiles per stream (the levels are latency chains: config 2
+        // step 1's levels 0.23 ms at 4 tiles, 0.20 at 2, 0.25 at 1)
+        int64_t S = std::min<int64_t>(rows / 64, max_streams);
         if (S < 1) S = 1;
         if (S > 1) {
             TT_TRY(ensure(ctx->ws_R, (size_t)S * m * m * 8));
