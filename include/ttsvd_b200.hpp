@@ -490,7 +490,7 @@ inline TensorTrain tt_svd_tsqr(const DenseTensor& X, TruncationSpec spec, const 
     const index_t d = static_cast<index_t>(X.dims().size());
     if (d < 2) throw DegenerateDimension("tt_svd_tsqr: requires d >= 2");
     ttsvd_cu_tt* h = nullptr;
-    const index_t rmax = spec.r_max == std::numeric_limits<index_t>::max() ? 0 : spec.r_max;
+    const index_t rmax = spec.r_max;
     b200::check(ttsvd_cu_tt_svd_host(b200::context(), X.data(), X.dims().data(), d, X.leading_stride(), rmax,
                                      spec.eps, &h));
     return b200::collect(h, X.dims());
@@ -500,7 +500,7 @@ inline TensorTrain tt_svd_tsqr(const DenseTensor& X, TruncationSpec spec, const 
 inline TensorTrain tt_svd_tsqr(const double* X_device, const std::vector<index_t>& dims, index_t ld,
                                TruncationSpec spec) {
     ttsvd_cu_tt* h = nullptr;
-    const index_t rmax = spec.r_max == std::numeric_limits<index_t>::max() ? 0 : spec.r_max;
+    const index_t rmax = spec.r_max;
     b200::check(ttsvd_cu_tt_svd(b200::context(), X_device, dims.data(), static_cast<index_t>(dims.size()), ld, rmax,
                                 spec.eps, &h));
     return b200::collect(h, dims);
@@ -518,7 +518,7 @@ inline std::pair<index_t, index_t> choose_combined_dims(const std::vector<index_
                                                         const ThickBoundsParams& params,
                                                         index_t r_max = std::numeric_limits<index_t>::max()) {
     index_t k = 0, m = 0;
-    const index_t rmax = r_max == std::numeric_limits<index_t>::max() ? 0 : r_max;
+    const index_t rmax = r_max;
     b200::check(ttsvd_cu_choose_combined_dims(dims.data(), static_cast<index_t>(dims.size()), params.m_min,
                                               params.f1_min, params.r_tilde.empty() ? nullptr : params.r_tilde.data(),
                                               static_cast<index_t>(params.r_tilde.size()), rmax, &k, &m));
@@ -531,7 +531,7 @@ inline TensorTrain tt_svd_thick_bounds(const DenseTensor& X, TruncationSpec spec
                                        const ExecContext& = {}) {
     const index_t d = static_cast<index_t>(X.dims().size());
     if (d < 2) throw DegenerateDimension("tt_svd_thick_bounds: requires d >= 2");
-    const index_t rmax = spec.r_max == std::numeric_limits<index_t>::max() ? 0 : spec.r_max;
+    const index_t rmax = spec.r_max;
     const index_t cols = X.dims()[static_cast<std::size_t>(d - 1)];
     b200::DeviceBuffer dx(static_cast<std::size_t>(X.leading_stride() * cols));
     dx.upload(X.data(), dx.size());
@@ -557,7 +557,7 @@ inline TensorTrain tt_svd_distributed(const std::vector<DenseTensor>& slabs, Tru
         ptrs.push_back(bufs.back().get());
     }
     const index_t P = static_cast<index_t>(slabs.size());
-    const index_t rmax = spec.r_max == std::numeric_limits<index_t>::max() ? 0 : spec.r_max;
+    const index_t rmax = spec.r_max;
     ttsvd_cu_tt* h = nullptr;
     b200::check(ttsvd_cu_tt_svd_distributed(b200::context(), ptrs.data(), P, 0, P, ld.data(),
                                             static_cast<index_t>(ld.size()), slabs.front().leading_stride(), rmax,

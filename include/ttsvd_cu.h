@@ -129,13 +129,15 @@ int ttsvd_cu_tsmm_reshape(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int64_t
 
 /* ---- drivers ----------------------------------------------------------- */
 /* tt_svd.hpp:281 tt_svd_tsqr() (Alg. 2): X is the device tensor in the padded
- * layout (ldx = padded_stride(N/n_d) or larger).  r_max <= 0 means uncapped. */
+ * layout (ldx = padded_stride(N/n_d) or larger).  r_max is the reference's
+ * TruncationSpec::r_max: INT64_MAX is uncapped, r_max < 1 clamps every rank to 1
+ * (select_rank, small_svd.hpp:49-63). */
 int ttsvd_cu_tt_svd(ttsvd_cu_ctx* ctx, const double* X, const int64_t* dims, int64_t d, int64_t ldx, int64_t r_max,
                     double eps, ttsvd_cu_tt** out);
 /* tt_svd.hpp:316-330 choose_combined_dims() with ThickBoundsParams
  * (tt_svd.hpp:292-310): k trailing modes merged into one of extent m.
- * r_tilde may be NULL (n_r_tilde = 0): the estimates default to r_max.
- * r_max <= 0 means uncapped. */
+ * r_tilde may be NULL (n_r_tilde = 0): the estimates default to r_max
+ * (INT64_MAX: uncapped). */
 int ttsvd_cu_choose_combined_dims(const int64_t* dims, int64_t d, int64_t m_min, double f1_min, const int64_t* r_tilde,
                                   int64_t n_r_tilde, int64_t r_max, int64_t* k_out, int64_t* m_out);
 /* tt_svd.hpp:338 tt_svd_thick_bounds() (Alg. 3): merge the k trailing modes,

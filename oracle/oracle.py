@@ -104,6 +104,8 @@ class Oracle:
             f("tsmm_reshape").argtypes = [dptr, i64, i64, i64, dptr, i64, i64, dptr, i64, i64, i64, C.c_int]
             f("tt_svd_tsqr").argtypes = [dptr, i64ptr, i64, i64, i64, C.c_double, C.c_int, i64ptr, dptr, i64,
                                          i64ptr, C.POINTER(Step)]
+            f("tt_svd_tsqr_sigma").argtypes = [dptr, i64ptr, i64, i64, i64, C.c_double, C.c_int, i64ptr, dptr, i64,
+                                               i64ptr, dptr, i64, i64ptr]
             f("tt_svd_distributed").argtypes = [C.POINTER(dptr), i64, i64ptr, i64, i64, i64, C.c_double, C.c_int,
                                                 i64ptr, dptr, i64, i64ptr]
             f("set_budget").argtypes = [i64]
@@ -178,20 +180,27 @@ class Oracle:
         self._check(self._f("derive_delta")(norm, eps, d, C.byref(out)), "derive_delta")
         return out.value
 
-    def tsmm_reshape(self, X: np.ndarray, V: np.ndarray, out_rows: int, out_cols: int) -> np.ndarray:
-        """Returns the padded (ld x out_cols) output buffer, Fortran order."""
-        X = np.asfortranarray(X, dtype=np.float64)
+    def tsmm_reshape(self, X: np.ndarray, V: np.ndarray, out_rows: int, out_cols: int, workers: int = 1,
+                     n: int | None = None, ld: int | None = None) -> np.ndarray:
+        """Returns the padded (ld x out_cols) output buffer, Fortran order.
+        With n and ld, X is a padded (ld x m) Fortran buffer holding n rows."""
         V = np.asfortranarray(V, dtype=np.float64)
-        n, m = X.shape
+        if ld is None:
+            X = np.asfortranarray(X, dtype=np.float64)
+            n, m = X.shape
+            ld = max(n, 1)
+        else:
+            assert X.flags.f_contiguous and X.shape[0] == ld
+            m = X.shape[1]
         k = V.shape[1]
         ldy = padded_stride(out_rows)
         Y = np.zeros((ldy, out_cols), order="F")
         if self.kind == "restated":
-            rc = self._f("tsmm_reshape")(_p(X), n, m, max(n, 1), _p(V), k, max(V.shape[0], 1), _p(Y), out_rows,
+            rc = self._f("tsmm_reshape")(_p(X), n, m, ld, _p(V), k, max(V.shape[0], 1), _p(Y), out_rows,
                                          out_cols, ldy)
         else:
-            rc = self._f("tsmm_reshape")(_p(X), n, m, max(n, 1), _p(V), k, max(V.shape[0], 1), _p(Y), out_rows,
-                                         out_cols, ldy, 1)
+            rc = self._f("tsmm_reshape")(_p(X), n, m, ld, _p(V), k, max(V.shape[0], 1), _p(Y), out_rows,
+                                         out_cols, ldy, workers)
         self._check(rc, "tsmm_reshape")
         return Y
 
@@ -233,6 +242,36 @@ class Oracle:
                 sig_list.append(sig[off:off + nsig].copy())
                 off += nsig
         return ranks.tolist(), core_list, step_list, sig_list
+
+    def tt_svd_tsqr_sigma(self, X: np.ndarray, dims, ld: int, r_max: int, eps: float = 0.0, workers: int = 1):
+        """The reference's Alg. 2 run step by step from its own functions
+        (ref_shim.cpp ref_tt_svd_tsqr_sigma) with `workers` host threads:
+        (ranks, cores, sigmas per step).  Reference library only."""
+        assert self.kind == "reference"
+        dims = np.ascontiguousarray(dims, dtype=np.int64)
+        d = len(dims)
+        ranks = np.zeros(d + 1, dtype=np.int64)
+        need = np.zeros(1, dtype=np.int64)
+        nsig = np.zeros(max(d - 1, 1), dtype=np.int64)
+        total = int(np.prod(dims))
+        cap = max(1, min(total, 1 << 22))
+        sig_cap = 1 << 20
+        while True:
+            cores = np.zeros(cap)
+            sig = np.zeros(sig_cap)
+            rc = self._f("tt_svd_tsqr_sigma")(_p(X), _pi(dims), d, ld, r_max, eps, workers, _pi(ranks), _p(cores),
+                                              cap, _pi(need), _p(sig), sig_cap, _pi(nsig))
+            if rc == 11:
+                cap = max(cap, int(need[0]))
+                sig_cap = max(sig_cap, int(nsig.sum()))
+                continue
+            self._check(rc, "tt_svd_tsqr_sigma")
+            break
+        sig_list, off = [], 0
+        for k in nsig[: d - 1]:
+            sig_list.append(sig[off:off + int(k)].copy())
+            off += int(k)
+        return ranks.tolist(), split_cores(cores, dims, ranks), sig_list
 
     def tt_svd_distributed(self, slabs: list[np.ndarray], ldims, ld: int, r_max: int, eps: float = 0.0,
                            workers: int = 1):

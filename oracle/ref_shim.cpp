@@ -169,6 +169,53 @@ int ref_tt_svd_tsqr(const double* X, const int64_t* dims, int64_t d, int64_t ldx
     } catch (const std::exception& e) { return code_of(e); }
 }
 
+// The reference's own Alg. 2 steps (tt_svd.hpp:159-199), called one by one
+// from this test driver so that every step's singular values can be recorded
+// (tt_svd_tsqr does not expose them): detail::svd_of_work, derive_delta,
+// detail::choose_rank, detail::core_from_vt, tsmm_reshape, all with
+// ctx.threads workers.  tests/test_oracle_pin.py pins it bitwise to
+// tt_svd_tsqr.  sigmas: the concatenated sigma of every step (nsig each,
+// in execution order; cap doubles), nsig_out: per step.
+int ref_tt_svd_tsqr_sigma(const double* X, const int64_t* dims, int64_t d, int64_t ldx, int64_t r_max, double eps,
+                          int workers, int64_t* ranks, double* cores, int64_t cap, int64_t* needed, double* sigmas,
+                          int64_t sig_cap, int64_t* nsig_out) {
+    try {
+        if (d < 2) throw DegenerateDimension("tt_svd_tsqr: requires d >= 2");
+        DenseTensor t = tensor_from(X, dims, d, ldx);
+        ExecContext ctx;
+        ctx.threads = workers;
+        ctx.validate_reflectors = false;
+        TruncationSpec spec = spec_of(r_max, eps);
+        std::vector<index_t> dv(dims, dims + d);
+        std::vector<TTCore> cs(static_cast<std::size_t>(d));
+        PaddedMatrix owned;
+        ConstMatrixView cur{t.data(), t.rows(), dims[d - 1], t.leading_stride()};
+        index_t r = 1;
+        int64_t soff = 0;
+        for (index_t i = d - 1; i >= 1; --i) {
+            const index_t n_i = dv[static_cast<std::size_t>(i)];
+            detail::WorkSVD s = detail::svd_of_work(cur, ctx, nullptr);
+            if (!spec.has_delta()) spec.delta = derive_delta(sigma_norm(s.sigma), spec.eps, d);
+            const index_t rnew = detail::choose_rank(s, spec, cur.rows);
+            nsig_out[d - 1 - i] = s.nsig;
+            if (soff + s.nsig <= sig_cap) std::memcpy(sigmas + soff, s.sigma.data(), s.nsig * 8);
+            soff += s.nsig;
+            cs[static_cast<std::size_t>(i)] = detail::core_from_vt(s, rnew, n_i, r);
+            const index_t n_next = dv[static_cast<std::size_t>(i - 1)];
+            owned = tsmm_reshape(cur, s.v_view(rnew), cur.rows / n_next, n_next * rnew, ctx.threads, nullptr);
+            cur = owned.view();
+            r = rnew;
+        }
+        TTCore first(1, dv[0], r);
+        for (index_t l = 0; l < dv[0] * r; ++l) first.data[static_cast<std::size_t>(l)] = cur(l % cur.rows, l / cur.rows);
+        cs[0] = std::move(first);
+        TensorTrain tt;
+        tt.cores = std::move(cs);
+        if (soff > sig_cap) return 11;
+        return export_tt(tt, ranks, cores, cap, needed);
+    } catch (const std::exception& e) { return code_of(e); }
+}
+
 // tt_svd.hpp:316-330 and tt_svd.hpp:338 (Alg. 3)
 int ref_choose_combined_dims(const int64_t* dims, int64_t d, int64_t m_min, double f1_min, const int64_t* r_tilde,
                              int64_t n_r_tilde, int64_t r_max, int64_t* k_out, int64_t* m_out) {

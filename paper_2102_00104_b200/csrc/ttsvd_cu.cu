@@ -13,7 +13,9 @@
 #include <cstdio>
 #include <cstring>
 #include <cstdlib>
+#include <map>
 #include <string>
+#include <tuple>
 #include <vector>
 
 #include "../../include/ttsvd_cu.h"
@@ -69,6 +71,7 @@ struct ttsvd_cu_ctx {
     bool timing = false;
     // grow-only device workspaces
     DevBuf ws_R, ws_R2, ws_P, ws_Scr, ws_G, ws_Gp, ws_A, ws_V, ws_Vacc, ws_U, ws_sigma, ws_flags, ws_work[2], ws_X, ws_send, ws_recv, ws_thick[2], ws_gs, ws_bd;
+    std::vector<DevBuf> ws_slab;  // tt_svd_distributed: two ping-pong work buffers per local slab
     DevBuf host_stage;  // pinned
     DevBuf host_cores;  // pinned arena of the steps' V blocks (core_from_vt after the chain)
     cudaEvent_t ev[9] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
@@ -78,6 +81,10 @@ struct ttsvd_cu_ctx {
     const double* bd_A = nullptr;
     int bd_n = 0, bd_m = 0;
     int last_kernel = 0;  // TTSVD_K_* of the last tsqr_device main sweep (ev[5], ev[6] bracket it when timing)
+    // kernel attributes and occupancies are properties of the device, so they
+    // are cached per context (one device each), never process-wide
+    std::map<const void*, int> smem_attr;
+    std::map<std::tuple<const void*, int, size_t>, int> occ;
 };
 
 struct ttsvd_cu_tt {
@@ -130,6 +137,40 @@ int check_launch(ttsvd_cu_ctx* ctx, const char* what) {
     return TTSVD_OK;
 }
 
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize [, NonPortableClusterSize])
+// for `fn` on the context's device, once per (context, kernel) and size.
+int kattr(ttsvd_cu_ctx* ctx, const void* fn, int smem_bytes, bool nonportable_cluster = false) {
+    auto it = ctx->smem_attr.find(fn);
+    if (it != ctx->smem_attr.end() && it->second >= smem_bytes) return TTSVD_OK;
+    TT_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes));
+    if (nonportable_cluster) TT_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    ctx->smem_attr[fn] = smem_bytes;
+    return TTSVD_OK;
+}
+
+// co-resident CTAs per SM of `fn` at (threads, dynamic smem) on the context's device
+int koccupancy(ttsvd_cu_ctx* ctx, const void* fn, int threads, size_t smem, int* per_sm) {
+    const auto key = std::make_tuple(fn, threads, smem);
+    auto it = ctx->occ.find(key);
+    if (it != ctx->occ.end()) {
+        *per_sm = it->second;
+        return TTSVD_OK;
+    }
+    int v = 0;
+    TT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, fn, threads, smem));
+    ctx->occ[key] = v;
+    *per_sm = v;
+    return TTSVD_OK;
+}
+
+// static shared memory of `fn`
+int kstatic_smem(const void* fn, int* bytes) {
+    cudaFuncAttributes fa;
+    TT_CUDA(cudaFuncGetAttributes(&fa, fn));
+    *bytes = (int)fa.sharedSizeBytes;
+    return TTSVD_OK;
+}
+
 int set_device(ttsvd_cu_ctx* ctx) {
     if (!ctx) return fail(TTSVD_ERR_INVALID, "null context");
     TT_CUDA(cudaSetDevice(ctx->device));
@@ -138,6 +179,7 @@ int set_device(ttsvd_cu_ctx* ctx) {
 
 constexpr int kTsqrThreads = 256;
 constexpr int kSmemLimit = 227 * 1024;
+constexpr int kTsmmSmem = 200 * 1024;  // V block of tsmm_kernel (m x KC doubles)
 
 // ---------------------------------------------------------------- K_TSQR ----
 struct TsqrPlan {
@@ -160,12 +202,7 @@ TsqrPlan tsqr_plan(int m) {
 }
 
 int launch_tsqr_kernel(ttsvd_cu_ctx* ctx, const TsqrArgs& a, int grid, size_t smem) {
-    static bool attr_set = false;
-    if (!attr_set) {
-        TT_CUDA(cudaFuncSetAttribute(tsqr_tile_kernel<kTsqrThreads>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     kSmemLimit));
-        attr_set = true;
-    }
+    TT_TRY(kattr(ctx, (const void*)tsqr_tile_kernel<kTsqrThreads>, kSmemLimit));
     tsqr_tile_kernel<kTsqrThreads><<<grid, kTsqrThreads, smem, ctx->stream>>>(a);
     return check_launch(ctx, "tsqr_tile_kernel");
 }
@@ -173,20 +210,14 @@ int launch_tsqr_kernel(ttsvd_cu_ctx* ctx, const TsqrArgs& a, int grid, size_t sm
 // ---- blocked DMMA path (m > 32) ----
 constexpr int kSmallM = 32;
 
-int set_la_attr() {
-    static int done = 0;
-    if (!done) {
-        cudaFuncAttributes fa;
-        TT_CUDA(cudaFuncGetAttributes(&fa, tsqr_la_kernel));
-        TT_CUDA(cudaFuncSetAttribute(tsqr_la_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     kSmemLimit - (int)fa.sharedSizeBytes));
-        done = 1;
-    }
-    return TTSVD_OK;
+int set_la_attr(ttsvd_cu_ctx* ctx) {
+    int ss = 0;
+    TT_TRY(kstatic_smem((const void*)tsqr_la_kernel, &ss));
+    return kattr(ctx, (const void*)tsqr_la_kernel, kSmemLimit - ss);
 }
 
 int launch_blk(ttsvd_cu_ctx* ctx, const BlkArgs& a, int grid) {
-    TT_TRY(set_la_attr());
+    TT_TRY(set_la_attr(ctx));
     tsqr_la_kernel<<<grid, kLaThreads, la_smem_bytes(a.M), ctx->stream>>>(a);
     return check_launch(ctx, "tsqr_la_kernel");
 }
@@ -280,45 +311,23 @@ int merge_tree(ttsvd_cu_ctx* ctx, double* parts, int64_t count, int m, double* R
 int gqr_device(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t ld, double* R) {
     const int M = (m + 31) / 32 * 32;
     if (n < M || n > (int64_t)kGqrMaxRows * ctx->num_sms) return -1;
-    // a cooperative grid of up to one CTA per SM.  TTSVD_GQR=cluster runs
-    // short steps (n <= 16 x 512) as one cluster of <= 16 CTAs with cluster
-    // barriers instead — measured slower on config 2 step 4 (3.77 vs 3.37 ms:
-    // 8.5k vs 9.1k cycles per reflector, but half the SMs for the blocked
-    // updates), kept for A/B timing
-    static const char* gsel = std::getenv("TTSVD_GQR");
-    const bool cl = n <= (int64_t)kGqrCluster * kGqrMaxRows && gsel && std::string(gsel) == "cluster";
-    // target rows per CTA (more CTAs: the blocked updates spread wider; config 2
-    // step 4, 4096 x 512: 3.30 ms at 128 rows, 3.07 at 64); TTSVD_GQR_ROWS overrides
-    static const int64_t gq_rows = std::getenv("TTSVD_GQR_ROWS") ? std::atoll(std::getenv("TTSVD_GQR_ROWS")) : 64;
-    int64_t Gq = std::max<int64_t>(1, std::min<int64_t>(cl ? kGqrCluster : ctx->num_sms, n / gq_rows));
-    if (cl) {  // a power-of-two cluster
-        int64_t g = 1;
-        while (2 * g <= Gq) g *= 2;
-        Gq = g;
-        while ((n + Gq - 1) / Gq > kGqrMaxRows) Gq *= 2;
-    }
+    // a cooperative grid of up to one CTA per SM, 64 target rows per CTA (more
+    // CTAs: the blocked updates spread wider; config 2 step 4, 4096 x 512:
+    // 3.30 ms at 128 rows, 3.07 at 64)
+    int64_t Gq = std::max<int64_t>(1, std::min<int64_t>(ctx->num_sms, n / 64));
     while ((n + Gq - 1) / Gq > kGqrMaxRows) ++Gq;
     const int rows_max = (int)((n + Gq - 1) / Gq);
     // more than 256 rows per CTA: 512 threads (one row each; the blocked
     // updates gain more than the reflector chain loses — config 2 step 3
     // 6.31 -> 5.74 ms); otherwise 256 (steps with <= 256 rows per CTA are
     // slower with 512)
-    const int gnt = (rows_max > 256 && !cl) ? 512 : 256;
+    const int gnt = rows_max > 256 ? 512 : 256;
     const size_t smem = gqr_smem_bytes(rows_max, gnt);
-    static bool gattr = false;
-    if (!gattr) {
-        TT_CUDA(cudaFuncSetAttribute(gqr_kernel<false, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit));
-        TT_CUDA(cudaFuncSetAttribute(gqr_kernel<false, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit));
-        TT_CUDA(cudaFuncSetAttribute(gqr_kernel<true, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit));
-        TT_CUDA(cudaFuncSetAttribute(gqr_kernel<true, 256>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-        gattr = true;
-    }
-    if (!cl) {
-        int per_sm = 0;
-        TT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gnt == 512 ? gqr_kernel<false, 512> : gqr_kernel<false, 256>,
-                                                              gnt, smem));
-        if (per_sm < 1 || Gq > (int64_t)per_sm * ctx->num_sms) return -1;
-    }
+    const void* gfn = gnt == 512 ? (const void*)gqr_kernel<false, 512> : (const void*)gqr_kernel<false, 256>;
+    TT_TRY(kattr(ctx, gfn, kSmemLimit));
+    int per_sm = 0;
+    TT_TRY(koccupancy(ctx, gfn, gnt, smem, &per_sm));
+    if (per_sm < 1 || Gq > (int64_t)per_sm * ctx->num_sms) return -1;
     TT_TRY(ensure(ctx->ws_G, (size_t)n * M * 8));
     const size_t np = (size_t)2 * Gq * 33 + (size_t)Gq * 1024 + (size_t)Gq * 32 * M;
     TT_TRY(ensure(ctx->ws_Gp, (np + 64 + (size_t)32 * M + 1024) * 8));
@@ -329,41 +338,12 @@ int gqr_device(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t ld,
         if (M > m) TT_CUDA(cudaMemsetAsync(Aw + (size_t)n * m, 0, (size_t)n * (M - m) * 8, ctx->stream));
     }
     double* pp = as<double>(ctx->ws_Gp);
-    static const bool prof = std::getenv("TTSVD_PROF_GQR") != nullptr;
-    long long* dprof = nullptr;
-    if (prof) {
-        TT_CUDA(cudaMalloc(&dprof, 8 * sizeof(long long)));
-        TT_CUDA(cudaMemset(dprof, 0, 8 * sizeof(long long)));
-    }
-    GqrArgs ga{Aw, n, n, m, M, pp, pp + np, pp + np + 64, pp + np + 64 + (size_t)32 * M, dprof};
-    if (cl) {
-        cudaLaunchConfig_t cfg = {};
-        cfg.gridDim = dim3((unsigned)Gq);
-        cfg.blockDim = dim3(kGqrThreads);
-        cfg.dynamicSmemBytes = smem;
-        cfg.stream = ctx->stream;
-        cudaLaunchAttribute at[1];
-        at[0].id = cudaLaunchAttributeClusterDimension;
-        at[0].val.clusterDim.x = (unsigned)Gq;
-        at[0].val.clusterDim.y = 1;
-        at[0].val.clusterDim.z = 1;
-        cfg.attrs = at;
-        cfg.numAttrs = 1;
-        TT_CUDA(cudaLaunchKernelEx(&cfg, gqr_kernel<true, 256>, ga));
-    } else {
+    GqrArgs ga{Aw, n, n, m, M, pp, pp + np, pp + np + 64, pp + np + 64 + (size_t)32 * M, nullptr};
+    {
         void* args[] = {&ga};
-        TT_CUDA(cudaLaunchCooperativeKernel(gnt == 512 ? (const void*)gqr_kernel<false, 512> : (const void*)gqr_kernel<false, 256>,
-                                            dim3((unsigned)Gq), dim3(gnt), args, smem, ctx->stream));
+        TT_CUDA(cudaLaunchCooperativeKernel(gfn, dim3((unsigned)Gq), dim3(gnt), args, smem, ctx->stream));
     }
     TT_TRY(check_launch(ctx, "gqr_kernel"));
-    if (prof) {
-        long long h[8];
-        TT_CUDA(cudaMemcpy(h, dprof, sizeof(h), cudaMemcpyDeviceToHost));
-        cudaFree(dprof);
-        std::fprintf(stderr, "[gqr prof] n=%lld m=%d G=%lld kcyc: stage %.0f reflectors %.0f (%.2f per refl) S+T %.0f Wpart %.0f Wred %.0f update %.0f | per refl: partials %.2f, fence+sync+sums %.2f\n",
-                     (long long)n, m, (long long)Gq, h[0] / 1e3, h[1] / 1e3, h[1] / 1e3 / M, h[2] / 1e3, h[3] / 1e3,
-                     h[4] / 1e3, h[5] / 1e3, h[6] / 1e3 / M, h[7] / 1e3 / M);
-    }
     gqr_extract_kernel<<<std::max(1, std::min(1024, (m * m + 255) / 256)), 256, 0, ctx->stream>>>(Aw, n, m, R);
     return check_launch(ctx, "gqr_extract_kernel");
 }
@@ -395,13 +375,11 @@ inline void kmark(ttsvd_cu_ctx* ctx, int i, int kernel) {
 // stream is left.
 template <int SW>
 int tsqr_ws_levels(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t ld, double* R, bool mark) {
-    static int per_sm = -1;
+    int per_sm = 0;
     const size_t smem = ws_smem_bytes<SW>();
-    if (per_sm < 0) {
-        TT_CUDA(cudaFuncSetAttribute(tsqr_ws_kernel<SW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        TT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tsqr_ws_kernel<SW>, kWsThreads, smem));
-        per_sm = std::max(1, per_sm);
-    }
+    TT_TRY(kattr(ctx, (const void*)tsqr_ws_kernel<SW>, (int)smem));
+    TT_TRY(koccupancy(ctx, (const void*)tsqr_ws_kernel<SW>, kWsThreads, smem, &per_sm));
+    per_sm = std::max(1, per_sm);
     constexpr int per_cta = (kWsThreads / 32) * (32 / SW);
     const int64_t max_streams = (int64_t)per_sm * ctx->num_sms * per_cta;
     const double* src = X;
@@ -409,8 +387,9 @@ int tsqr_ws_levels(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t
     int flip = 0;
     for (;;) {
         // >= 2 tiles per stream (the levels are latency chains: config 2
-        // step 1's levels 0.23 ms at 4 tiles, 0.20 at 2, 0.25 at 1)
-        int64_t S = std::min<int64_t>(rows / 64, max_streams);
+        // step 1's levels 0.23 ms at 4 tiles, 0.20 at 2, 0.25 at 1), and
+        // >= 4 m rows per stream so that every level cuts the rows by >= 4x
+        int64_t S = std::min<int64_t>(rows / std::max<int64_t>(64, 4 * (int64_t)m), max_streams);
         if (S < 1) S = 1;
         if (S > 1) {
             TT_TRY(ensure(ctx->ws_R, (size_t)S * m * m * 8));
@@ -445,11 +424,9 @@ int tsqr_pt_levels(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int64_t ld, do
     // rows per fold (x (U x M) and R stay in registers); measured on B200:
     // U = 4 keeps two CTAs per SM for m = 5, 6, U = 8 wins at m = 7, 8
     constexpr int U = (M == 5 || M == 6) ? 4 : 8;
-    static int per_sm = -1;
-    if (per_sm < 0) {
-        TT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tsqr_pt_kernel<M, U>, kPtThreads, 0));
-        per_sm = std::max(1, per_sm);
-    }
+    int per_sm = 0;
+    TT_TRY(koccupancy(ctx, (const void*)tsqr_pt_kernel<M, U>, kPtThreads, 0, &per_sm));
+    per_sm = std::max(1, per_sm);
     const int64_t max_t = (int64_t)per_sm * ctx->num_sms * kPtThreads;
     const double* src = X;
     int64_t rows = n, sld = ld;
@@ -494,11 +471,9 @@ int tsqr_pt_device(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t
 // padded width), levels of stacked factors as tsqr_pt_levels.
 template <int M, int P, int U>
 int tsqr_gs_levels(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t ld, double* R) {
-    static int per_sm = -1;
-    if (per_sm < 0) {
-        TT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tsqr_gs_kernel<M, P, U>, kPtThreads, 0));
-        per_sm = std::max(1, per_sm);
-    }
+    int per_sm = 0;
+    TT_TRY(koccupancy(ctx, (const void*)tsqr_gs_kernel<M, P, U>, kPtThreads, 0, &per_sm));
+    per_sm = std::max(1, per_sm);
     const int64_t max_t = (int64_t)per_sm * ctx->num_sms * (kPtThreads / P);
     int64_t T = std::max<int64_t>(1, std::min<int64_t>(n / 64, max_t));
     // the stacked factors get their own buffer (the warp-stream tail uses
@@ -533,99 +508,44 @@ int tsqr_device(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t ld
         const int64_t RS = blk_rsize(M);
         // Short-fat (n <= 256 M, n <= 512 rows per SM): one cooperative grid
         // factorises the whole matrix (gqr.cuh), no merge tree.
-        if (!R_init && n >= M && n <= (int64_t)256 * M && !(std::getenv("TTSVD_TSQR") && std::string(std::getenv("TTSVD_TSQR")) == "t128")) {
+        if (!R_init && n >= M && n <= (int64_t)256 * M) {
             kmark(ctx, 0, TTSVD_K_GQR);
             const int rc = gqr_device(ctx, X, n, m, ld, R);
             kmark(ctx, 1, TTSVD_K_GQR);
             if (rc != -1) return rc;
             ctx->last_kernel = 0;
         }
-        // 128-row tiles, one CTA per SM, when every CTA gets >= 4 tiles (the
-        // 148 factors are merged by one cooperative QR of their stack)
-        static const char* tsel = std::getenv("TTSVD_TSQR");  // diagnostics: "t128", "la"
-        const bool force_t128 = tsel && std::string(tsel) == "t128";
-        const bool want_t128 = tsel ? force_t128 : true;
-        // 256-row tiles (8 panel + 8 update warps of a 512-thread CTA) when
-        // every CTA gets >= 4 of them: the reflector chain per row is half the
-        // 128-row tile's (config 2 step 2 sweep: 13.7 ms at 128 rows / 384
-        // threads, 12.35 at 192 / 384, 11.8 at 256 / 512; 12.8 at 320 / 512).
-        // TTSVD_T2ROWS=128|192|256|320 selects one for A/B timing.
-        static const char* t2sel = std::getenv("TTSVD_T2ROWS");
-        const int t2want = t2sel ? std::atoi(t2sel) : 256;
-        const int t2rows = (t2want == 192 || t2want == 256 || t2want == 320) &&
-                                   n >= (int64_t)ctx->num_sms * 4 * t2want
-                               ? t2want
-                               : 128;
-        if (!R_init && want_t128 && (n >= (int64_t)ctx->num_sms * 4 * kT2Rows || (force_t128 && n >= 4 * kT2Rows))) {
+        // Tall: ROWS-row tiles, one CTA per SM, when every CTA gets >= 4 tiles
+        // (the 148 factors are merged by one cooperative QR of their stack).
+        // 256-row tiles (8 panel + 8 update warps of a 512-thread CTA): the
+        // reflector chain per row is half the 128-row tile's (config 2 step 2
+        // sweep: 13.7 ms at 128 rows / 384 threads, 12.35 at 192 / 384, 11.8
+        // at 256 / 512; 12.8 at 320 / 512).
+        const int t2rows = n >= (int64_t)ctx->num_sms * 4 * 256 ? 256 : 128;
+        if (!R_init && n >= (int64_t)ctx->num_sms * 4 * kT2Rows) {
             const int64_t Gt = ctx->num_sms;
             TT_TRY(ensure(ctx->ws_R, (size_t)Gt * RS * 8));
             TT_TRY(ensure(ctx->ws_Scr, (size_t)Gt * t2rows * M * 8));
             double* parts = as<double>(ctx->ws_R);
-            static bool tattr = false;
-            if (!tattr) {
-                TT_CUDA(cudaFuncSetAttribute(tsqr_t128_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)t2_smem_bytes(128)));
-                TT_CUDA(cudaFuncSetAttribute(tsqr_t128_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)t2_smem_bytes(256)));
-                TT_CUDA(cudaFuncSetAttribute(tsqr_t128_kernel<192>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)t2_smem_bytes(192)));
-                TT_CUDA(cudaFuncSetAttribute(tsqr_t128_kernel<320>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)t2_smem_bytes(320)));
-                tattr = true;
-            }
-            static const bool tprof = std::getenv("TTSVD_PROF_BLK") != nullptr;
-            long long* dprof = nullptr;
-            if (tprof) TT_CUDA(cudaMalloc(&dprof, (size_t)Gt * 8 * sizeof(long long)));
-            T2Args ta{X, n, ld, parts, as<double>(ctx->ws_Scr), m, M, dprof};
+            const void* tfn = t2rows == 256 ? (const void*)tsqr_t128_kernel<256> : (const void*)tsqr_t128_kernel<128>;
+            TT_TRY(kattr(ctx, tfn, (int)t2_smem_bytes(t2rows)));
+            T2Args ta{X, n, ld, parts, as<double>(ctx->ws_Scr), m, M, nullptr};
             kmark(ctx, 0, TTSVD_K_T128);
             if (t2rows == 256)
                 tsqr_t128_kernel<256><<<(unsigned)Gt, kT2Threads, t2_smem_bytes(256), ctx->stream>>>(ta);
-            else if (t2rows == 192)
-                tsqr_t128_kernel<192><<<(unsigned)Gt, kT2Threads, t2_smem_bytes(192), ctx->stream>>>(ta);
-            else if (t2rows == 320)
-                tsqr_t128_kernel<320><<<(unsigned)Gt, kT2Threads, t2_smem_bytes(320), ctx->stream>>>(ta);
             else
                 tsqr_t128_kernel<128><<<(unsigned)Gt, kT2Threads, t2_smem_bytes(128), ctx->stream>>>(ta);
             TT_TRY(check_launch(ctx, "tsqr_t128_kernel"));
             kmark(ctx, 1, TTSVD_K_T128);
-            if (tprof) {
-                std::vector<long long> hp((size_t)Gt * 8);
-                TT_CUDA(cudaMemcpy(hp.data(), dprof, hp.size() * 8, cudaMemcpyDeviceToHost));
-                cudaFree(dprof);
-                double ph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-                for (int64_t g = 0; g < Gt; ++g)
-                    for (int q = 0; q < 8; ++q) ph[q] += (double)hp[g * 8 + q] / Gt;
-                const double tiles = (double)n / Gt / t2rows;
-                std::fprintf(stderr, "[t128 prof] n=%lld m=%d rows/tile=%d tiles/CTA=%.1f per tile kcyc: load+panel0 %.1f, phaseA %.1f (warp 0 work %.1f, rdiag wait %.1f, barrier %.1f), panel %.1f, T+store %.1f, trailing wait %.1f\n",
-                             (long long)n, m, t2rows, tiles, ph[0] / tiles / 1e3, (ph[1] + ph[5] + ph[6]) / tiles / 1e3,
-                             ph[5] / tiles / 1e3, ph[6] / tiles / 1e3, ph[1] / tiles / 1e3, ph[2] / tiles / 1e3,
-                             ph[3] / tiles / 1e3, ph[4] / tiles / 1e3);
-            }
-            static const bool prof = std::getenv("TTSVD_PROF_BLK") != nullptr;
-            cudaEvent_t e0, e1;
-            if (prof) {
-                cudaEventCreate(&e0);
-                cudaEventCreate(&e1);
-                cudaEventRecord(e0, ctx->stream);
-            }
             const int rc = merge_stack_gqr(ctx, parts, Gt, m, M, R);
-            if (prof) {
-                cudaEventRecord(e1, ctx->stream);
-                cudaEventSynchronize(e1);
-                float ms = 0.f;
-                cudaEventElapsedTime(&ms, e0, e1);
-                std::fprintf(stderr, "[t128 prof] n=%lld m=%d merge of %lld parts: %.3f ms\n", (long long)n, m, (long long)Gt, ms);
-                cudaEventDestroy(e0);
-                cudaEventDestroy(e1);
-            }
             if (rc != -1) return rc;
             TT_TRY(ensure(ctx->ws_P, (size_t)RS * 8));
             TT_TRY(merge_tree_blk(ctx, parts, Gt, m, M, as<double>(ctx->ws_P)));
             return copy_leading(ctx, as<double>(ctx->ws_P), M, m, R);
         }
         int per_sm = 1;
-        TT_TRY(set_la_attr());
-        TT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tsqr_la_kernel, kLaThreads, la_smem_bytes(M)));
+        TT_TRY(set_la_attr(ctx));
+        TT_TRY(koccupancy(ctx, (const void*)tsqr_la_kernel, kLaThreads, la_smem_bytes(M), &per_sm));
         per_sm = std::max(1, per_sm);
         int64_t G = std::max<int64_t>(1, n / (4 * (int64_t)M));
         G = std::min<int64_t>(G, (int64_t)per_sm * ctx->num_sms);
@@ -638,25 +558,9 @@ int tsqr_device(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t ld
             TT_TRY(pack_parts(ctx, R_init, 1, m, M, Rinit_ws));
         }
         BlkArgs a{X, n, ld, parts, Rinit_ws, m, M, 0, nullptr};
-        static const bool prof = std::getenv("TTSVD_PROF_BLK") != nullptr;
-        long long* dprof = nullptr;
-        if (prof) TT_CUDA(cudaMalloc(&dprof, (size_t)G * 8 * sizeof(long long)));
-        a.prof = dprof;
         kmark(ctx, 0, TTSVD_K_LA);
         TT_TRY(launch_blk(ctx, a, (int)G));
         kmark(ctx, 1, TTSVD_K_LA);
-        if (prof) {
-            std::vector<long long> hp((size_t)G * 8);
-            TT_CUDA(cudaMemcpy(hp.data(), dprof, hp.size() * 8, cudaMemcpyDeviceToHost));
-            cudaFree(dprof);
-            double ph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-            for (int64_t g = 0; g < G; ++g)
-                for (int q = 0; q < 8; ++q) ph[q] += (double)hp[g * 8 + q] / G;
-            const double tiles = (double)n / G / 32.0;
-            std::fprintf(stderr, "[blk prof] n=%lld m=%d G=%lld tiles/CTA=%.1f per tile kcyc (la: load, wait-A, panel, T, end-sync, start, prologue panel, prologue T): %.1f %.1f %.1f %.1f %.1f %.1f %.1f %.1f\n",
-                         (long long)n, m, (long long)G, tiles, ph[0] / tiles / 1e3, ph[1] / tiles / 1e3, ph[2] / tiles / 1e3,
-                         ph[3] / tiles / 1e3, ph[4] / tiles / 1e3, ph[5] / tiles / 1e3, ph[6] / tiles / 1e3, ph[7] / tiles / 1e3);
-        }
         if (G > 1) {
             const int rc = merge_stack_gqr(ctx, parts, G, m, M, R);
             if (rc != -1) return rc;
@@ -666,14 +570,8 @@ int tsqr_device(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t ld
         }
         return copy_leading(ctx, parts, M, m, R);
     }
-    {
-        static const char* tsel = std::getenv("TTSVD_TSQR");  // diagnostics: "v1" = the block-per-job kernel
-        const bool v1 = tsel && std::string(tsel) == "v1";
-        const bool ws = tsel && std::string(tsel) == "ws";
-        if (!R_init && !v1 && !ws && m <= 8 && n >= 4096) return tsqr_pt_device(ctx, X, n, m, ld, R);
-        if (!R_init && !v1 && !ws && n >= 4096) return tsqr_gs_device(ctx, X, n, m, ld, R);
-        if (!R_init && !v1 && n >= 4096) return tsqr_ws_device(ctx, X, n, m, ld, R);
-    }
+    if (!R_init && m <= 8 && n >= 4096) return tsqr_pt_device(ctx, X, n, m, ld, R);
+    if (!R_init && n >= 4096) return tsqr_gs_device(ctx, X, n, m, ld, R);
     TsqrPlan p = tsqr_plan(m);
     const int64_t min_rows = std::max<int64_t>(p.bt, 8 * (int64_t)m);
     int64_t G = std::max<int64_t>(1, n / min_rows);
@@ -710,15 +608,9 @@ int jacobi_bj(ttsvd_cu_ctx* ctx, double* A, int n, int m, int* status, bool* lau
     const int nblk = (m + 3) / 4;
     const int C = (nblk + 2 * kBjSlots - 1) / (2 * kBjSlots);
     const size_t smem = bj_smem_bytes(ldc);
-    static int static_smem = -1;
-    if (static_smem < 0) {
-        cudaFuncAttributes fa;
-        TT_CUDA(cudaFuncGetAttributes(&fa, jacobi_bj_kernel));
-        static_smem = (int)fa.sharedSizeBytes;
-        TT_CUDA(cudaFuncSetAttribute(jacobi_bj_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-        TT_CUDA(cudaFuncSetAttribute(jacobi_bj_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     kSmemLimit - static_smem));
-    }
+    int static_smem = 0;
+    TT_TRY(kstatic_smem((const void*)jacobi_bj_kernel, &static_smem));
+    TT_TRY(kattr(ctx, (const void*)jacobi_bj_kernel, kSmemLimit - static_smem, true));
     if (C > 16 || smem > (size_t)(kSmemLimit - static_smem)) return TTSVD_OK;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(C);
@@ -737,27 +629,9 @@ int jacobi_bj(ttsvd_cu_ctx* ctx, double* A, int n, int m, int* status, bool* lau
         (void)cudaGetLastError();
         return TTSVD_OK;
     }
-    static const bool prof = std::getenv("TTSVD_PROF_BJ") != nullptr;
-    long long* dprof = nullptr;
-    if (prof) {
-        TT_CUDA(cudaMalloc(&dprof, 32 * sizeof(long long)));
-        TT_CUDA(cudaMemset(dprof, 0, 32 * sizeof(long long)));
-    }
-    BjArgs ba{A, n, m, n8, ldc, C, status, 30, dprof};
+    BjArgs ba{A, n, m, n8, ldc, C, status, 30, nullptr};
     TT_CUDA(cudaLaunchKernelEx(&cfg, jacobi_bj_kernel, ba));
     TT_TRY(check_launch(ctx, "jacobi_bj_kernel"));
-    if (prof) {
-        long long h[32];
-        int sw = 0;
-        TT_CUDA(cudaMemcpy(h, dprof, sizeof(h), cudaMemcpyDeviceToHost));
-        TT_CUDA(cudaMemcpy(&sw, status, sizeof(int), cudaMemcpyDeviceToHost));
-        cudaFree(dprof);
-        const double rounds = (double)std::max(sw, 1) * (2 * kBjSlots * C - 1);
-        std::fprintf(stderr, "[bj prof] n=%d m=%d sweeps=%d per round cycles: gram %.0f solve %.0f apply %.0f moves+sync %.0f; rotating visits per sweep (of %d):",
-                     n, m, sw, h[0] / rounds, h[1] / rounds, h[2] / rounds, h[3] / rounds, (2 * kBjSlots * C - 1) * kBjSlots * C);
-        for (int i = 0; i < std::min(sw, 28); ++i) std::fprintf(stderr, " %lld", h[4 + i]);
-        std::fprintf(stderr, "\n");
-    }
     *launched = true;
     return TTSVD_OK;
 }
@@ -768,20 +642,13 @@ int jacobi_device(ttsvd_cu_ctx* ctx, double* A, int n, int m, double* Vacc) {
     TT_CUDA(cudaMemsetAsync(flags, 0, 64 * sizeof(int), ctx->stream));
     JacobiArgs a{A, Vacc, n, m, flags, flags + 40, 30};
     const size_t smem = ((size_t)n * m + (Vacc ? (size_t)m * m : 0)) * 8;
-    static const char* jsel = std::getenv("TTSVD_JACOBI");  // diagnostics: "smem", "bj", "coop"
-    const std::string sel = jsel ? jsel : "";
-    if (!Vacc && m >= 96 && (sel.empty() || sel == "bj")) {
+    if (!Vacc && m >= 96) {
         bool launched = false;
         TT_TRY(jacobi_bj(ctx, A, n, m, flags + 40, &launched));
         if (launched) return TTSVD_OK;
     }
-    if (smem <= 220 * 1024 && (sel.empty() || sel == "smem" || sel == "bj")) {
-        static bool attr = false;
-        if (!attr) {
-            TT_CUDA(cudaFuncSetAttribute(jacobi_smem_kernel<kJacobiSmemThreads>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit));
-            attr = true;
-        }
+    if (smem <= 220 * 1024) {
+        TT_TRY(kattr(ctx, (const void*)jacobi_smem_kernel<kJacobiSmemThreads>, kSmemLimit));
         jacobi_smem_kernel<kJacobiSmemThreads><<<1, kJacobiSmemThreads, smem, ctx->stream>>>(a);
         TT_TRY(check_launch(ctx, "jacobi_smem_kernel"));
         return TTSVD_OK;
@@ -803,8 +670,6 @@ int jacobi_status(ttsvd_cu_ctx* ctx, int* sweeps) {
     TT_CUDA(cudaMemcpyAsync(&h, as<int>(ctx->ws_flags) + 40, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
     TT_CUDA(cudaStreamSynchronize(ctx->stream));
     *sweeps = h;
-    static const bool dbg = std::getenv("TTSVD_DEBUG_SVD") != nullptr;
-    if (dbg) std::fprintf(stderr, "[jacobi] sweeps %d\n", h);
     if (h < 0) return fail(TTSVD_ERR_CONVERGENCE, "jacobi_svd: no convergence in 30 sweeps");
     return TTSVD_OK;
 }
@@ -819,25 +684,18 @@ int finalize_device(ttsvd_cu_ctx* ctx, const double* A, int n, int m, const doub
 // Bidiagonal path (bidiag.cuh) of svd_work: sigma now, the vectors later by
 // svd_vectors.  Returns -1 (nothing launched) when A does not fit the cluster.
 // the bidiagonal path from m = 16 (config 2 steps 1 and 6: 0.17 -> 0.10 ms, 0.21 -> 0.12 ms)
-static const int kBdMinM = std::getenv("TTSVD_BDMIN") ? std::atoi(std::getenv("TTSVD_BDMIN")) : 16;
+constexpr int kBdMinM = 16;
 int bd_sigma(ttsvd_cu_ctx* ctx, double* A, int n, int m, double* sigma) {
     const int need = (m + kBdCluster - 1) / kBdCluster;
     const int cpc = need <= 8 ? 8 : (need <= 16 ? 16 : 32);
     if (need > 32 || n < m) return -1;
-    static const char* bsel = std::getenv("TTSVD_BD");  // diagnostics: "smem" forces the shared-memory kernel
-    const bool reg = n <= kBdThreads && !(bsel && std::string(bsel) == "smem");
+    const bool reg = n <= kBdThreads;
     void (*kern)(BdArgs) = reg ? (cpc == 8 ? bd_reg_kernel<8> : (cpc == 16 ? bd_reg_kernel<16> : bd_reg_kernel<32>))
                                : (cpc == 8 ? bd_kernel<8> : (cpc == 16 ? bd_kernel<16> : bd_kernel<32>));
     const size_t smem = reg ? 0 : bd_smem_bytes(n, cpc);
-    static int static_smem[6] = {-1, -1, -1, -1, -1, -1};
-    int& ss = static_smem[(cpc == 8 ? 0 : (cpc == 16 ? 1 : 2)) + (reg ? 3 : 0)];
-    if (ss < 0) {
-        cudaFuncAttributes fa;
-        TT_CUDA(cudaFuncGetAttributes(&fa, kern));
-        ss = (int)fa.sharedSizeBytes;
-        TT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-        TT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit - ss));
-    }
+    int ss = 0;
+    TT_TRY(kstatic_smem((const void*)kern, &ss));
+    TT_TRY(kattr(ctx, (const void*)kern, kSmemLimit - ss, true));
     if (smem > (size_t)(kSmemLimit - ss)) return -1;
     TT_TRY(ensure(ctx->ws_bd, ((size_t)3 * m + 2 * (size_t)(n + 1) + (size_t)kBdCluster * n + 32 * (kBdCluster + 1)) * 8));
     double* d = as<double>(ctx->ws_bd);
@@ -856,23 +714,9 @@ int bd_sigma(ttsvd_cu_ctx* ctx, double* A, int n, int m, double* sigma) {
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    static const bool prof = std::getenv("TTSVD_PROF_BD") != nullptr;
-    long long* dprof = nullptr;
-    if (prof) {
-        TT_CUDA(cudaMalloc(&dprof, 16 * sizeof(long long)));
-        TT_CUDA(cudaMemset(dprof, 0, 16 * sizeof(long long)));
-    }
-    BdArgs ba{A, n, m, cpc, d, e, tauL, xg, dprof};
+    BdArgs ba{A, n, m, cpc, d, e, tauL, xg, nullptr};
     TT_CUDA(cudaLaunchKernelEx(&cfg, kern, ba));
     TT_TRY(check_launch(ctx, "bd_kernel"));
-    if (prof) {
-        long long h[16];
-        TT_CUDA(cudaMemcpy(h, dprof, sizeof(h), cudaMemcpyDeviceToHost));
-        cudaFree(dprof);
-        std::fprintf(stderr, "[bd prof] n=%d m=%d cycles per step: update+E1 send+T %.0f E1 wait %.0f refl-R+zpart %.0f E2 %.0f zpull+update %.0f reflect+dots %.0f\n",
-                     n, m, (h[0] + h[1]) / (double)m, h[2] / (double)m, h[3] / (double)m, h[4] / (double)m,
-                     h[5] / (double)m, h[6] / (double)m);
-    }
     const int wpb = kBisThreads / 32;
     bd_bisect_kernel<<<(m + wpb - 1) / wpb, kBisThreads, (size_t)(2 * m) * 8, ctx->stream>>>(d, e, m, sigma);
     TT_TRY(check_launch(ctx, "bd_bisect_kernel"));
@@ -899,34 +743,15 @@ int svd_vectors(ttsvd_cu_ctx* ctx, int64_t r, const double* sigma, double* Vout)
     double* X = scratch + (size_t)r * 7 * 2 * m;
     BdVecArgs va{d, e, sigma, m, (int)r, scratch, X};
     const size_t tsm = (size_t)kTwWarps * 4 * m * 8;
-    static bool tattr = false;
-    if (!tattr) {
-        TT_CUDA(cudaFuncSetAttribute(bd_twisted_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit));
-        tattr = true;
-    }
+    TT_TRY(kattr(ctx, (const void*)bd_twisted_kernel, kSmemLimit));
     bd_twisted_kernel<<<(unsigned)((r + kTwWarps - 1) / kTwWarps), kTwWarps * 32, tsm, ctx->stream>>>(va);
     TT_TRY(check_launch(ctx, "bd_twisted_kernel"));
     // clusters (rare): inverse iteration with modified Gram-Schmidt
     bd_vectors_kernel<<<(unsigned)((r + 63) / 64), 64, 0, ctx->stream>>>(va);
     TT_TRY(check_launch(ctx, "bd_vectors_kernel"));
     if (n <= 512) {
-        const unsigned g = (unsigned)((r + 4 * kBack4Warps - 1) / (4 * kBack4Warps));
-        static const char* bsel = std::getenv("TTSVD_BACK");  // diagnostics: "reg" = the register-prefetch kernel
-        if (bsel && std::string(bsel) == "reg") {
-            if (n <= 256)
-                bd_back4_kernel<8><<<g, kBack4Warps * 32, 0, ctx->stream>>>(ctx->bd_A, tauL, n, m, X, (int)r, Vout);
-            else
-                bd_back4_kernel<16><<<g, kBack4Warps * 32, 0, ctx->stream>>>(ctx->bd_A, tauL, n, m, X, (int)r, Vout);
-            return check_launch(ctx, "bd_back4_kernel");
-        }
-        static bool b4attr = false;
-        if (!b4attr) {
-            TT_CUDA(cudaFuncSetAttribute(bd_back4s_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)bd_back4s_smem(8)));
-            TT_CUDA(cudaFuncSetAttribute(bd_back4s_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)bd_back4s_smem(16)));
-            b4attr = true;
-        }
+        TT_TRY(kattr(ctx, (const void*)bd_back4s_kernel<8>, (int)bd_back4s_smem(8)));
+        TT_TRY(kattr(ctx, (const void*)bd_back4s_kernel<16>, (int)bd_back4s_smem(16)));
         const unsigned gs = (unsigned)((r + kB4sVpw * kB4sWarps - 1) / (kB4sVpw * kB4sWarps));
         if (n <= 256)
             bd_back4s_kernel<8><<<gs, kB4sWarps * 32, bd_back4s_smem(8), ctx->stream>>>(ctx->bd_A, tauL, n, m, X,
@@ -937,11 +762,7 @@ int svd_vectors(ttsvd_cu_ctx* ctx, int64_t r, const double* sigma, double* Vout)
         return check_launch(ctx, "bd_back4s_kernel");
     }
     const size_t smem = (size_t)kBackWarps * n * 8;
-    static bool attr = false;
-    if (!attr) {
-        TT_CUDA(cudaFuncSetAttribute(bd_back_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit));
-        attr = true;
-    }
+    TT_TRY(kattr(ctx, (const void*)bd_back_kernel, kSmemLimit));
     bd_back_kernel<<<(unsigned)((r + kBackWarps - 1) / kBackWarps), kBackWarps * 32, smem, ctx->stream>>>(
         ctx->bd_A, tauL, n, m, X, (int)r, Vout);
     return check_launch(ctx, "bd_back_kernel");
@@ -976,9 +797,7 @@ int svd_work(ttsvd_cu_ctx* ctx, const double* src, int64_t src_rows, int64_t src
     }
     ctx->bd_pending = false;
     if (!accumulate) {
-        static const char* ssel = std::getenv("TTSVD_SVD");  // diagnostics: "jacobi" forces the sweeps
-        const bool jac = ssel && std::string(ssel) == "jacobi";
-        if (!jac && m >= kBdMinM) {
+        if (m >= kBdMinM) {
             const int rc = bd_sigma(ctx, A, (int)n, (int)m, sigma);
             if (rc != -1) {
                 *sweeps = 0;
@@ -1002,11 +821,8 @@ template <int KC>
 int launch_tsmm(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t ldx, const double* V, int64_t ldv, int k,
                 double* Y, int64_t out_rows, int64_t ldy) {
     const size_t smem = (size_t)m * KC * 8;
-    static bool attr = false;
-    if (!attr) {
-        TT_CUDA(cudaFuncSetAttribute(tsmm_kernel<KC>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit));
-        attr = true;
-    }
+    if (smem > (size_t)kSmemLimit) return fail(TTSVD_ERR_SHAPE, "tsmm_kernel: V block exceeds shared memory");
+    TT_TRY(kattr(ctx, (const void*)tsmm_kernel<KC>, kSmemLimit));
     const int chunks = (k + KC - 1) / KC;
     int64_t blocks = (n + 255) / 256;
     blocks = std::min<int64_t>(blocks, (int64_t)ctx->num_sms * 8);
@@ -1019,13 +835,9 @@ template <int KC>
 int launch_tsmm_async(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t ldx, const double* V, int64_t ldv,
                       int k, double* Y, int64_t out_rows, int64_t ldy) {
     const size_t smem = ((size_t)((m * KC + 1) & ~1) + (size_t)2 * m * 256) * 8;
-    static bool attr = false;
-    static int per_sm = 1;
-    if (!attr) {
-        TT_CUDA(cudaFuncSetAttribute(tsmm_async_kernel<KC>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit));
-        attr = true;
-    }
-    TT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tsmm_async_kernel<KC>, 256, smem));
+    int per_sm = 1;
+    TT_TRY(kattr(ctx, (const void*)tsmm_async_kernel<KC>, kSmemLimit));
+    TT_TRY(koccupancy(ctx, (const void*)tsmm_async_kernel<KC>, 256, smem, &per_sm));
     const int64_t chunks = (n + 255) / 256;
     const int64_t blocks = std::min<int64_t>(chunks, (int64_t)std::max(1, per_sm) * ctx->num_sms);
     const int ychunks = (k + KC - 1) / KC;
@@ -1039,14 +851,9 @@ int launch_tsmm_async_wide(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m,
                            int64_t ldv, int k, double* Y, int64_t out_rows, int64_t ldy) {
     const size_t smem = ((size_t)((m * KC + 1) & ~1) + (size_t)2 * 32 * 256) * 8;
     if (smem > (size_t)kSmemLimit) return -1;
-    static bool attr = false;
-    if (!attr) {
-        TT_CUDA(cudaFuncSetAttribute(tsmm_async_wide_kernel<KC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     kSmemLimit));
-        attr = true;
-    }
+    TT_TRY(kattr(ctx, (const void*)tsmm_async_wide_kernel<KC>, kSmemLimit));
     int per_sm = 1;
-    TT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tsmm_async_wide_kernel<KC>, 256, smem));
+    TT_TRY(koccupancy(ctx, (const void*)tsmm_async_wide_kernel<KC>, 256, smem, &per_sm));
     const int64_t chunks = (n + 255) / 256;
     const int64_t blocks = std::min<int64_t>(chunks, (int64_t)std::max(1, per_sm) * ctx->num_sms);
     const int ychunks = (k + KC - 1) / KC;
@@ -1059,11 +866,7 @@ template <int NT>
 int launch_tsmm_dmma(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t ldx, const double* V, int64_t ldv,
                      int k, double* Y, int64_t out_rows, int64_t ldy) {
     const size_t smem = (size_t)((m + 3) & ~3) * tsmm_vld(NT) * 8;
-    static bool attr = false;
-    if (!attr) {
-        TT_CUDA(cudaFuncSetAttribute(tsmm_dmma_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit));
-        attr = true;
-    }
+    TT_TRY(kattr(ctx, (const void*)tsmm_dmma_kernel<NT>, kSmemLimit));
     const int chunks = (k + 8 * NT - 1) / (8 * NT);
     int64_t blocks = (n + 255) / 256;
     blocks = std::min<int64_t>(blocks, (int64_t)ctx->num_sms * 4);
@@ -1075,10 +878,9 @@ int launch_tsmm_dmma(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64
 int tsmm_device(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t ldx, const double* V, int64_t ldv, int k,
                 double* Y, int64_t out_rows, int64_t out_cols, int64_t ldy) {
     int rc;
-    static const char* tsel = std::getenv("TTSVD_TSMM");  // diagnostics: "ffma" = the one-row-per-thread kernel
     // measured (tools/config3_sweep.py): the tensor-core path wins only once the
     // FFMA kernel turns compute-bound (k > 16 output columns, m >= 32)
-    const bool dmma = !(tsel && std::string(tsel) == "ffma") && k > 16 && m >= 32 && n >= (int64_t)1 << 18 &&
+    const bool dmma = k > 16 && m >= 32 && n >= (int64_t)1 << 18 &&
                       (size_t)((m + 3) & ~3) * tsmm_vld(4) * 8 <= 200 * 1024;
     if (dmma) {
         rc = launch_tsmm_dmma<4>(ctx, X, n, m, ldx, V, ldv, k, Y, out_rows, ldy);
@@ -1091,13 +893,12 @@ int tsmm_device(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t ld
         }
         return TTSVD_OK;
     }
-    static const bool tsmm_async = !(tsel && std::string(tsel) == "ffma");
-    if (tsmm_async && k > 1 && k <= 16 && m <= 32 && n >= (int64_t)1 << 18) {
+    if (k > 1 && k <= 16 && m <= 32 && n >= (int64_t)1 << 18) {
         // narrow X: rows staged by cp.async (tsmm_async_kernel)
         rc = k <= 4 ? launch_tsmm_async<4>(ctx, X, n, m, ldx, V, ldv, k, Y, out_rows, ldy)
                     : (k <= 8 ? launch_tsmm_async<8>(ctx, X, n, m, ldx, V, ldv, k, Y, out_rows, ldy)
                               : launch_tsmm_async<16>(ctx, X, n, m, ldx, V, ldv, k, Y, out_rows, ldy));
-    } else if (tsmm_async && k > 1 && k <= 32 && m > 32 && n >= (int64_t)1 << 16 && !dmma &&
+    } else if (k > 1 && k <= 32 && m > 32 && n >= (int64_t)1 << 16 && !dmma &&
                (rc = k <= 4 ? launch_tsmm_async_wide<4>(ctx, X, n, m, ldx, V, ldv, k, Y, out_rows, ldy)
                             : (k <= 8 ? launch_tsmm_async_wide<8>(ctx, X, n, m, ldx, V, ldv, k, Y, out_rows, ldy)
                                       : (k <= 16 || (size_t)m * 32 * 8 + 2 * 32 * 256 * 8 > (size_t)kSmemLimit
@@ -1105,12 +906,20 @@ int tsmm_device(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t ld
                                              : launch_tsmm_async_wide<32>(ctx, X, n, m, ldx, V, ldv, k, Y, out_rows,
                                                                           ldy)))) != -1) {
         // wider X: column blocks of the row chunk staged by cp.async
-    } else if (k <= 1) rc = launch_tsmm<1>(ctx, X, n, m, ldx, V, ldv, k, Y, out_rows, ldy);
-    else if (k <= 2) rc = launch_tsmm<2>(ctx, X, n, m, ldx, V, ldv, k, Y, out_rows, ldy);
-    else if (k <= 4) rc = launch_tsmm<4>(ctx, X, n, m, ldx, V, ldv, k, Y, out_rows, ldy);
-    else if (k <= 8) rc = launch_tsmm<8>(ctx, X, n, m, ldx, V, ldv, k, Y, out_rows, ldy);
-    else if (k <= 16 || (size_t)m * 32 * 8 > 200 * 1024) rc = launch_tsmm<16>(ctx, X, n, m, ldx, V, ldv, k, Y, out_rows, ldy);
-    else rc = launch_tsmm<32>(ctx, X, n, m, ldx, V, ldv, k, Y, out_rows, ldy);
+    } else {
+        // KC output columns per CTA pass, capped so V's m x KC block fits
+        // shared memory (more column chunks on grid.y otherwise)
+        int kc = k <= 1 ? 1 : (k <= 2 ? 2 : (k <= 4 ? 4 : (k <= 8 ? 8 : (k <= 16 ? 16 : 32))));
+        while (kc > 1 && (size_t)m * kc * 8 > (size_t)kTsmmSmem) kc /= 2;
+        switch (kc) {
+            case 1: rc = launch_tsmm<1>(ctx, X, n, m, ldx, V, ldv, k, Y, out_rows, ldy); break;
+            case 2: rc = launch_tsmm<2>(ctx, X, n, m, ldx, V, ldv, k, Y, out_rows, ldy); break;
+            case 4: rc = launch_tsmm<4>(ctx, X, n, m, ldx, V, ldv, k, Y, out_rows, ldy); break;
+            case 8: rc = launch_tsmm<8>(ctx, X, n, m, ldx, V, ldv, k, Y, out_rows, ldy); break;
+            case 16: rc = launch_tsmm<16>(ctx, X, n, m, ldx, V, ldv, k, Y, out_rows, ldy); break;
+            default: rc = launch_tsmm<32>(ctx, X, n, m, ldx, V, ldv, k, Y, out_rows, ldy); break;
+        }
+    }
     if (rc != TTSVD_OK) return rc;
     if (ldy > out_rows) {
         const int64_t pad = (ldy - out_rows) * out_cols;
@@ -1368,6 +1177,8 @@ int ttsvd_cu_ctx_destroy(ttsvd_cu_ctx* ctx) {
     for (DevBuf* b : {&ctx->ws_R, &ctx->ws_R2, &ctx->ws_P, &ctx->ws_Scr, &ctx->ws_G, &ctx->ws_Gp, &ctx->ws_A, &ctx->ws_V, &ctx->ws_Vacc, &ctx->ws_U, &ctx->ws_sigma, &ctx->ws_flags, &ctx->ws_work[0],
                       &ctx->ws_work[1], &ctx->ws_X, &ctx->ws_send, &ctx->ws_recv, &ctx->ws_thick[0], &ctx->ws_thick[1], &ctx->ws_gs, &ctx->ws_bd})
         if (b->p) cudaFree(b->p);
+    for (DevBuf& b : ctx->ws_slab)
+        if (b.p) cudaFree(b.p);
     if (ctx->host_stage.p) cudaFreeHost(ctx->host_stage.p);
     if (ctx->host_cores.p) cudaFreeHost(ctx->host_cores.p);
     for (auto& e : ctx->ev)
@@ -1509,7 +1320,7 @@ int ttsvd_cu_tsmm_reshape(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int64_t
         return fail(TTSVD_ERR_SHAPE, "tsmm_reshape: out shape does not hold n*k elements");
     if (!X || !V || !Y || ldx < n || ldv < m || ldy < out_rows || k < 1)
         return fail(TTSVD_ERR_INVALID, "tsmm_reshape: bad pointer or leading dimension");
-    if ((size_t)m * 8 > 200 * 1024) return fail(TTSVD_ERR_SHAPE, "tsmm_reshape: m too large");
+    if ((size_t)m * 8 > (size_t)kTsmmSmem) return fail(TTSVD_ERR_SHAPE, "tsmm_reshape: m too large");
     return tsmm_device(ctx, X, n, (int)m, ldx, V, ldv, (int)k, Y, out_rows, out_cols, ldy);
 }
 
@@ -1526,7 +1337,6 @@ int ttsvd_cu_tt_svd(ttsvd_cu_ctx* ctx, const double* X, const int64_t* dims, int
     }
     const int64_t rows = total / dims[d - 1];
     if (ldx < rows) return fail(TTSVD_ERR_LAYOUT, "tt_svd: leading stride below the row count");
-    if (r_max <= 0) r_max = INT64_MAX;
     auto* tt = new ttsvd_cu_tt();
     std::vector<int64_t> dv(dims, dims + d);
     int rc = run_chain(ctx, WorkView{X, rows, dims[d - 1], ldx}, dv, r_max, eps, d, tt);
@@ -1544,7 +1354,6 @@ int ttsvd_cu_choose_combined_dims(const int64_t* dims, int64_t d, int64_t m_min,
     if (d < 2) return fail(TTSVD_ERR_DEGENERATE, "choose_combined_dims: requires d >= 2");
     if (m_min < 1 || !(f1_min > 0.0) || f1_min > 1.0)
         return fail(TTSVD_ERR_DIMENSION_MISMATCH, "choose_combined_dims: invalid parameters");
-    if (r_max <= 0) r_max = INT64_MAX;
     int64_t total = 1;
     for (int64_t i = 0; i < d; ++i) total *= dims[i];
     // ThickBoundsParams::estimate_at (tt_svd.hpp:298-309)
@@ -1583,7 +1392,6 @@ int ttsvd_cu_tt_svd_thick(ttsvd_cu_ctx* ctx, const double* X, const int64_t* dim
         if (dims[i] < 1) return fail(TTSVD_ERR_DIMENSION, "Shape: extents must be >= 1");
         total *= dims[i];
     }
-    if (r_max <= 0) r_max = INT64_MAX;
     const int64_t rows0 = total / dims[d - 1];
     if (ldx < rows0) return fail(TTSVD_ERR_LAYOUT, "tt_svd_thick: leading stride below the row count");
     int64_t k = 1, m = dims[d - 1];
@@ -1685,7 +1493,6 @@ int ttsvd_cu_tt_svd_distributed(ttsvd_cu_ctx* ctx, const double* const* slabs, i
         return fail(TTSVD_ERR_PARTITION, "tt_svd_distributed: inconsistent partition counts");
     if (n_slabs != P_total && !exchange)
         return fail(TTSVD_ERR_INVALID, "tt_svd_distributed: exchange callback required across processes");
-    if (r_max <= 0) r_max = INT64_MAX;
     const int64_t d = d_local + 1;
     int64_t total = 1;
     for (int64_t i = 0; i < d_local; ++i) total *= ldims[i];
@@ -1706,13 +1513,11 @@ int ttsvd_cu_tt_svd_distributed(ttsvd_cu_ctx* ctx, const double* const* slabs, i
         const int64_t rows = d_local == 1 ? 1 : total / ldims[d_local - 1];
         return done(run_chain(ctx, WorkView{slabs[0], rows, ldims[d_local - 1], ld_slab}, gdims, r_max, eps, d, tt));
     }
-    // per-slab state: ping-pong buffers owned here
+    // per-slab state: grow-only ping-pong workspaces of the context (nothing
+    // is allocated or freed per call once they have grown)
     std::vector<WorkView> cur(n_slabs);
-    std::vector<DevBuf> bufs(2 * n_slabs);
-    auto free_bufs = [&]() {
-        for (auto& b : bufs)
-            if (b.p) cudaFree(b.p);
-    };
+    if (ctx->ws_slab.size() < (size_t)(2 * n_slabs)) ctx->ws_slab.resize((size_t)(2 * n_slabs));
+    std::vector<DevBuf>& bufs = ctx->ws_slab;
     for (int64_t p = 0; p < n_slabs; ++p) {
         if (d_local == 1) cur[p] = WorkView{slabs[p], 1, ldims[0], ld_slab};
         else cur[p] = WorkView{slabs[p], total / ldims[d_local - 1], ldims[d_local - 1], ld_slab};
@@ -1820,7 +1625,6 @@ int ttsvd_cu_tt_svd_distributed(ttsvd_cu_ctx* ctx, const double* const* slabs, i
         }
     }
     cudaStreamSynchronize(ctx->stream);
-    free_bufs();
     (void)part0;
     return done(rc);
 }

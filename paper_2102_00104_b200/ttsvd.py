@@ -482,7 +482,7 @@ def tt_svd_tsqr(X, dims, spec: TruncationSpec | tuple | None = None, ctx_exec=No
     d = len(dims)
     if d < 2:
         raise DegenerateDimension("tt_svd_tsqr: requires d >= 2")
-    r_max = spec.r_max if spec.r_max < 2 ** 62 else 0
+    r_max = int(spec.r_max)
     dv = np.asarray(dims, dtype=np.int64)
     L = _lib.lib()
     h = C.c_void_p()
@@ -518,7 +518,7 @@ def choose_combined_dims(dims, params: ThickBoundsParams | None = None, r_max: i
     k, m = C.c_int64(), C.c_int64()
     _check(_lib.lib().ttsvd_cu_choose_combined_dims(dv.ctypes.data_as(_lib.i64p), len(dv), int(params.m_min),
                                                     float(params.f1_min), rt.ctypes.data if len(rt) else None,
-                                                    len(rt), int(r_max or 0), C.byref(k), C.byref(m)))
+                                                    len(rt), int(2 ** 63 - 1 if r_max is None else r_max), C.byref(k), C.byref(m)))
     return int(k.value), int(m.value)
 
 
@@ -532,7 +532,7 @@ def tt_svd_thick_bounds(X, dims, spec: TruncationSpec | tuple | None = None,
     d = len(dims)
     if d < 2:
         raise DegenerateDimension("tt_svd_thick_bounds: requires d >= 2")
-    r_max = spec.r_max if spec.r_max < 2 ** 62 else 0
+    r_max = int(spec.r_max)
     X = to_device_matrix(X)
     dv = np.asarray(dims, dtype=np.int64)
     rt = np.asarray(params.r_tilde, dtype=np.int64)
@@ -593,7 +593,7 @@ def tt_svd_distributed(slabs, ldims, spec: TruncationSpec | tuple | None = None,
         P_total = n_slabs
     ptrs = (C.c_void_p * n_slabs)(*[C.c_void_p(s.data_ptr()) for s in slabs])
     dv = np.asarray(ldims, dtype=np.int64)
-    r_max = spec.r_max if spec.r_max < 2 ** 62 else 0
+    r_max = int(spec.r_max)
     if exchange is not None:
         def _cb(user, send, recv, count, stream):
             try:

@@ -66,6 +66,13 @@ def test_drivers_bitwise_vs_reference(orc, ref, dims, rmax, eps, seed):
         assert ra == rb
         assert all(np.array_equal(a, b) for a, b in zip(ca, cb))
         assert [s[3] for s in sa] == [s[3] for s in sb]
+        # the step-by-step reference driver (the GPU parity tests' sigma
+        # source) is the reference's tt_svd_tsqr, bitwise, and its sigmas are
+        # the restatement's
+        rc, cc, sc = ref.tt_svd_tsqr_sigma(X, dims, X.shape[0], rmax, eps, workers=w)
+        assert rc == rb and all(np.array_equal(a, b) for a, b in zip(cc, cb))
+        _, _, _, so = orc.tt_svd_tsqr(X, dims, X.shape[0], rmax, eps, workers=w, with_sigma=True)
+        assert len(sc) == len(so) and all(np.array_equal(a, b) for a, b in zip(sc, so))
 
 
 def test_distributed_bitwise_vs_reference(orc, ref):
