@@ -54,6 +54,7 @@ typedef struct {
     double t_tsqr_sweep_ms;                /* the TSQR's main sweep kernel alone (no merge) */
     int32_t tsqr_kernel;                   /* which: TTSVD_K_* below */
     int32_t svd_sweeps;                    /* Jacobi sweeps of the step's small SVD */
+    double t_reorder_ms;                   /* two-sided sweep: transpose_reorder (StepRecord::t_reorder) */
 } ttsvd_cu_step;
 
 /* tsqr_kernel values (diagnostics) */
@@ -134,6 +135,25 @@ int ttsvd_cu_tsmm_reshape(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int64_t
  * (select_rank, small_svd.hpp:49-63). */
 int ttsvd_cu_tt_svd(ttsvd_cu_ctx* ctx, const double* X, const int64_t* dims, int64_t d, int64_t ldx, int64_t r_max,
                     double eps, ttsvd_cu_tt** out);
+/* tt_svd.hpp:159-199 detail::run_chain(): the Alg. 2 loop on a work matrix W
+ * (rows x cols, device, ld ldw) that is the last-mode matricization of a
+ * tensor with extents dims[0..d-1].  *delta_io < 0 derives the truncation
+ * parameter from the first step's sigma with d_for_delta modes and writes it
+ * back (run_chain takes the TruncationSpec by reference, tt_svd.hpp:160);
+ * first_sigma_norm_out (optional) receives ChainResult::first_sigma_norm. */
+int ttsvd_cu_run_chain(ttsvd_cu_ctx* ctx, const double* W, int64_t rows, int64_t cols, int64_t ldw, const int64_t* dims,
+                       int64_t d, int64_t r_max, double eps, int64_t d_for_delta, double* delta_io,
+                       double* first_sigma_norm_out, ttsvd_cu_tt** out);
+/* tt_svd.hpp:402-512 tt_svd_two_sided() (Alg. 4): alternating right / left
+ * steps with a transpose_reorder between them; same arguments as
+ * ttsvd_cu_tt_svd. */
+int ttsvd_cu_tt_svd_two_sided(ttsvd_cu_ctx* ctx, const double* X, const int64_t* dims, int64_t d, int64_t ldx,
+                              int64_t r_max, double eps, ttsvd_cu_tt** out);
+/* tsmm.hpp:84-126 transpose_reorder(): Y (out_rows x out_cols, ld ldy) holds
+ * the column-major flat order of W^T (W: n x m, ld ldw), i.e. W(i, j) lands at
+ * flat position m*i + j; padding rows out_rows..ldy-1 are zeroed. */
+int ttsvd_cu_transpose_reorder(ttsvd_cu_ctx* ctx, const double* W, int64_t n, int64_t m, int64_t ldw, double* Y,
+                               int64_t out_rows, int64_t out_cols, int64_t ldy);
 /* tt_svd.hpp:316-330 choose_combined_dims() with ThickBoundsParams
  * (tt_svd.hpp:292-310): k trailing modes merged into one of extent m.
  * r_tilde may be NULL (n_r_tilde = 0): the estimates default to r_max

@@ -116,6 +116,9 @@ class Oracle:
             f("choose_combined_dims").argtypes = [i64ptr, i64, i64, C.c_double, C.c_void_p, i64, i64, i64ptr, i64ptr]
             f("tt_svd_thick_bounds").argtypes = [dptr, i64ptr, i64, i64, i64, C.c_double, i64, C.c_double,
                                                  C.c_void_p, i64, C.c_int, i64ptr, dptr, i64, i64ptr]
+            f("tt_svd_two_sided").argtypes = [dptr, i64ptr, i64, i64, i64, C.c_double, C.c_int, i64ptr, dptr, i64,
+                                              i64ptr]
+            f("transpose_reorder").argtypes = [dptr, i64, i64, i64, dptr, i64, i64, i64, C.c_int]
             L.ref_set_budget(1 << 40)
 
     def _f(self, name):
@@ -330,6 +333,34 @@ class Oracle:
             self._check(rc, "tt_svd_thick_bounds")
             break
         return ranks.tolist(), split_cores(cores, dims, ranks)
+
+    def tt_svd_two_sided(self, X: np.ndarray, dims, ld: int, r_max: int, eps: float = 0.0, workers: int = 1):
+        """Reference only (tt_svd.hpp:402-512, Alg. 4).  Returns (ranks, cores)."""
+        dims = np.ascontiguousarray(dims, dtype=np.int64)
+        d = len(dims)
+        ranks = np.zeros(d + 1, dtype=np.int64)
+        need = np.zeros(1, dtype=np.int64)
+        cap = max(1, min(int(np.prod(dims)), 1 << 22))
+        while True:
+            cores = np.zeros(cap)
+            rc = self._f("tt_svd_two_sided")(_p(X), _pi(dims), d, ld, r_max, eps, workers, _pi(ranks), _p(cores),
+                                             cap, _pi(need))
+            if rc == 11:
+                cap = int(need[0])
+                continue
+            self._check(rc, "tt_svd_two_sided")
+            break
+        return ranks.tolist(), split_cores(cores, dims, ranks)
+
+    def transpose_reorder(self, W: np.ndarray, out_rows: int, out_cols: int, workers: int = 1) -> np.ndarray:
+        """Reference only (tsmm.hpp:84-126): the padded (ld x out_cols) output."""
+        W = np.asfortranarray(W, dtype=np.float64)
+        n, m = W.shape
+        ldy = padded_stride(out_rows)
+        Y = np.zeros((ldy, out_cols), order="F")
+        self._check(self._f("transpose_reorder")(_p(W), n, m, max(n, 1), _p(Y), out_rows, out_cols, ldy, workers),
+                    "transpose_reorder")
+        return Y
 
     def tt_error(self, X: np.ndarray, ld: int, dims, ranks, cores: list[np.ndarray]) -> float:
         dims = np.ascontiguousarray(dims, dtype=np.int64)

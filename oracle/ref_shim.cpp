@@ -248,6 +248,29 @@ int ref_tt_svd_thick_bounds(const double* X, const int64_t* dims, int64_t d, int
     } catch (const std::exception& e) { return code_of(e); }
 }
 
+// tt_svd.hpp:402-512 (Alg. 4) and tsmm.hpp:84-126
+int ref_tt_svd_two_sided(const double* X, const int64_t* dims, int64_t d, int64_t ldx, int64_t r_max, double eps,
+                         int workers, int64_t* ranks, double* cores, int64_t cap, int64_t* needed) {
+    try {
+        DenseTensor t = tensor_from(X, dims, d, ldx);
+        ExecContext ctx;
+        ctx.threads = workers;
+        ctx.validate_reflectors = false;
+        TensorTrain tt = tt_svd_two_sided(t, spec_of(r_max, eps), ctx);
+        return export_tt(tt, ranks, cores, cap, needed);
+    } catch (const std::exception& e) { return code_of(e); }
+}
+
+int ref_transpose_reorder(const double* W, int64_t n, int64_t m, int64_t ldw, double* Y, int64_t out_rows,
+                          int64_t out_cols, int64_t ldy, int workers) {
+    try {
+        PaddedMatrix o = transpose_reorder(ConstMatrixView{W, n, m, ldw}, out_rows, out_cols, workers);
+        if (o.stride() != ldy) return 3;
+        std::memcpy(Y, o.data(), o.stride() * out_cols * 8);
+        return 0;
+    } catch (const std::exception& e) { return code_of(e); }
+}
+
 // Timing entry for the CPU baseline: the input is already a reference
 // DenseTensor built once by ref_tensor_new, so only tt_svd_tsqr is timed.
 void* ref_tensor_new(const double* X, const int64_t* dims, int64_t d, int64_t ldx) {

@@ -23,7 +23,8 @@ i64p = C.POINTER(C.c_int64)
 class Step(C.Structure):
     _fields_ = [("rows", i64), ("cols", i64), ("nsig", i64), ("rank", i64),
                 ("t_tsqr_ms", C.c_double), ("t_svd_ms", C.c_double), ("t_tsmm_ms", C.c_double),
-                ("t_tsqr_sweep_ms", C.c_double), ("tsqr_kernel", C.c_int32), ("svd_sweeps", C.c_int32)]
+                ("t_tsqr_sweep_ms", C.c_double), ("tsqr_kernel", C.c_int32), ("svd_sweeps", C.c_int32),
+                ("t_reorder_ms", C.c_double)]
 
 
 TSQR_KERNELS = {0: "none", 1: "tsqr_ws_kernel", 2: "tsqr_tile_kernel", 3: "tsqr_la_kernel", 4: "tsqr_t128_kernel",
@@ -54,6 +55,11 @@ _SIGS = {
     "ttsvd_cu_derive_delta": (C.c_int, [C.c_double, C.c_double, i64, C.POINTER(C.c_double)]),
     "ttsvd_cu_tsmm_reshape": (C.c_int, [C.c_void_p, dptr, i64, i64, i64, dptr, i64, i64, dptr, i64, i64, i64]),
     "ttsvd_cu_tt_svd": (C.c_int, [C.c_void_p, dptr, i64p, i64, i64, i64, C.c_double, C.POINTER(C.c_void_p)]),
+    "ttsvd_cu_run_chain": (C.c_int, [C.c_void_p, dptr, i64, i64, i64, i64p, i64, i64, C.c_double, i64,
+                                     C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(C.c_void_p)]),
+    "ttsvd_cu_tt_svd_two_sided": (C.c_int, [C.c_void_p, dptr, i64p, i64, i64, i64, C.c_double,
+                                            C.POINTER(C.c_void_p)]),
+    "ttsvd_cu_transpose_reorder": (C.c_int, [C.c_void_p, dptr, i64, i64, i64, dptr, i64, i64, i64]),
     "ttsvd_cu_choose_combined_dims": (C.c_int, [i64p, i64, i64, C.c_double, C.c_void_p, i64, i64, i64p, i64p]),
     "ttsvd_cu_tt_svd_thick": (C.c_int, [C.c_void_p, C.c_void_p, i64p, i64, i64, i64, C.c_double, i64, C.c_double,
                                         C.c_void_p, i64, C.POINTER(C.c_void_p)]),

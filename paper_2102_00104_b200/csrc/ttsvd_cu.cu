@@ -1136,6 +1136,179 @@ int run_chain(ttsvd_cu_ctx* ctx, WorkView cur, const std::vector<int64_t>& dims,
     return TTSVD_OK;
 }
 
+// tsmm.hpp:84-126 transpose_reorder: Y (out_rows x out_cols, ld ldy) <- the
+// flat order of W^T; padding rows zeroed.
+int transpose_reorder_device(ttsvd_cu_ctx* ctx, const double* W, int64_t n, int64_t m, int64_t ldw, double* Y,
+                             int64_t out_rows, int64_t out_cols, int64_t ldy) {
+    const int64_t tiles = ((n + 31) / 32) * ((m + 31) / 32);
+    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(tiles, (int64_t)ctx->num_sms * 8));
+    transpose_reorder_kernel<<<(unsigned)grid, dim3(32, 8), 0, ctx->stream>>>(W, n, m, ldw, Y, out_rows, ldy);
+    TT_TRY(check_launch(ctx, "transpose_reorder_kernel"));
+    if (ldy > out_rows) {
+        const int64_t pad = (ldy - out_rows) * out_cols;
+        const int blocks = (int)std::min<int64_t>((pad + 255) / 256, 1024);
+        zero_padding_kernel<<<std::max(blocks, 1), 256, 0, ctx->stream>>>(Y, out_rows, ldy, out_cols);
+        TT_TRY(check_launch(ctx, "zero_padding_kernel"));
+    }
+    return TTSVD_OK;
+}
+
+// The first `count` flat (column-major) entries of a padded device matrix
+// (rows x ?, ld) on the host: core_from_padded (tt_svd.hpp:140-147).
+int flat_d2h(ttsvd_cu_ctx* ctx, const double* M, int64_t rows, int64_t ld, int64_t count, std::vector<double>& out) {
+    const int64_t cols = (count + rows - 1) / rows;
+    TT_TRY(ensure_host(ctx->host_stage, (size_t)rows * cols * 8));
+    TT_CUDA(cudaMemcpy2DAsync(ctx->host_stage.p, (size_t)rows * 8, M, (size_t)ld * 8, (size_t)rows * 8, (size_t)cols,
+                              cudaMemcpyDeviceToHost, ctx->stream));
+    TT_CUDA(cudaStreamSynchronize(ctx->stream));
+    out.assign(as<double>(ctx->host_stage), as<double>(ctx->host_stage) + count);
+    return TTSVD_OK;
+}
+
+// Two-sided sweep (Alg. 4, tt_svd.hpp:402-512): steps alternate between the
+// right end (core from V^T, as run_chain) and the left end (core from V);
+// each step's TSMM output is re-laid out by transpose_reorder for the
+// opposite end.  Same kernels as run_chain (K_TSQR, K_SVD, K_TSMM) plus the
+// reorder.
+int run_two_sided(ttsvd_cu_ctx* ctx, WorkView cur, const std::vector<int64_t>& dims, int64_t r_max, double eps,
+                  ttsvd_cu_tt* out) {
+    const int64_t d = (int64_t)dims.size();
+    out->dims = dims;
+    out->cores.assign(d, {});
+    std::vector<int64_t> rl(d, 1), rr(d, 1);  // core shapes
+    int64_t lo = 0, hi = d - 1, r_left = 1, r_right = 1, built = 0;
+    bool right = true;
+    double delta = -1.0;
+    int which = 0;
+    std::vector<double> sig, Vh, flat;
+    Timer tm(ctx);
+    while (built < d - 1) {
+        ttsvd_cu_step st{};
+        const int64_t m = cur.cols;
+        st.rows = cur.rows;
+        st.cols = m;
+        const bool tall = cur.rows >= cur.cols;
+        const int64_t nsig = tall ? m : cur.rows;
+        TT_TRY(ensure(ctx->ws_sigma, (size_t)std::max<int64_t>(m, nsig) * 8));
+        TT_TRY(ensure(ctx->ws_V, (size_t)m * std::max<int64_t>(nsig, 1) * 8));
+        double* d_sigma = as<double>(ctx->ws_sigma);
+        double* d_V = as<double>(ctx->ws_V);
+        int sweeps = 0;
+        tm.mark(0);
+        if (tall) {
+            TT_TRY(ensure(ctx->ws_X, (size_t)m * m * 8));
+            double* R = as<double>(ctx->ws_X);
+            TT_TRY(tsqr_device(ctx, cur.data, cur.rows, (int)m, cur.ld, R));
+            tm.mark(1);
+            TT_TRY(svd_work(ctx, R, m, m, m, true, false, d_sigma, d_V, &sweeps));
+        } else {
+            tm.mark(1);
+            TT_TRY(svd_work(ctx, cur.data, cur.rows, cur.cols, cur.ld, true, false, d_sigma, d_V, &sweeps));
+        }
+        tm.mark(2);
+        sig.resize(nsig);
+        TT_TRY(d2h(ctx, sig.data(), d_sigma, nsig));
+        if (delta < 0.0) {
+            if (d < 2) return fail(TTSVD_ERR_DEGENERATE, "derive_delta: requires d >= 2");
+            delta = eps / std::sqrt((double)(d - 1)) * sigma_norm_h(sig.data(), nsig);
+        }
+        const int64_t rnew = choose_rank_h(sig.data(), nsig, cur.cols, nsig, delta, r_max, cur.rows);
+        TT_TRY(svd_vectors(ctx, rnew, d_sigma, d_V));
+        Vh.resize((size_t)m * rnew);
+        TT_TRY(d2h(ctx, Vh.data(), d_V, (size_t)m * rnew));
+        st.nsig = nsig;
+        st.rank = rnew;
+        st.svd_sweeps = sweeps;
+        st.tsqr_kernel = tall ? ctx->last_kernel : TTSVD_K_NONE;
+        ++built;
+        const bool last = built == d - 1;
+        // the step's TSMM target (tsmm_reshape's out_rows) and, unless this
+        // step finishes the train, the reorder's target shape
+        int64_t p_rows, t_rows = 0, t_cols = 0;
+        if (right) {
+            const int64_t n_hi = dims[hi];
+            std::vector<double> core((size_t)(rnew * n_hi * r_right));  // core_from_vt (tt_svd.hpp:121-128)
+            for (int64_t b = 0; b < r_right; ++b)
+                for (int64_t x = 0; x < n_hi; ++x)
+                    for (int64_t a = 0; a < rnew; ++a) core[a + rnew * (x + n_hi * b)] = Vh[a * m + (x + n_hi * b)];
+            out->cores[hi] = std::move(core);
+            rl[hi] = rnew;
+            rr[hi] = r_right;
+            p_rows = r_left * dims[lo];
+            if (!last) {
+                t_rows = cur.rows * rnew / p_rows;
+                t_cols = p_rows;
+            }
+        } else {
+            const int64_t n_lo = dims[lo];
+            std::vector<double> core((size_t)(r_left * n_lo * rnew));  // core_from_v (tt_svd.hpp:131-138)
+            for (int64_t b = 0; b < rnew; ++b)
+                for (int64_t x = 0; x < n_lo; ++x)
+                    for (int64_t a = 0; a < r_left; ++a) core[a + r_left * (x + n_lo * b)] = Vh[b * m + (a + r_left * x)];
+            out->cores[lo] = std::move(core);
+            rl[lo] = r_left;
+            rr[lo] = rnew;
+            p_rows = cur.rows;
+            if (last) {
+                t_rows = rnew;
+                t_cols = cur.rows;
+            } else {
+                t_cols = dims[hi] * r_right;
+                t_rows = rnew * cur.rows / t_cols;
+            }
+        }
+        const int64_t p_cols = cur.rows * rnew / p_rows, ldp = padded_stride_h(p_rows);
+        TT_TRY(ensure(ctx->ws_thick[1], (size_t)ldp * p_cols * 8));
+        double* P = as<double>(ctx->ws_thick[1]);
+        tm.mark(3);
+        TT_TRY(tsmm_device(ctx, cur.data, cur.rows, (int)m, cur.ld, d_V, m, (int)rnew, P, p_rows, p_cols, ldp));
+        tm.mark(4);
+        WorkView next{P, p_rows, p_cols, ldp};
+        if (t_rows > 0) {
+            const int64_t ldt = padded_stride_h(t_rows);
+            TT_TRY(ensure(ctx->ws_work[which], (size_t)ldt * t_cols * 8));
+            double* T = as<double>(ctx->ws_work[which]);
+            TT_TRY(transpose_reorder_device(ctx, P, p_rows, p_cols, ldp, T, t_rows, t_cols, ldt));
+            next = WorkView{T, t_rows, t_cols, ldt};
+            which ^= 1;
+        }
+        tm.mark(7);
+        if (tm.on) {
+            st.t_tsqr_ms = tm.ms(0, 1);
+            st.t_svd_ms = tm.ms(1, 2);
+            st.t_tsmm_ms = tm.ms(3, 4);
+            st.t_reorder_ms = tm.ms(4, 7);
+        }
+        out->steps.push_back(st);
+        out->sigmas.push_back(sig);
+        if (last) {
+            // the remaining middle core, in place (tt_svd.hpp:440-449, 478-489)
+            const int64_t j = right ? lo : hi;
+            const int64_t a = right ? r_left : rnew, b = right ? rnew : r_right;
+            TT_TRY(flat_d2h(ctx, next.data, next.rows, next.ld, a * dims[j] * b, flat));
+            out->cores[j] = flat;
+            rl[j] = a;
+            rr[j] = b;
+            break;
+        }
+        cur = next;
+        if (right) {
+            hi -= 1;
+            r_right = rnew;
+        } else {
+            lo += 1;
+            r_left = rnew;
+        }
+        right = !right;
+    }
+    out->ranks.assign(d + 1, 1);
+    for (int64_t j = 0; j < d; ++j) {
+        if (j > 0 && rr[j - 1] != rl[j]) return fail(TTSVD_ERR_DIMENSION_MISMATCH, "two-sided: rank chain broken");
+        out->ranks[j + 1] = rr[j];
+    }
+    return TTSVD_OK;
+}
+
 }  // namespace
 
 // =========================================================================
@@ -1346,6 +1519,66 @@ int ttsvd_cu_tt_svd(ttsvd_cu_ctx* ctx, const double* X, const int64_t* dims, int
     }
     *out = tt;
     return TTSVD_OK;
+}
+
+int ttsvd_cu_run_chain(ttsvd_cu_ctx* ctx, const double* W, int64_t rows, int64_t cols, int64_t ldw, const int64_t* dims,
+                       int64_t d, int64_t r_max, double eps, int64_t d_for_delta, double* delta_io,
+                       double* first_sigma_norm_out, ttsvd_cu_tt** out) {
+    TT_TRY(set_device(ctx));
+    if (!out || !dims || !W || !delta_io) return fail(TTSVD_ERR_INVALID, "run_chain: null argument");
+    *out = nullptr;
+    if (d < 2) return fail(TTSVD_ERR_DEGENERATE, "run_chain: requires d >= 2");
+    int64_t total = 1;
+    for (int64_t i = 0; i < d; ++i) {
+        if (dims[i] < 1) return fail(TTSVD_ERR_DIMENSION, "Shape: extents must be >= 1");
+        total *= dims[i];
+    }
+    if (cols != dims[d - 1] || rows * cols != total) return fail(TTSVD_ERR_SHAPE, "run_chain: W is not the last-mode matricization");
+    if (ldw < rows) return fail(TTSVD_ERR_LAYOUT, "run_chain: leading stride below the row count");
+    auto* tt = new ttsvd_cu_tt();
+    double fsn = 0.0;
+    int rc = run_chain(ctx, WorkView{W, rows, cols, ldw}, std::vector<int64_t>(dims, dims + d), r_max, eps, d_for_delta,
+                       tt, delta_io, &fsn);
+    if (rc != TTSVD_OK) {
+        delete tt;
+        return rc;
+    }
+    if (first_sigma_norm_out) *first_sigma_norm_out = fsn;
+    *out = tt;
+    return TTSVD_OK;
+}
+
+int ttsvd_cu_tt_svd_two_sided(ttsvd_cu_ctx* ctx, const double* X, const int64_t* dims, int64_t d, int64_t ldx,
+                              int64_t r_max, double eps, ttsvd_cu_tt** out) {
+    TT_TRY(set_device(ctx));
+    if (!out || !dims || !X) return fail(TTSVD_ERR_INVALID, "tt_svd_two_sided: null argument");
+    *out = nullptr;
+    if (d < 2) return fail(TTSVD_ERR_DEGENERATE, "tt_svd_two_sided: requires d >= 2");
+    int64_t total = 1;
+    for (int64_t i = 0; i < d; ++i) {
+        if (dims[i] < 1) return fail(TTSVD_ERR_DIMENSION, "Shape: extents must be >= 1");
+        total *= dims[i];
+    }
+    const int64_t rows = total / dims[d - 1];
+    if (ldx < rows) return fail(TTSVD_ERR_LAYOUT, "tt_svd_two_sided: leading stride below the row count");
+    auto* tt = new ttsvd_cu_tt();
+    int rc = run_two_sided(ctx, WorkView{X, rows, dims[d - 1], ldx}, std::vector<int64_t>(dims, dims + d), r_max, eps, tt);
+    if (rc != TTSVD_OK) {
+        delete tt;
+        return rc;
+    }
+    *out = tt;
+    return TTSVD_OK;
+}
+
+int ttsvd_cu_transpose_reorder(ttsvd_cu_ctx* ctx, const double* W, int64_t n, int64_t m, int64_t ldw, double* Y,
+                               int64_t out_rows, int64_t out_cols, int64_t ldy) {
+    TT_TRY(set_device(ctx));
+    if (out_rows < 1 || out_cols < 1 || out_rows * out_cols != n * m)
+        return fail(TTSVD_ERR_SHAPE, "transpose_reorder: out shape does not hold n*m elements");
+    if (!W || !Y || n < 1 || m < 1 || ldw < n || ldy < out_rows)
+        return fail(TTSVD_ERR_INVALID, "transpose_reorder: bad pointer or leading dimension");
+    return transpose_reorder_device(ctx, W, n, m, ldw, Y, out_rows, out_cols, ldy);
 }
 
 int ttsvd_cu_choose_combined_dims(const int64_t* dims, int64_t d, int64_t m_min, double f1_min, const int64_t* r_tilde,

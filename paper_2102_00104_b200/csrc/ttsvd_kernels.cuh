@@ -830,6 +830,38 @@ __global__ void __launch_bounds__(256) tsmm_dmma_kernel(const double* __restrict
     }
 }
 
+// ---------------------------------------------------------------------------
+// transpose_reorder (tsmm.hpp:84-126, the two-sided sweep's reorder): W (n x m,
+// ld ldw) is flattened as W^T, i.e. W(i, j) goes to flat position p = m i + j,
+// which is Y(p mod out_rows, p div out_rows).  A pure permutation, HBM-bound
+// (16 n m bytes).  A 32 x 32 tile is read along W's columns (coalesced) into
+// shared memory and written along W's rows: for a fixed i the 32 values of
+// j are 32 consecutive flat positions, i.e. a contiguous run of Y (split at
+// most once where it crosses an out_rows boundary).  Grid-stride over tiles.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) transpose_reorder_kernel(const double* __restrict__ W, int64_t n, int64_t m,
+                                                                int64_t ldw, double* __restrict__ Y,
+                                                                int64_t out_rows, int64_t ldy) {
+    __shared__ double tile[32][33];
+    const int64_t ti = (n + 31) / 32, tj = (m + 31) / 32;
+    for (int64_t t = blockIdx.x; t < ti * tj; t += gridDim.x) {
+        const int64_t i0 = (t % ti) * 32, j0 = (t / ti) * 32;
+        for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+            const int64_t i = i0 + threadIdx.x, j = j0 + k;
+            if (i < n && j < m) tile[k][threadIdx.x] = W[j * ldw + i];
+        }
+        __syncthreads();
+        for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+            const int64_t i = i0 + k, j = j0 + threadIdx.x;
+            if (i < n && j < m) {
+                const int64_t p = m * i + j;
+                Y[(p / out_rows) * ldy + p % out_rows] = tile[threadIdx.x][k];
+            }
+        }
+        __syncthreads();
+    }
+}
+
 // zero rows [out_rows, ldy) of every column of Y (the padded slots, storage.hpp:57)
 __global__ void zero_padding_kernel(double* Y, int64_t out_rows, int64_t ldy, int64_t cols) {
     const int64_t pad = ldy - out_rows;

@@ -391,6 +391,7 @@ class StepRecord:
     t_tsqr_sweep: float = 0.0  # the TSQR main sweep kernel alone (diagnostics)
     tsqr_kernel: str = "none"
     svd_sweeps: int = 0
+    t_reorder: float = 0.0
 
 
 @dataclass
@@ -439,7 +440,8 @@ def _collect(handle: C.c_void_p) -> TensorTrain:
             steps.append(StepRecord(s + 1, st.rows, st.cols, st.rank, st.nsig,
                                     st.rank / st.cols if st.cols else 0.0, st.t_tsqr_ms * 1e-3, st.t_svd_ms * 1e-3,
                                     st.t_tsmm_ms * 1e-3, st.t_tsqr_sweep_ms * 1e-3,
-                                    _lib.TSQR_KERNELS.get(st.tsqr_kernel, "?"), st.svd_sweeps))
+                                    _lib.TSQR_KERNELS.get(st.tsqr_kernel, "?"), st.svd_sweeps,
+                                    st.t_reorder_ms * 1e-3))
             tt.sigmas.append(sig)
         tt.steps = steps
         return tt, ranks
@@ -500,6 +502,43 @@ def tt_svd_tsqr(X, dims, spec: TruncationSpec | tuple | None = None, ctx_exec=No
         _check(L.ttsvd_cu_tt_svd_host(ctx.handle, a.ctypes.data, dv.ctypes.data_as(_lib.i64p), d, ld, r_max,
                                       float(spec.eps), C.byref(h)))
     return _finish(h, dims)
+
+
+def tt_svd_two_sided(X, dims, spec: TruncationSpec | tuple | None = None) -> TensorTrain:
+    """tt_svd.hpp:402-512 (Alg. 4) on a device tensor in the padded layout
+    (host numpy buffers are staged to the device first)."""
+    spec = _spec(spec)
+    dims = [int(x) for x in dims]
+    d = len(dims)
+    if d < 2:
+        raise DegenerateDimension("tt_svd_two_sided: requires d >= 2")
+    X = to_device_matrix(X)
+    dv = np.asarray(dims, dtype=np.int64)
+    ctx = context(X.device.index)
+    p, rows, cols, ld = _mat(X)
+    h = C.c_void_p()
+    _check(_lib.lib().ttsvd_cu_tt_svd_two_sided(ctx.handle, p, dv.ctypes.data_as(_lib.i64p), d, ld,
+                                                int(spec.r_max), float(spec.eps), C.byref(h)))
+    return _finish(h, dims)
+
+
+def transpose_reorder(W, out_rows: int | None = None, out_cols: int | None = None, workers: int = 1,
+                      counters=None) -> torch.Tensor:
+    """tsmm.hpp:84-126 (default shape: the plain transpose, :121-125) — the
+    padded (out_rows x out_cols) result, ld = padded_stride(out_rows)."""
+    W = to_device_matrix(W)
+    pw, n, m, ldw = _mat(W)
+    if out_rows is None:
+        out_rows, out_cols = m, n
+    if out_rows < 1 or out_cols < 1 or out_rows * out_cols != n * m:
+        raise ShapeError("transpose_reorder: out shape does not hold n*m elements")
+    ldy = padded_stride(out_rows)
+    Y = fortran_empty(out_rows, out_cols, ld=ldy)
+    ctx = context(W.device.index)
+    _check(_lib.lib().ttsvd_cu_transpose_reorder(ctx.handle, pw, n, m, ldw, Y.data_ptr(), out_rows, out_cols, ldy))
+    if counters is not None:
+        counters.add(0, 16 * n * m)
+    return Y
 
 
 @dataclass
