@@ -6,6 +6,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <vector>
 
 #include "ttsvd_b200.hpp"
 
@@ -70,6 +71,30 @@ int main(int argc, char** argv) {
     TriangularFactor R = tsqr(M.view(), BlockParams::for_cols(4), 1);
     for (index_t j = 0; j < 4; ++j)
         if (std::abs(std::abs(R(j, j)) - 1.0) > 1e-14) return 5;
+    // Alg. 5 over the GPUs of this process (NCCL inside the library) must
+    // agree bitwise with the in-process form: 4 partitions on device 0
+    {
+        int ndev = 0;
+        cudaGetDeviceCount(&ndev);
+        std::vector<DenseTensor> slabs;
+        for (int p = 0; p < 4; ++p) {
+            DenseTensor s(Shape{4, 4, 4, 4, 4, 4, 4});
+            for (index_t l = 0; l < s.total(); ++l) s.at_flat(l) = X.at_flat(p + 4 * (l % 4) + 16 * (l / 4) % X.total());
+            slabs.push_back(std::move(s));
+        }
+        std::vector<TensorTrain> parts;
+        const TensorTrain a = tt_svd_distributed(slabs, spec, ExecContext{}, &parts);
+        const TensorTrain b = tt_svd_distributed(slabs, std::vector<int>{0}, spec);
+        if (a.ranks() != b.ranks()) return 10;
+        for (std::size_t j = 0; j < a.cores.size(); ++j)
+            if (a.cores[j].data != b.cores[j].data) return 11;
+        if (parts.size() != 4 || parts[1].cores.front().r_left != 1 || parts[1].cores.front().n != 1) return 12;
+        if (ndev >= 2) {  // one partition pair per device
+            const TensorTrain c = tt_svd_distributed(slabs, std::vector<int>{0, 1}, spec);
+            for (std::size_t j = 1; j < a.cores.size(); ++j)
+                if (a.cores[j].data != c.cores[j].data) return 13;
+        }
+    }
     std::printf("device entry points ok\n");
     return 0;
 }

@@ -439,4 +439,63 @@ inline TensorTrain tt_svd_distributed(const std::vector<DenseTensor>& slabs, Tru
     return tt;
 }
 
+// Alg. 5 across the GPUs of this process: partition p of P = slabs.size()
+// lives on devices[p / (P / D)] (D = devices.size() must divide P); the
+// library attaches an NCCL communicator over the devices (ncclCommInitAll)
+// and runs one host thread per device, all-gathering the R factors with
+// ncclAllGather.  Same result contract as the in-process overload.
+inline TensorTrain tt_svd_distributed(const std::vector<DenseTensor>& slabs, const std::vector<int>& devices,
+                                      TruncationSpec spec, const ExecContext& ctx = {},
+                                      std::vector<TensorTrain>* per_partition = nullptr) {
+    if (slabs.empty() || devices.empty()) throw PartitionMismatch("tt_svd_distributed: no partitions or devices");
+    const Shape& local = slabs.front().shape();
+    for (const DenseTensor& s : slabs)
+        if (!(s.shape() == local)) throw PartitionMismatch("tt_svd_distributed: slab shapes differ");
+    const int D = static_cast<int>(devices.size());
+    const index_t P = static_cast<index_t>(slabs.size());
+    if (P % D) throw PartitionMismatch("tt_svd_distributed: the device count must divide the partition count");
+    int prev = 0;
+    b200::cuda(cudaGetDevice(&prev));
+    struct Ctxs {
+        std::vector<ttsvd_cu_ctx*> c;
+        ~Ctxs() {
+            for (ttsvd_cu_ctx* x : c) ttsvd_cu_ctx_destroy(x);
+        }
+    } ctxs;
+    std::vector<b200::DeviceBuffer> bufs;
+    std::vector<const double*> ptrs;
+    for (index_t p = 0; p < P; ++p) {
+        const int dev = devices[static_cast<std::size_t>(p / (P / D))];
+        if (p % (P / D) == 0) {
+            ttsvd_cu_ctx* c = nullptr;
+            b200::check(ttsvd_cu_ctx_create(dev, nullptr, &c));
+            ctxs.c.push_back(c);
+        }
+        b200::cuda(cudaSetDevice(dev));
+        bufs.push_back(b200::stage(slabs[static_cast<std::size_t>(p)]));
+        ptrs.push_back(bufs.back().get());
+    }
+    b200::check(ttsvd_cu_ctx_comm_init_all(ctxs.c.data(), D));
+    b200::Result res;
+    b200::check(ttsvd_cu_tt_svd_distributed_devices(ctxs.c.data(), D, ptrs.data(), P / D, local.dims().data(),
+                                                    local.d(), slabs.front().leading_stride(), spec.r_max, spec.eps,
+                                                    res.out()));
+    b200::cuda(cudaSetDevice(prev));
+    b200::account(res, ctx);
+    std::vector<index_t> gdims{P};
+    gdims.insert(gdims.end(), local.dims().begin(), local.dims().end());
+    TensorTrain tt = res.train(gdims);
+    tt.validate();
+    if (per_partition) {
+        per_partition->assign(static_cast<std::size_t>(P), tt);
+        const TTCore& first = tt.cores.front();
+        for (index_t p = 0; p < P && P > 1; ++p) {
+            TTCore own(1, 1, first.r_right);
+            for (index_t b = 0; b < first.r_right; ++b) own(0, 0, b) = first(0, p, b);
+            (*per_partition)[static_cast<std::size_t>(p)].cores.front() = std::move(own);
+        }
+    }
+    return tt;
+}
+
 }  // namespace ttsvd

@@ -182,6 +182,28 @@ int ttsvd_cu_tt_svd_distributed(ttsvd_cu_ctx* ctx, const double* const* slabs, i
                                 int64_t r_max, double eps, ttsvd_cu_exchange_fn exchange, void* user,
                                 ttsvd_cu_tt** out);
 
+/* ---- multi-GPU: NCCL inside the library --------------------------------- */
+/* Replaces the in-process combine of tt_svd.hpp:568-575 across GPUs (Alg. 5's
+ * MPI_Allreduce, becomes an all-gather of the R factors +
+ * the pinned-order merge).  libnccl.so.2 is loaded on first use. */
+#define TTSVD_COMM_ID_BYTES 128
+/* a fresh NCCL unique id (128 bytes) — create on one rank, broadcast it */
+int ttsvd_cu_comm_unique_id(void* id_out);
+/* one process per GPU: attach an NCCL communicator (nranks, rank) to ctx.
+ * ttsvd_cu_tt_svd_distributed with exchange == NULL then all-gathers over it
+ * on the context's stream; rank k must own partitions k*n_slabs .. */
+int ttsvd_cu_ctx_comm_init(ttsvd_cu_ctx* ctx, const void* unique_id, int nranks, int rank);
+/* one process driving ndev GPUs (one context per device): ncclCommInitAll */
+int ttsvd_cu_ctx_comm_init_all(ttsvd_cu_ctx* const* ctxs, int ndev);
+/* Alg. 5 over ndev GPUs of this process, one host thread per device: device i
+ * owns slabs[i*slabs_per_device ..] (device pointers on that device, each the
+ * padded layout of ldims with leading stride ld_slab).  Needs
+ * ttsvd_cu_ctx_comm_init_all on ctxs.  Result as ttsvd_cu_tt_svd_distributed
+ * (first core (1, P, r), P = ndev * slabs_per_device). */
+int ttsvd_cu_tt_svd_distributed_devices(ttsvd_cu_ctx* const* ctxs, int ndev, const double* const* slabs,
+                                        int64_t slabs_per_device, const int64_t* ldims, int64_t d_local,
+                                        int64_t ld_slab, int64_t r_max, double eps, ttsvd_cu_tt** out);
+
 /* ---- results ----------------------------------------------------------- */
 int64_t ttsvd_cu_tt_d(const ttsvd_cu_tt* tt);
 int ttsvd_cu_tt_ranks(const ttsvd_cu_tt* tt, int64_t* ranks /* d+1 */);
@@ -196,6 +218,12 @@ void ttsvd_cu_tt_free(ttsvd_cu_tt* tt);
 /* ---- synthetic inputs (off the timed path) ------------------------------ */
 /* Counter-based uniform[-1,1) tensor (restated bit-exactly in the oracle). */
 int ttsvd_cu_gen_uniform(ttsvd_cu_ctx* ctx, uint64_t seed, int64_t total, int64_t rows, int64_t ld, double* X);
+/* Partition `part` of `nparts` of a counter-based tensor: local flat entry l
+ * is global entry part + nparts*l (split_first_dim, ttsvd_bench.cpp:72-86), so
+ * every partition count generates the same global tensor.  kind 0: X = 2u-1
+ * (gen_uniform when nparts == 1); kind 1: X += scale * N(0,1) (Box-Muller). */
+int ttsvd_cu_gen_partition(ttsvd_cu_ctx* ctx, uint64_t seed, int kind, double scale, int64_t total_local,
+                           int64_t rows, int64_t ld, int64_t nparts, int64_t part, double* X);
 
 #ifdef __cplusplus
 }

@@ -11,7 +11,8 @@ from .ttsvd import (AllocationError, BlockParams, Context, ConvergenceError, Deg
                     PartitionMismatch, ShapeError, SmallSVD, StepRecord, TensorTrain, ThickBoundsParams, TruncationSpec,
                     TTCore, choose_combined_dims, combine_factors, context, derive_delta, driver_svd, fortran_empty, gen_uniform, jacobi_svd, padded_stride,
                     reduce_block, select_rank, small_svd, to_device_matrix, to_host, transpose_reorder, tsmm_reshape, tsqr,
-                    tt_svd_distributed, tt_svd_thick_bounds, tt_svd_tsqr, tt_svd_two_sided)
+                    tt_svd_distributed, tt_svd_distributed_devices, tt_svd_thick_bounds, tt_svd_tsqr,
+                    tt_svd_two_sided, gen_partition)
 from .wire import dump_tensor, emit_csv, load_tensor, load_tt, parse_csv, report_rows, save_tt
 from . import verify  # noqa: F401  (device tt_error / check_orthonormality)
 

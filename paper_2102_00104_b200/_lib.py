@@ -66,6 +66,12 @@ _SIGS = {
     "ttsvd_cu_tt_svd_host": (C.c_int, [C.c_void_p, dptr, i64p, i64, i64, i64, C.c_double, C.POINTER(C.c_void_p)]),
     "ttsvd_cu_tt_svd_distributed": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p), i64, i64, i64, i64p, i64, i64, i64,
                                               C.c_double, EXCHANGE_FN, C.c_void_p, C.POINTER(C.c_void_p)]),
+    "ttsvd_cu_comm_unique_id": (C.c_int, [C.c_void_p]),
+    "ttsvd_cu_ctx_comm_init": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_int]),
+    "ttsvd_cu_ctx_comm_init_all": (C.c_int, [C.POINTER(C.c_void_p), C.c_int]),
+    "ttsvd_cu_tt_svd_distributed_devices": (C.c_int, [C.POINTER(C.c_void_p), C.c_int, C.POINTER(C.c_void_p), i64, i64p,
+                                                      i64, i64, i64, C.c_double, C.POINTER(C.c_void_p)]),
+    "ttsvd_cu_gen_partition": (C.c_int, [C.c_void_p, C.c_uint64, C.c_int, C.c_double, i64, i64, i64, i64, i64, dptr]),
     "ttsvd_cu_tt_d": (i64, [C.c_void_p]),
     "ttsvd_cu_tt_ranks": (C.c_int, [C.c_void_p, i64p]),
     "ttsvd_cu_tt_core": (C.c_int, [C.c_void_p, i64, C.c_void_p]),

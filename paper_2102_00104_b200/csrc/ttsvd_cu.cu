@@ -6,6 +6,8 @@
 // and launches the sm_100a kernels of ttsvd_kernels.cuh.  There is no CPU
 // fallback anywhere in this library: every numeric step runs on the device.
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>  // types only: libnccl.so.2 is dlopen'ed on first use
 
 #include <algorithm>
 #include <cfloat>
@@ -14,7 +16,9 @@
 #include <cstring>
 #include <cstdlib>
 #include <map>
+#include <mutex>
 #include <string>
+#include <thread>
 #include <tuple>
 #include <vector>
 
@@ -85,6 +89,10 @@ struct ttsvd_cu_ctx {
     // are cached per context (one device each), never process-wide
     std::map<const void*, int> smem_attr;
     std::map<std::tuple<const void*, int, size_t>, int> occ;
+    // NCCL communicator of a distributed run (ttsvd_cu_ctx_comm_init*):
+    // tt_svd_distributed all-gathers the R factors over it on `stream`
+    ncclComm_t comm = nullptr;
+    int comm_rank = 0, comm_size = 1;
 };
 
 struct ttsvd_cu_tt {
@@ -121,6 +129,48 @@ template <class T>
 T* as(DevBuf& b) {
     return static_cast<T*>(b.p);
 }
+
+// ---- NCCL, loaded at run time (the single-GPU path never needs it) -------
+struct NcclApi {
+    bool ok = false;
+    std::string why;
+    ncclResult_t (*get_unique_id)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*comm_init_rank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*comm_init_all)(ncclComm_t*, int, const int*) = nullptr;
+    ncclResult_t (*all_gather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*comm_destroy)(ncclComm_t) = nullptr;
+    const char* (*error_string)(ncclResult_t) = nullptr;
+};
+
+const NcclApi& nccl() {
+    static NcclApi api;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        // the libnccl.so.2 already in the process (e.g. torch's) is reused by soname
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) {
+            api.why = std::string("libnccl.so.2 not loadable: ") + dlerror();
+            return;
+        }
+        auto sym = [&](const char* n) { return dlsym(h, n); };
+        api.get_unique_id = reinterpret_cast<decltype(api.get_unique_id)>(sym("ncclGetUniqueId"));
+        api.comm_init_rank = reinterpret_cast<decltype(api.comm_init_rank)>(sym("ncclCommInitRank"));
+        api.comm_init_all = reinterpret_cast<decltype(api.comm_init_all)>(sym("ncclCommInitAll"));
+        api.all_gather = reinterpret_cast<decltype(api.all_gather)>(sym("ncclAllGather"));
+        api.comm_destroy = reinterpret_cast<decltype(api.comm_destroy)>(sym("ncclCommDestroy"));
+        api.error_string = reinterpret_cast<decltype(api.error_string)>(sym("ncclGetErrorString"));
+        api.ok = api.get_unique_id && api.comm_init_rank && api.comm_init_all && api.all_gather && api.comm_destroy &&
+                 api.error_string;
+        if (!api.ok) api.why = "libnccl.so.2 lacks a required symbol";
+    });
+    return api;
+}
+
+#define TT_NCCL(call)                                                                                     \
+    do {                                                                                                  \
+        const ncclResult_t r_ = (call);                                                                   \
+        if (r_ != ncclSuccess) return fail(TTSVD_ERR_DEVICE, std::string(#call) + ": " + nccl().error_string(r_)); \
+    } while (0)
 
 int64_t padded_stride_h(int64_t n) {
     if (n < 1) return -1;
@@ -1354,6 +1404,7 @@ int ttsvd_cu_ctx_destroy(ttsvd_cu_ctx* ctx) {
         if (b.p) cudaFree(b.p);
     if (ctx->host_stage.p) cudaFreeHost(ctx->host_stage.p);
     if (ctx->host_cores.p) cudaFreeHost(ctx->host_cores.p);
+    if (ctx->comm && nccl().ok) nccl().comm_destroy(ctx->comm);
     for (auto& e : ctx->ev)
         if (e) cudaEventDestroy(e);
     delete ctx;
@@ -1724,8 +1775,24 @@ int ttsvd_cu_tt_svd_distributed(ttsvd_cu_ctx* ctx, const double* const* slabs, i
     *out = nullptr;
     if (P_total < n_slabs || part0 < 0 || part0 + n_slabs > P_total || P_total % n_slabs != 0)
         return fail(TTSVD_ERR_PARTITION, "tt_svd_distributed: inconsistent partition counts");
-    if (n_slabs != P_total && !exchange)
-        return fail(TTSVD_ERR_INVALID, "tt_svd_distributed: exchange callback required across processes");
+    // the exchange: a caller's callback, else the context's NCCL communicator
+    // (ranks own consecutive partitions: rank k holds k*n_slabs ..), else
+    // none (every partition in this process, the reference's in-process form)
+    const bool use_nccl = !exchange && ctx->comm;
+    if (use_nccl && (P_total != n_slabs * ctx->comm_size || part0 != (int64_t)ctx->comm_rank * n_slabs))
+        return fail(TTSVD_ERR_PARTITION, "tt_svd_distributed: partitions do not match the communicator's ranks");
+    if (n_slabs != P_total && !exchange && !use_nccl)
+        return fail(TTSVD_ERR_INVALID, "tt_svd_distributed: an exchange (callback or NCCL communicator) is required across processes");
+    const bool exchanged = exchange || use_nccl;
+    auto all_gather = [&](const double* send, double* recv, int64_t count) -> int {
+        if (use_nccl) {
+            TT_NCCL(nccl().all_gather(send, recv, (size_t)count, ncclDouble, ctx->comm, ctx->stream));
+            return TTSVD_OK;
+        }
+        if (exchange(user, send, recv, count, (void*)ctx->stream) != 0)
+            return fail(TTSVD_ERR_DEVICE, "tt_svd_distributed: exchange failed");
+        return TTSVD_OK;
+    };
     const int64_t d = d_local + 1;
     int64_t total = 1;
     for (int64_t i = 0; i < d_local; ++i) total *= ldims[i];
@@ -1741,7 +1808,7 @@ int ttsvd_cu_tt_svd_distributed(ttsvd_cu_ctx* ctx, const double* const* slabs, i
         *out = tt;
         return (int)TTSVD_OK;
     };
-    if (P_total == 1) {
+    if (P_total == 1) {  // one partition: tt_svd_tsqr of (1, n_1, ...) (tt_svd.hpp:530-541)
         gdims[0] = 1;
         const int64_t rows = d_local == 1 ? 1 : total / ldims[d_local - 1];
         return done(run_chain(ctx, WorkView{slabs[0], rows, ldims[d_local - 1], ld_slab}, gdims, r_max, eps, d, tt));
@@ -1761,7 +1828,29 @@ int ttsvd_cu_tt_svd_distributed(ttsvd_cu_ctx* ctx, const double* const* slabs, i
     double delta = -1.0;
     int64_t r = 1;
     int flip = 0;
-    std::vector<double> sig, Vh;
+    std::vector<double> sig;
+    // the steps' V blocks go to the pinned core arena asynchronously and the
+    // cores are built after the sweep (as run_chain: one host round trip per
+    // step, for the sigmas the rank rule needs)
+    struct Pending {
+        int64_t i, m, rnew, n_i, r;
+        size_t off;
+    };
+    std::vector<Pending> pending;
+    size_t core_off = 0;
+    auto flush = [&]() {
+        const double* base = as<double>(ctx->host_cores);
+        for (const Pending& pc : pending) {
+            std::vector<double> core((size_t)(pc.rnew * pc.n_i * pc.r));
+            for (int64_t b = 0; b < pc.r; ++b)
+                for (int64_t x = 0; x < pc.n_i; ++x)
+                    for (int64_t a = 0; a < pc.rnew; ++a)
+                        core[a + pc.rnew * (x + pc.n_i * b)] = base[pc.off + a * pc.m + (x + pc.n_i * b)];
+            tt->cores[pc.i + 1] = std::move(core);
+        }
+        pending.clear();
+        core_off = 0;
+    };
     int rc = TTSVD_OK;
     for (int64_t i = d_local - 1; i >= 0 && rc == TTSVD_OK; --i) {
         const int64_t n_i = ldims[i];
@@ -1770,17 +1859,12 @@ int ttsvd_cu_tt_svd_distributed(ttsvd_cu_ctx* ctx, const double* const* slabs, i
         if ((rc = ensure(ctx->ws_send, n_slabs * mm * 8)) != TTSVD_OK) break;
         if ((rc = ensure(ctx->ws_recv, P_total * mm * 8)) != TTSVD_OK) break;
         double* send = as<double>(ctx->ws_send);
-        double* recv = n_slabs == P_total ? send : as<double>(ctx->ws_recv);
+        double* recv = exchanged ? as<double>(ctx->ws_recv) : send;
         // gram_triangular per local partition (tt_svd.hpp:204-210, 573)
         for (int64_t p = 0; p < n_slabs && rc == TTSVD_OK; ++p)
             rc = tsqr_device(ctx, cur[p].data, cur[p].rows, (int)m, cur[p].ld, send + p * mm);
         if (rc != TTSVD_OK) break;
-        if (n_slabs != P_total) {
-            if (exchange(user, send, recv, (int64_t)(n_slabs * mm), (void*)ctx->stream) != 0) {
-                rc = fail(TTSVD_ERR_DEVICE, "tt_svd_distributed: exchange failed");
-                break;
-            }
-        }
+        if (exchanged && (rc = all_gather(send, recv, (int64_t)(n_slabs * mm))) != TTSVD_OK) break;
         // pinned-order combine over all partitions (tt_svd.hpp:575)
         if ((rc = ensure(ctx->ws_X, mm * 8)) != TTSVD_OK) break;
         double* R = as<double>(ctx->ws_X);
@@ -1800,13 +1884,20 @@ int ttsvd_cu_tt_svd_distributed(ttsvd_cu_ctx* ctx, const double* const* slabs, i
         if (delta < 0.0) delta = eps / std::sqrt((double)(d - 1)) * sigma_norm_h(sig.data(), m);
         const int64_t rnew = choose_rank_h(sig.data(), m, m, nsig, delta, r_max, global_rows);
         if ((rc = svd_vectors(ctx, rnew, d_sigma, d_V)) != TTSVD_OK) break;
-        Vh.resize((size_t)m * rnew);
-        if ((rc = d2h(ctx, Vh.data(), d_V, (size_t)m * rnew)) != TTSVD_OK) break;
-        std::vector<double> core((size_t)(rnew * n_i * r));
-        for (int64_t b = 0; b < r; ++b)
-            for (int64_t x = 0; x < n_i; ++x)
-                for (int64_t a = 0; a < rnew; ++a) core[a + rnew * (x + n_i * b)] = Vh[a * m + (x + n_i * b)];
-        tt->cores[i + 1] = std::move(core);
+        {
+            const size_t need = (size_t)m * rnew;
+            if (core_off + need > ctx->host_cores.bytes / 8) {
+                cudaError_t e = cudaStreamSynchronize(ctx->stream);
+                if (e != cudaSuccess) { rc = fail(TTSVD_ERR_DEVICE, cudaGetErrorString(e)); break; }
+                flush();
+                if ((rc = ensure_host(ctx->host_cores, std::max<size_t>(need, (size_t)1 << 20) * 8 * 2)) != TTSVD_OK) break;
+            }
+            cudaError_t e = cudaMemcpyAsync(as<double>(ctx->host_cores) + core_off, d_V, need * 8,
+                                            cudaMemcpyDeviceToHost, ctx->stream);
+            if (e != cudaSuccess) { rc = fail(TTSVD_ERR_DEVICE, cudaGetErrorString(e)); break; }
+            pending.push_back(Pending{i, m, rnew, n_i, r, core_off});
+            core_off += need;
+        }
         tt->ranks[i + 1] = rnew;
         ttsvd_cu_step st{};
         st.rows = global_rows;
@@ -1840,14 +1931,14 @@ int ttsvd_cu_tt_svd_distributed(ttsvd_cu_ctx* ctx, const double* const* slabs, i
             if (e != cudaSuccess) rc = fail(TTSVD_ERR_DEVICE, cudaGetErrorString(e));
         }
         double* recv = send;
-        if (rc == TTSVD_OK && n_slabs != P_total) {
+        if (rc == TTSVD_OK && exchanged) {
             recv = as<double>(ctx->ws_recv);
-            if (exchange(user, send, recv, (int64_t)cnt, (void*)ctx->stream) != 0)
-                rc = fail(TTSVD_ERR_DEVICE, "tt_svd_distributed: exchange failed");
+            rc = all_gather(send, recv, (int64_t)cnt);
         }
         std::vector<double> vals((size_t)P_total * r);
-        if (rc == TTSVD_OK) rc = d2h(ctx, vals.data(), recv, vals.size());
+        if (rc == TTSVD_OK) rc = d2h(ctx, vals.data(), recv, vals.size());  // synchronises: the V blocks have landed
         if (rc == TTSVD_OK) {
+            flush();
             std::vector<double> first((size_t)P_total * r);
             for (int64_t p = 0; p < P_total; ++p)
                 for (int64_t b = 0; b < r; ++b) first[p + P_total * b] = vals[p * r + b];
@@ -1858,8 +1949,85 @@ int ttsvd_cu_tt_svd_distributed(ttsvd_cu_ctx* ctx, const double* const* slabs, i
         }
     }
     cudaStreamSynchronize(ctx->stream);
-    (void)part0;
     return done(rc);
+}
+
+int ttsvd_cu_comm_unique_id(void* id_out) {
+    if (!id_out) return fail(TTSVD_ERR_INVALID, "comm_unique_id: null out");
+    if (!nccl().ok) return fail(TTSVD_ERR_DEVICE, nccl().why);
+    ncclUniqueId id;
+    TT_NCCL(nccl().get_unique_id(&id));
+    static_assert(sizeof(ncclUniqueId) == TTSVD_COMM_ID_BYTES, "NCCL unique id size");
+    std::memcpy(id_out, &id, sizeof id);
+    return TTSVD_OK;
+}
+
+int ttsvd_cu_ctx_comm_init(ttsvd_cu_ctx* ctx, const void* unique_id, int nranks, int rank) {
+    TT_TRY(set_device(ctx));
+    if (!unique_id || nranks < 1 || rank < 0 || rank >= nranks) return fail(TTSVD_ERR_INVALID, "comm_init: bad arguments");
+    if (!nccl().ok) return fail(TTSVD_ERR_DEVICE, nccl().why);
+    if (ctx->comm) nccl().comm_destroy(ctx->comm);
+    ctx->comm = nullptr;
+    ncclUniqueId id;
+    std::memcpy(&id, unique_id, sizeof id);
+    TT_NCCL(nccl().comm_init_rank(&ctx->comm, nranks, id, rank));
+    ctx->comm_rank = rank;
+    ctx->comm_size = nranks;
+    return TTSVD_OK;
+}
+
+int ttsvd_cu_ctx_comm_init_all(ttsvd_cu_ctx* const* ctxs, int ndev) {
+    if (!ctxs || ndev < 1) return fail(TTSVD_ERR_INVALID, "comm_init_all: bad arguments");
+    if (!nccl().ok) return fail(TTSVD_ERR_DEVICE, nccl().why);
+    std::vector<int> devs(ndev);
+    for (int i = 0; i < ndev; ++i) {
+        if (!ctxs[i]) return fail(TTSVD_ERR_INVALID, "comm_init_all: null context");
+        devs[i] = ctxs[i]->device;
+        if (ctxs[i]->comm) nccl().comm_destroy(ctxs[i]->comm);
+        ctxs[i]->comm = nullptr;
+    }
+    std::vector<ncclComm_t> comms(ndev);
+    TT_NCCL(nccl().comm_init_all(comms.data(), ndev, devs.data()));
+    for (int i = 0; i < ndev; ++i) {
+        ctxs[i]->comm = comms[i];
+        ctxs[i]->comm_rank = i;
+        ctxs[i]->comm_size = ndev;
+    }
+    return TTSVD_OK;
+}
+
+int ttsvd_cu_tt_svd_distributed_devices(ttsvd_cu_ctx* const* ctxs, int ndev, const double* const* slabs,
+                                        int64_t slabs_per_device, const int64_t* ldims, int64_t d_local,
+                                        int64_t ld_slab, int64_t r_max, double eps, ttsvd_cu_tt** out) {
+    if (!ctxs || ndev < 1 || !slabs || slabs_per_device < 1 || !out)
+        return fail(TTSVD_ERR_INVALID, "tt_svd_distributed_devices: bad arguments");
+    *out = nullptr;
+    for (int i = 0; i < ndev; ++i)
+        if (!ctxs[i] || !ctxs[i]->comm || ctxs[i]->comm_size != ndev || ctxs[i]->comm_rank != i)
+            return fail(TTSVD_ERR_INVALID, "tt_svd_distributed_devices: contexts need ttsvd_cu_ctx_comm_init_all");
+    // one host thread per device (SURVEY §8 e topology); the shared cores come
+    // out bitwise identical on every device, device 0's train is returned
+    const int64_t P = (int64_t)ndev * slabs_per_device;
+    std::vector<ttsvd_cu_tt*> res(ndev, nullptr);
+    std::vector<int> rcs(ndev, TTSVD_OK);
+    std::vector<std::string> msgs(ndev);
+    std::vector<std::thread> pool;
+    for (int i = 0; i < ndev; ++i)
+        pool.emplace_back([&, i] {
+            rcs[i] = ttsvd_cu_tt_svd_distributed(ctxs[i], slabs + (size_t)i * slabs_per_device, slabs_per_device,
+                                                 (int64_t)i * slabs_per_device, P, ldims, d_local, ld_slab, r_max,
+                                                 eps, nullptr, nullptr, &res[i]);
+            if (rcs[i] != TTSVD_OK) msgs[i] = g_last_error;
+        });
+    for (auto& t : pool) t.join();
+    for (int i = 1; i < ndev; ++i) ttsvd_cu_tt_free(res[i]);
+    for (int i = 0; i < ndev; ++i)
+        if (rcs[i] != TTSVD_OK) {
+            ttsvd_cu_tt_free(res[0]);
+            return fail(rcs[i], "device " + std::to_string(i) + ": " + msgs[i]);
+        }
+    *out = res[0];
+    return TTSVD_OK;
 }
 
 int64_t ttsvd_cu_tt_d(const ttsvd_cu_tt* tt) { return tt ? (int64_t)tt->dims.size() : -1; }
@@ -1891,6 +2059,17 @@ int ttsvd_cu_tt_sigma(const ttsvd_cu_tt* tt, int64_t s, double* dst) {
 }
 
 void ttsvd_cu_tt_free(ttsvd_cu_tt* tt) { delete tt; }
+
+int ttsvd_cu_gen_partition(ttsvd_cu_ctx* ctx, uint64_t seed, int kind, double scale, int64_t total, int64_t rows,
+                           int64_t ld, int64_t nparts, int64_t part, double* X) {
+    TT_TRY(set_device(ctx));
+    if (!X || rows < 1 || ld < rows || total < 0 || nparts < 1 || part < 0 || part >= nparts || (kind != 0 && kind != 1))
+        return fail(TTSVD_ERR_INVALID, "gen_partition: bad arguments");
+    const int64_t blocks = std::min<int64_t>((total + 255) / 256, (int64_t)ctx->num_sms * 16);
+    gen_partition_kernel<<<(unsigned)std::max<int64_t>(blocks, 1), 256, 0, ctx->stream>>>(seed, kind, scale, total, rows,
+                                                                                          ld, nparts, part, X);
+    return check_launch(ctx, "gen_partition_kernel");
+}
 
 int ttsvd_cu_gen_uniform(ttsvd_cu_ctx* ctx, uint64_t seed, int64_t total, int64_t rows, int64_t ld, double* X) {
     TT_TRY(set_device(ctx));

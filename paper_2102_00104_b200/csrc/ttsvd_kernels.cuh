@@ -117,6 +117,27 @@ __global__ void gen_uniform_kernel(uint64_t seed, int64_t total, int64_t rows, i
     }
 }
 
+// partition `part` of `nparts`: local flat l is global part + nparts*l.
+// kind 0: uniform[-1,1) (as gen_uniform); kind 1: += scale * N(0,1) from
+// Box-Muller on two counter draws of the global index
+__global__ void gen_partition_kernel(uint64_t seed, int kind, double scale, int64_t total, int64_t rows, int64_t ld,
+                                     int64_t nparts, int64_t part, double* X) {
+    for (int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; l < total; l += (int64_t)gridDim.x * blockDim.x) {
+        const uint64_t g = (uint64_t)(part + nparts * l);
+        const int64_t j = l / rows;
+        double* x = X + j * ld + (l - j * rows);
+        if (kind == 0) {
+            const uint64_t z = splitmix64(seed + (g + 1) * 0x9E3779B97F4A7C15ULL);
+            *x = 2.0 * ((double)(z >> 11) * 0x1.0p-53) - 1.0;
+        } else {
+            const uint64_t z1 = splitmix64(seed + (2 * g + 1) * 0x9E3779B97F4A7C15ULL);
+            const uint64_t z2 = splitmix64(seed + (2 * g + 2) * 0x9E3779B97F4A7C15ULL);
+            const double u1 = ((double)(z1 >> 11) + 0.5) * 0x1.0p-53, u2 = (double)(z2 >> 11) * 0x1.0p-53;
+            *x += scale * sqrt(-2.0 * log(u1)) * cospi(2.0 * u2);
+        }
+    }
+}
+
 // ---------------------------------------------------------------------------
 // K_TSQR — structured Householder reduction of [R; B] over row tiles.
 //

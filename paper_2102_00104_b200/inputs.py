@@ -7,13 +7,23 @@ path; torch is used here only as plumbing for the contractions.
     config 3  n x k uniform[-1,1], n*k = 2^30       (seed 3)
     config 4  2^32 as d=32, n=2, TT rank <= 64 + 1e-10 noise (seed 4/104)
     config 5  8^11 uniform + rank-50 TT signal of 100x the noise norm (seed 5/105)
+
+Configs 4 and 5 are also generated per partition (config4_slab,
+config5_slab): partition p of P holds the global entries l = p + P * l_local
+(split_first_dim, ttsvd_bench.cpp:72-86) — for config 4 the leading log2(P)
+modes are merged into the partition index, for config 5 mode 1 (extent 8) is
+split as (P, 8/P) with P fastest.  The exact-TT part of a slab is itself a TT
+(the merged modes contracted into the first local core), the noise and the
+uniform part are counter-based on the GLOBAL index, and the norms that scale
+them are global (analytic for the TT, an all-reduce for the uniform part), so
+every P generates the same global tensor.
 """
 from __future__ import annotations
 
 import numpy as np
 import torch
 
-from .ttsvd import fortran_empty, gen_uniform, padded_stride
+from .ttsvd import fortran_empty, gen_partition, gen_uniform, padded_stride
 
 
 def tt_contract_flat(cores: list[torch.Tensor]) -> torch.Tensor:
@@ -102,27 +112,83 @@ def config3_matrix(k: int, device: int = 0, total: int = 1 << 30):
     return gen_uniform(3, [n, k]), n, k
 
 
+def tt_norm(cores: list[torch.Tensor]) -> float:
+    """||TT||_F from the chain of core Gram matrices (no contraction)."""
+    G = torch.ones((1, 1), dtype=torch.float64, device=cores[0].device)
+    for c in cores:
+        G = torch.einsum("ab,axc,bxd->cd", G, c, c)
+    return float(G[0, 0].clamp(min=0).sqrt())
+
+
+def _merge_leading(cores: list[torch.Tensor], digits: list[int]) -> list[torch.Tensor]:
+    """Fix the leading modes at `digits` and fold them into the next core."""
+    v = torch.ones((1, 1), dtype=torch.float64, device=cores[0].device)
+    for j, x in enumerate(digits):
+        v = v @ cores[j][:, x, :]
+    rest = cores[len(digits):]
+    return [torch.einsum("a,axb->xb", v[0], rest[0]).unsqueeze(0)] + list(rest[1:])
+
+
+def config4_slab(P: int, p: int, d: int = 32, device: int = 0):
+    """Partition p of P of config 4 (P a power of two): the slab of the
+    global 2^d tensor whose leading log2(P) modes index p; local dims
+    [2] * (d - log2 P).  P = 1 is the whole tensor."""
+    q = int(P).bit_length() - 1
+    if P < 1 or (1 << q) != P or q >= d:
+        raise ValueError("config 4 partitions: P must be a power of two below 2^d")
+    dims = [2] * d
+    ranks = [min(64, 2 ** j, 2 ** (d - j)) for j in range(d + 1)]
+    cores = gaussian_cores(dims, ranks, 4, device)
+    sigma = 1e-10 * tt_norm(cores) / np.sqrt(2.0 ** d)
+    local = _merge_leading(cores, [(p >> j) & 1 for j in range(q)]) if q else cores
+    ldims = dims[q:]
+    X = to_padded(tt_contract_flat(local), ldims)
+    gen_partition(104, 1, X, 2 ** (d - q), P, p, scale=sigma)
+    torch.cuda.empty_cache()
+    return X, ldims, 64, 0.0
+
+
 def config4(d: int = 32, device: int = 0):
     """2^d entries as d modes of 2 (d = 32: 2^32, 32 GiB), exact TT with
     r_j = min(64, 2^j, 2^(d-j)), N(0,1) cores (seed 4), plus N(0, s^2) noise
-    with s = 1e-10 ||X|| / sqrt(N) (seed 104); TT-SVD r_max = 64, eps = 0."""
-    dims = [2] * d
-    ranks = [min(64, 2 ** j, 2 ** (d - j)) for j in range(d + 1)]
-    return exact_tt(dims, ranks, 4, 1e-10, 104, device), dims, 64, 0.0
+    with s = 1e-10 ||X|| / sqrt(N) (counter-based, seed 104); TT-SVD
+    r_max = 64, eps = 0."""
+    return config4_slab(1, 0, d, device)
+
+
+def config5_slab(P: int, p: int, d: int = 11, device: int = 0, allreduce=None):
+    """Partition p of P (P | 8) of config 5: mode 1 split as (P, 8/P), P
+    fastest, so the slab holds j_1 = p (mod P); local dims [8/P, 8, ...]
+    ([8] * (d-1) at P = 8).  ``allreduce(float) -> float`` sums ||E_p||^2
+    over the partitions (torch.distributed); without it P must be 1."""
+    if 8 % P or P < 1:
+        raise ValueError("config 5 partitions: P must divide 8")
+    dims = [8] * d
+    ranks = [min(50, 8 ** j, 8 ** (d - j)) for j in range(d + 1)]
+    cores = gaussian_cores(dims, ranks, 105, device)
+    s_norm = tt_norm(cores)
+    if P == 8:
+        local, ldims = _merge_leading(cores, [p]), dims[1:]
+    else:
+        local, ldims = [cores[0][:, p::P, :].contiguous()] + cores[1:], [8 // P] + dims[1:]
+    total = int(np.prod(ldims))
+    rows = total // ldims[-1]
+    X = fortran_empty(rows, ldims[-1], ld=padded_stride(rows), device=device, zero=True)
+    gen_partition(5, 0, X, total, P, p)
+    e2 = float(sum(torch.sum(X[:, j] ** 2) for j in range(ldims[-1])))
+    if allreduce is not None:
+        e2 = allreduce(e2)
+    elif P != 1:
+        raise ValueError("config5_slab: pass allreduce for P > 1")
+    S = tt_contract_flat(local).view(ldims[-1], rows).t()
+    X.add_(S, alpha=100.0 * np.sqrt(e2) / s_norm)
+    del S
+    torch.cuda.empty_cache()
+    return X, ldims, 50, 1e-4
 
 
 def config5(d: int = 11, device: int = 0):
     """8^d entries (d = 11: 2^33, 64 GiB): E uniform[-1,1] (seed 5) plus a TT
     signal S with N(0,1) cores, r_j = min(50, 8^j, 8^(d-j)) (seed 105), scaled
     so ||S|| = 100 ||E||; TT-SVD r_max = 50, eps = 1e-4."""
-    dims = [8] * d
-    ranks = [min(50, 8 ** j, 8 ** (d - j)) for j in range(d + 1)]
-    X = gen_uniform(5, dims)
-    rows = int(np.prod(dims)) // dims[-1]
-    S = tt_contract_flat(gaussian_cores(dims, ranks, 105, device)).view(dims[-1], rows).t()
-    e2 = float(sum(torch.sum(X[:rows, j] ** 2) for j in range(dims[-1])))
-    s2 = float(sum(torch.sum(S[:, j] ** 2) for j in range(dims[-1])))
-    X[:rows].add_(S, alpha=100.0 * np.sqrt(e2 / s2))
-    del S
-    torch.cuda.empty_cache()
-    return X, dims, 50, 1e-4
+    return config5_slab(1, 0, d, device)

@@ -131,6 +131,7 @@ class Context:
     def __init__(self, device: int = 0, stream: torch.cuda.Stream | None = None):
         self.device = device
         self.handle = C.c_void_p()
+        self.comm_size = 0  # > 0 once an NCCL communicator is attached
         s = stream if stream is not None else torch.cuda.current_stream(device)
         self._stream = s
         _check(_lib.lib().ttsvd_cu_ctx_create(device, C.c_void_p(s.cuda_stream), C.byref(self.handle)))
@@ -151,6 +152,25 @@ class Context:
 
     def synchronize(self) -> None:
         _check(_lib.lib().ttsvd_cu_synchronize(self.handle))
+
+    def attach_nccl(self, group=None) -> None:
+        """Attach the library's own NCCL communicator over the ranks of a
+        torch.distributed group (one process per GPU): rank 0 creates the
+        unique id, the group broadcasts it, every rank joins.  Afterwards
+        tt_svd_distributed all-gathers inside the library (ncclAllGather on
+        this context's stream, no Python on the exchange path)."""
+        import torch.distributed as dist
+        world, rank = dist.get_world_size(group), dist.get_rank(group)
+        uid = (C.c_ubyte * 128)()
+        if rank == 0:
+            _check(_lib.lib().ttsvd_cu_comm_unique_id(uid))
+        t = torch.tensor(list(bytes(uid)), dtype=torch.uint8,
+                         device="cuda" if dist.get_backend(group) == "nccl" else "cpu")
+        dist.broadcast(t, src=dist.get_global_rank(group, 0) if group is not None else 0, group=group)
+        raw = bytes(t.cpu().tolist())
+        uid = (C.c_ubyte * 128).from_buffer_copy(raw)
+        _check(_lib.lib().ttsvd_cu_ctx_comm_init(self.handle, uid, world, rank))
+        self.comm_size = world
 
     def close(self) -> None:
         if self.handle:
@@ -643,6 +663,8 @@ def tt_svd_distributed(slabs, ldims, spec: TruncationSpec | tuple | None = None,
             except Exception:
                 return 1
         exch = _lib.EXCHANGE_FN(_cb)
+    elif ctx.comm_size > 0:
+        exch = _lib.EXCHANGE_FN()  # NULL: the library's NCCL communicator
     else:
         exch = _torch_exchange(group) if n_slabs != P_total else _lib.EXCHANGE_FN()
     h = C.c_void_p()
@@ -651,6 +673,53 @@ def tt_svd_distributed(slabs, ldims, spec: TruncationSpec | tuple | None = None,
                                                   float(spec.eps), exch, None, C.byref(h)))
     gdims = [P_total if P_total > 1 else 1] + ldims
     return _finish(h, gdims)
+
+
+def tt_svd_distributed_devices(slabs_per_device, ldims, spec: TruncationSpec | tuple | None = None) -> TensorTrain:
+    """Alg. 5 over several GPUs of ONE process (tt_svd.hpp:520 across
+    devices): ``slabs_per_device[i]`` lists device i's slabs (same count on
+    every device, partitions numbered device-major); the library attaches an
+    NCCL communicator over the devices (ncclCommInitAll) and drives one host
+    thread per device."""
+    spec = _spec(spec)
+    ldims = [int(x) for x in ldims]
+    ndev = len(slabs_per_device)
+    spd = {len(s) for s in slabs_per_device}
+    if ndev == 0 or len(spd) != 1 or 0 in spd:
+        raise PartitionMismatch("tt_svd_distributed_devices: every device needs the same number of slabs")
+    spd = spd.pop()
+    flat = [s for dev_slabs in slabs_per_device for s in dev_slabs]
+    if len({tuple(s.shape) for s in flat}) != 1 or len({_ld(s) for s in flat}) != 1:
+        raise PartitionMismatch("tt_svd_distributed_devices: slab shapes differ")
+    ctxs = [context(dev_slabs[0].device.index) for dev_slabs in slabs_per_device]
+    if len({c.device for c in ctxs}) != ndev:
+        raise PartitionMismatch("tt_svd_distributed_devices: one entry per distinct device")
+    L = _lib.lib()
+    handles = (C.c_void_p * ndev)(*[c.handle for c in ctxs])
+    if any(c.comm_size != ndev for c in ctxs):
+        _check(L.ttsvd_cu_ctx_comm_init_all(handles, ndev))
+        for c in ctxs:
+            c.comm_size = ndev
+    ptrs = (C.c_void_p * len(flat))(*[C.c_void_p(s.data_ptr()) for s in flat])
+    dv = np.asarray(ldims, dtype=np.int64)
+    for c in ctxs:
+        torch.cuda.synchronize(c.device)
+    h = C.c_void_p()
+    _check(L.ttsvd_cu_tt_svd_distributed_devices(handles, ndev, ptrs, spd, dv.ctypes.data_as(_lib.i64p), len(ldims),
+                                                 _ld(flat[0]), int(spec.r_max), float(spec.eps), C.byref(h)))
+    P = ndev * spd
+    return _finish(h, [P if P > 1 else 1] + ldims)
+
+
+def gen_partition(seed: int, kind: int, X: torch.Tensor, total_local: int, nparts: int = 1, part: int = 0,
+                  scale: float = 1.0) -> None:
+    """Partition ``part`` of ``nparts`` of a counter-based tensor into the
+    padded device matrix X (local flat l = global part + nparts*l): kind 0
+    writes uniform[-1,1), kind 1 adds scale * N(0,1)."""
+    p, rows, cols, ld = _mat(X)
+    ctx = context(X.device.index)
+    _check(_lib.lib().ttsvd_cu_gen_partition(ctx.handle, int(seed), int(kind), float(scale), int(total_local), rows, ld,
+                                             int(nparts), int(part), p))
 
 
 def gen_uniform(seed: int, dims, ld: int | None = None) -> torch.Tensor:
