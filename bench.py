@@ -12,7 +12,10 @@ tt_svd_tsqr).  A step is one full decomposition.  X (2 GiB) is larger than the
 
 N > 1 (torchrun, one rank per GPU): weak scaling of Alg. 5 — every rank owns a
 config-2-sized slab of the (N, 16^7) global tensor and the per-step R factors
-are all-gathered over NCCL.
+are all-gathered over NCCL (the library's own communicator, ncclAllGather on
+its stream).  Every run also times BASELINE's multi-GPU configs under
+"north_star_configs": config 4 (one global 2^32 tensor, strong scaling, N >= 1)
+and config 5 (8^11, N >= 2), each rank generating only its slab.
 
 ``--impl reference`` times the reference's own CPU tt_svd_tsqr (compiled from
 /root/reference into oracle/_ref) on all host cores, on a bounded sample of
@@ -47,6 +50,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--modes", type=int, default=7, help="16^modes tensor (7 = config 2)")
+    ap.add_argument("--north-star", default="auto", choices=["auto", "off"],
+                    help="also time BASELINE configs 4 (N >= 1) and 5 (N >= 2) sharded over the N GPUs")
     return ap.parse_args()
 
 
@@ -190,6 +195,8 @@ def run_ours(args, rank: int, world: int):
     X, dims, r_max, eps = inputs.config2(args.modes, device=dev)
     torch.cuda.synchronize()
     ctx = tt.context(dev)
+    if world > 1:
+        ctx.attach_nccl(dist.group.WORLD)  # the R-factor all-gather runs inside the library
     nbytes_local = 8 * int(np.prod(dims))
 
     if world == 1:
@@ -342,10 +349,85 @@ def run_ours(args, rank: int, world: int):
                           "api": "ttsvd_cu_tt_svd_host (pinned host X -> H2D -> TT-SVD -> cores D2H)"}
     elif out is not None:
         out["e2e"] = None
+    # ---- the north-star multi-GPU configs (BASELINE configs 4 and 5), row-
+    # sharded over the N ranks with the library's NCCL exchange ----
+    if args.north_star != "off":
+        del X
+        torch.cuda.empty_cache()
+        extra = {}
+        for which in (["config4"] + (["config5"] if world >= 2 else [])):
+            try:
+                extra[which] = run_north_star(args, rank, world, dev, dist, which)
+            except Exception as e:  # reported, never fatal for the headline line
+                extra[which] = {"error": f"{type(e).__name__}: {e}"[:300]}
+            torch.cuda.empty_cache()
+        if out is not None:
+            out["north_star_configs"] = extra
     if dist:
         dist.barrier()
         dist.destroy_process_group()
     return out
+
+
+def run_north_star(args, rank: int, world: int, dev: int, dist, which: str) -> dict:
+    """BASELINE config 4 (2^32 as 32 modes of 2, r_max 64: strong scaling of
+    ONE global tensor over N = 1/2/4/8 GPUs, the leading log2 N modes merged
+    into the partition index) or config 5 (8^11, eps 1e-4, r_max 50, mode 1
+    split as (N, 8/N); N >= 2).  Every rank generates only its slab (l = p +
+    N * l_local); the R factors are all-gathered by the library's NCCL
+    communicator.  value = global tensor bytes / max-over-ranks device time."""
+    import torch
+    import paper_2102_00104_b200 as tt
+    from paper_2102_00104_b200 import inputs
+    if which == "config4":
+        X, ldims, r_max, eps = inputs.config4_slab(world, rank, 32, device=dev)
+        gbytes = 8 * 2 ** 32
+    else:
+        red = None
+        if dist:
+            def red(x):
+                t = torch.tensor([x], dtype=torch.float64, device="cuda")
+                dist.all_reduce(t)
+                return float(t.item())
+        X, ldims, r_max, eps = inputs.config5_slab(world, rank, 11, device=dev, allreduce=red)
+        gbytes = 8 * 8 ** 11
+    torch.cuda.synchronize()
+    spec = tt.TruncationSpec(r_max=r_max, eps=eps)
+    ctx = tt.context(dev)
+    if world > 1 and ctx.comm_size == 0:
+        ctx.attach_nccl(dist.group.WORLD)
+
+    def step():
+        if world == 1:
+            return tt.tt_svd_tsqr(X, ldims, spec)
+        return tt.tt_svd_distributed([X], ldims, spec, group=dist.group.WORLD, P_total=world, part0=rank)
+
+    for _ in range(2):
+        T = step()
+    torch.cuda.synchronize()
+    steps = max(1, min(args.steps, 5))
+    stream = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for _ in range(steps):
+        T = step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    if dist:
+        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        dist.barrier()
+    del X
+    return {"workload": ("config 4: 2^32 fp64 (32 modes of 2), exact TT r<=64 + 1e-10 noise, r_max=64" if which == "config4"
+                         else "config 5: 8^11 fp64, uniform + rank-50 TT signal, eps=1e-4, r_max=50"),
+            "n_gpus": world, "scaling": "strong", "partitioning": f"leading modes -> {world} partitions (l = p + N l_local)",
+            "value": round(gbytes / (ms * 1e-3) / 1e9, 3), "unit": UNIT, "ms_per_step": round(ms, 3), "steps": steps,
+            "ranks": T.ranks(), "exchange": "NCCL all-gather inside the library" if world > 1 else "none (1 GPU)"}
 
 
 def main():
