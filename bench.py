@@ -128,7 +128,12 @@ def fp64_peak(device: int) -> dict:
     lib = C.CDLL(os.path.join(ROOT, "paper_2102_00104_b200", "libttsvd_probe.so"))
     a, b = C.c_double(), C.c_double()
     lib.ttsvd_probe_fp64(device, C.byref(a), C.byref(b))
-    return {"dfma_tflops": a.value, "dmma_tflops": b.value, "peak_tflops": max(a.value, b.value)}
+    out = {"dfma_tflops": a.value, "dmma_tflops": b.value, "peak_tflops": max(a.value, b.value)}
+    k4, k8, k16 = C.c_double(), C.c_double(), C.c_double()
+    if lib.ttsvd_probe_fp64_shapes(device, C.byref(k4), C.byref(k8), C.byref(k16)) == 0:
+        # the sm_90+ f64 shapes lower to several DMMA.8x8x4 in SASS; recorded, not used
+        out["dmma_m16n8k4_tflops"], out["dmma_m16n8k8_tflops"], out["dmma_m16n8k16_tflops"] = k4.value, k8.value, k16.value
+    return out
 
 
 def cpu_sample_tensor(modes: int = 6):

@@ -944,7 +944,8 @@ int tsmm_device(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t ld
         return TTSVD_OK;
     }
     if (k > 1 && k <= 16 && m <= 32 && n >= (int64_t)1 << 18) {
-        // narrow X: rows staged by cp.async (tsmm_async_kernel)
+        // narrow X: rows staged by cp.async (tsmm_async_kernel; measured
+        // against TMA bulk staging, tools/tsmm_bulk_experiment.cuh)
         rc = k <= 4 ? launch_tsmm_async<4>(ctx, X, n, m, ldx, V, ldv, k, Y, out_rows, ldy)
                     : (k <= 8 ? launch_tsmm_async<8>(ctx, X, n, m, ldx, V, ldv, k, Y, out_rows, ldy)
                               : launch_tsmm_async<16>(ctx, X, n, m, ldx, V, ldv, k, Y, out_rows, ldy));
