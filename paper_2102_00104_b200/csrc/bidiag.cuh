@@ -365,10 +365,9 @@ __device__ __forceinline__ double bd_transpose_reduce(double (&p)[CPC], int lane
     return p[0];  // column lane % CPC
 }
 
-template <int CPC>
+template <int CPC, int C = kBdCluster>
 __global__ void __launch_bounds__(kBdThreads, 1) bd_reg_kernel(BdArgs a) {
     cg::cluster_group cl = cg::this_cluster();
-    constexpr int C = kBdCluster;
     constexpr int W = kBdThreads / 32;
     __shared__ double wred[W][CPC], sred[W];
     __shared__ double wl[CPC], rowa[CPC], rowk[CPC];

@@ -735,12 +735,35 @@ int finalize_device(ttsvd_cu_ctx* ctx, const double* A, int n, int m, const doub
 // svd_vectors.  Returns -1 (nothing launched) when A does not fit the cluster.
 // the bidiagonal path from m = 16 (config 2 steps 1 and 6: 0.17 -> 0.10 ms, 0.21 -> 0.12 ms)
 constexpr int kBdMinM = 16;
+// cluster size C and columns per CTA of the register-resident
+// bidiagonalisation (C * cpc >= m).  Measured (config 1, m = 64 steps;
+// config 2 m = 256 steps): 8 CTAs for m <= 128 (config 1 4.20 -> 4.09 ms),
+// 16 above (m = 256 on 8 CTAs: 1.49 -> 1.96 ms; on 4: the same).
+void bd_shape(int m, int* C, int* cpc) {
+    const int c = m <= 128 ? 8 : kBdCluster;
+    const int need = (m + c - 1) / c;
+    *C = c;
+    *cpc = need <= 8 ? 8 : (need <= 16 ? 16 : 32);
+}
+
+template <int CPC>
+void (*bd_reg_for(int C))(BdArgs) {
+    if constexpr (CPC <= 16)
+        if (C == 8) return bd_reg_kernel<CPC, 8>;
+    return bd_reg_kernel<CPC, kBdCluster>;
+}
+
 int bd_sigma(ttsvd_cu_ctx* ctx, double* A, int n, int m, double* sigma) {
-    const int need = (m + kBdCluster - 1) / kBdCluster;
-    const int cpc = need <= 8 ? 8 : (need <= 16 ? 16 : 32);
-    if (need > 32 || n < m) return -1;
+    int C = kBdCluster, cpc = 8;
     const bool reg = n <= kBdThreads;
-    void (*kern)(BdArgs) = reg ? (cpc == 8 ? bd_reg_kernel<8> : (cpc == 16 ? bd_reg_kernel<16> : bd_reg_kernel<32>))
+    if (reg) {
+        bd_shape(m, &C, &cpc);
+    } else {
+        const int need = (m + kBdCluster - 1) / kBdCluster;
+        cpc = need <= 8 ? 8 : (need <= 16 ? 16 : 32);
+    }
+    if ((m + C - 1) / C > 32 || n < m) return -1;
+    void (*kern)(BdArgs) = reg ? (cpc == 8 ? bd_reg_for<8>(C) : (cpc == 16 ? bd_reg_for<16>(C) : bd_reg_for<32>(C)))
                                : (cpc == 8 ? bd_kernel<8> : (cpc == 16 ? bd_kernel<16> : bd_kernel<32>));
     const size_t smem = reg ? 0 : bd_smem_bytes(n, cpc);
     int ss = 0;
@@ -753,13 +776,13 @@ int bd_sigma(ttsvd_cu_ctx* ctx, double* A, int n, int m, double* sigma) {
     double* tauL = e + m;
     double* xg = tauL + m;
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(kBdCluster);
+    cfg.gridDim = dim3(C);
     cfg.blockDim = dim3(kBdThreads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = ctx->stream;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = kBdCluster;
+    at[0].val.clusterDim.x = C;
     at[0].val.clusterDim.y = 1;
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
