@@ -365,56 +365,169 @@ __device__ __forceinline__ double bd_transpose_reduce(double (&p)[CPC], int lane
     return p[0];  // column lane % CPC
 }
 
+// Register-resident kernel's exchanges: point-to-point st.async into the
+// receivers' shared memory, each receiver counting the bytes on an mbarrier
+// (no cluster barrier, no L2 round trip).  Per step k (right reflector):
+//   EN  at the end of reflect(k) every CTA sends its row-k norm partial (and
+//       the owner of column k+1 A[k][k+1]) to every CTA;
+//   E1  every CTA sends, for each row i > k, its partial
+//       T_i = sum_j x_ij rowk_j (and the owner's x_i,k+1) to the row's
+//       reducer, CTA i / S (a reduce-scatter over S-row slices);
+//   E2  the reducer sums its slice, forms z_i = tauR (scaleR T_i + x_i,k+1)
+//       and sends (z_i, x_i,k+1 - z_i) for every row of the slice to every
+//       CTA (the all-gather).
+// Buffers alternate by step parity; a CTA can only reach step k + 2 of an
+// exchange after every CTA has consumed step k (each E1/EN follows the
+// previous E2 from every reducer, each E2 the E1 from every CTA).
+// Measured and dropped: the exchanges as cp.async.bulk copies of staged
+// warp chunks (m = 512: 3.2-3.5 vs 2.74 ms).
+__device__ __forceinline__ void bd_st_async2(unsigned raddr, double v0, double v1, unsigned rbar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.b64 [%0], {%1, %2}, [%3];" ::"r"(raddr),
+                 "l"(__double_as_longlong(v0)), "l"(__double_as_longlong(v1)), "r"(rbar)
+                 : "memory");
+}
+
+// x[jc] for a warp-uniform jc in [0, CPC): a jump table instead of CPC selects
+template <int CPC>
+__device__ __forceinline__ double bd_pick(const double (&x)[CPC], int jc) {
+    double v = 0.0;
+    switch (jc) {
+#define BD_CASE(c) \
+    case c:        \
+        if constexpr (c < CPC) v = x[c]; \
+        break;
+        BD_CASE(0) BD_CASE(1) BD_CASE(2) BD_CASE(3) BD_CASE(4) BD_CASE(5) BD_CASE(6) BD_CASE(7)
+        BD_CASE(8) BD_CASE(9) BD_CASE(10) BD_CASE(11) BD_CASE(12) BD_CASE(13) BD_CASE(14) BD_CASE(15)
+        BD_CASE(16) BD_CASE(17) BD_CASE(18) BD_CASE(19) BD_CASE(20) BD_CASE(21) BD_CASE(22) BD_CASE(23)
+        BD_CASE(24) BD_CASE(25) BD_CASE(26) BD_CASE(27) BD_CASE(28) BD_CASE(29) BD_CASE(30) BD_CASE(31)
+#undef BD_CASE
+        default: break;
+    }
+    return v;
+}
+template <int CPC>
+__device__ __forceinline__ void bd_put(double (&x)[CPC], int jc, double v) {
+    switch (jc) {
+#define BD_CASE(c) \
+    case c:        \
+        if constexpr (c < CPC) x[c] = v; \
+        break;
+        BD_CASE(0) BD_CASE(1) BD_CASE(2) BD_CASE(3) BD_CASE(4) BD_CASE(5) BD_CASE(6) BD_CASE(7)
+        BD_CASE(8) BD_CASE(9) BD_CASE(10) BD_CASE(11) BD_CASE(12) BD_CASE(13) BD_CASE(14) BD_CASE(15)
+        BD_CASE(16) BD_CASE(17) BD_CASE(18) BD_CASE(19) BD_CASE(20) BD_CASE(21) BD_CASE(22) BD_CASE(23)
+        BD_CASE(24) BD_CASE(25) BD_CASE(26) BD_CASE(27) BD_CASE(28) BD_CASE(29) BD_CASE(30) BD_CASE(31)
+#undef BD_CASE
+        default: break;
+    }
+}
+
+// bd_transpose_reduce of cb * x without materialising the CPC products: at
+// CPC = 32 the first halving level forms them pairwise (x and the products
+// together would take every register of the thread)
+template <int CPC>
+__device__ __forceinline__ double bd_transpose_reduce_scaled(const double (&x)[CPC], double cb, int lane) {
+    if constexpr (CPC == 32) {
+        double p[16];
+        const bool up = (lane & 16) != 0;
+#pragma unroll
+        for (int t = 0; t < 16; ++t) {
+            const double lo = cb * x[t], hi = cb * x[t + 16];
+            const double send = up ? lo : hi;
+            const double keep = up ? hi : lo;
+            p[t] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+        }
+#pragma unroll
+        for (int o = 8; o >= 1; o >>= 1) {
+            const bool u2 = (lane & o) != 0;
+#pragma unroll
+            for (int t = 0; t < o; ++t) {
+                const double send = u2 ? p[t] : p[t + o];
+                const double keep = u2 ? p[t + o] : p[t];
+                p[t] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+            }
+        }
+        return p[0];
+    } else {
+        double p[CPC];
+#pragma unroll
+        for (int j = 0; j < CPC; ++j) p[j] = cb * x[j];
+        return bd_transpose_reduce<CPC>(p, lane);
+    }
+}
+
 template <int CPC, int C = kBdCluster>
 __global__ void __launch_bounds__(kBdThreads, 1) bd_reg_kernel(BdArgs a) {
     cg::cluster_group cl = cg::this_cluster();
     constexpr int W = kBdThreads / 32;
+    constexpr int S = kBdThreads / C;  // rows per reduction slice
     __shared__ double wred[W][CPC], sred[W];
     __shared__ double wl[CPC], rowa[CPC], rowk[CPC];
-    __shared__ double pnorm[2][C + 1];  // row-norm partials of all CTAs + A[k][k+1], by step parity
+    __shared__ double pnorm[2][C + 1];                // EN: row-norm partials of all CTAs + A[k][k+1]
+    __shared__ double rsb[2][C][S];                   // E1: T partials of my slice from every CTA
+    __shared__ double rsx[2][S];                      // E1: column k+1 on my slice (its owner's)
+    __shared__ __align__(16) double agb[2][kBdThreads][2];  // E2: (z_i, column k+1 after the update)
     __shared__ double rs[2];
-    __shared__ __align__(8) unsigned long long e1bar;  // E1 arrivals (C + 1 doubles per step)
+    __shared__ __align__(8) unsigned long long mbar[4];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int rank = (int)cl.block_rank();
     const int n = a.n, m = a.m;
     const int c0 = rank * CPC;
-    const int i = tid;  // my row
-    double* colg = a.xg;                        // column k+1 after the left update (its owner), 2 x n by parity
-    double* zg = a.xg + 2 * (size_t)(n + 1);    // partial z, C x n
+    const int i = tid;                 // my row
+    const int si = i / S, so = i % S;  // my row's reducer CTA and slot
+    const int w0 = 32 * warp;          // my warp's first row
     double x[CPC];
 #pragma unroll
     for (int j = 0; j < CPC; ++j) x[j] = (i < n && c0 + j < m) ? a.A[(int64_t)(c0 + j) * n + i] : 0.0;
-    long long* pf = (a.prof && rank == C - 1 && tid == 0) ? a.prof : nullptr;
-    long long tp = pf ? bj_clock() : 0;
+#ifdef TTSVD_BD_PROF
+    // diagnostics builds (tools/bd_prof.cu): per-phase cycles of one thread
+    // per CTA, kept in registers and written once at the end
+    long long pacc[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+    long long tp = bj_clock();
 #define BD_MARK(q)                           \
-    if (pf) {                                \
+    {                                        \
         const long long tq = bj_clock();     \
-        pf[q] += tq - tp;                    \
+        pacc[q] += tq - tp;                  \
         tp = tq;                             \
     }
-    const unsigned bar = bd_smem_addr(&e1bar);
+#else
+#define BD_MARK(q)
+#endif
+    // EN needs one mbarrier per step parity: a CTA with no rows left to
+    // reduce is not on the E1 -> E2 path that orders the other exchanges
+    const unsigned mbn0 = bd_smem_addr(&mbar[0]), mb1 = bd_smem_addr(&mbar[2]), mb2 = bd_smem_addr(&mbar[3]);
     if (tid == 0) {
-        bd_mbar_init(bar, 1);
+        bd_mbar_init(mbn0, 1);
+        bd_mbar_init(mbn0 + 8, 1);
+        bd_mbar_init(mb1, 1);
+        bd_mbar_init(mb2, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
+    const unsigned r_mb1 = bd_mapa(mb1, si);
+    const int s_lo = S * rank, s_hi = min(S * rank + S, n);  // my slice
     // Left reflector of column k from its entries ck (every CTA computes it
     // from the same bits) fused with the next products w_j = tau u^T x_j:
     // one reduction of (ck^2, ck x_ij) over the rows below k; u_k = 1 adds
-    // row k.  Returns u_i; the owner keeps u in its column.
-    double tauL = 0.0;
+    // row k.  Warps whose rows all lie above k contribute zeros without
+    // computing.  Also row k after the left update (rowk = rowa - wl, the
+    // right reflector's row) and, when step k has a right reflector, its
+    // norm partial to every CTA (EN).  Returns u_i; the owner keeps u in its
+    // column.
     auto reflect = [&](int k, double ck) -> double {
         const bool below = i > k && i < n;
-        double p[CPC];
+        if (w0 + 31 >= k && w0 < n) {
+            const double cb = below ? ck : 0.0;
+            const double cs = bd_transpose_reduce_scaled<CPC>(x, cb, lane);
+            const double ss = bd_warp_sum(cb * cb);
+            if (lane < CPC) wred[warp][lane] = cs;
+            if (lane == 0) sred[warp] = ss;
+            if (i == k) {
+                rs[0] = ck;
 #pragma unroll
-        for (int j = 0; j < CPC; ++j) p[j] = below ? ck * x[j] : 0.0;
-        const double cs = bd_transpose_reduce<CPC>(p, lane);
-        const double ss = bd_warp_sum(below ? ck * ck : 0.0);
-        if (lane < CPC) wred[warp][lane] = cs;
-        if (lane == 0) sred[warp] = ss;
-        if (i == k) {
-            rs[0] = ck;
-#pragma unroll
-            for (int j = 0; j < CPC; ++j) rowa[j] = x[j];
+                for (int j = 0; j < CPC; ++j) rowa[j] = x[j];
+            }
+        } else {
+            if (lane < CPC) wred[warp][lane] = 0.0;
+            if (lane == 0) sred[warp] = 0.0;
         }
         __syncthreads();
         double sv[W];
@@ -429,79 +542,92 @@ __global__ void __launch_bounds__(kBdThreads, 1) bd_reg_kernel(BdArgs a) {
             tau = 1.0 + fabs(alpha) * inv;  // (beta - alpha) / beta
             scale = fast_rcp(alpha - beta);
         }
+        double rk = 0.0, yk = 0.0;  // warp 0: row k after the left update, A[k][k+1]
         if (tid < CPC) {
             double wv[W];
 #pragma unroll
             for (int q = 0; q < W; ++q) wv[q] = wred[q][tid];
             const double sj = bd_tree_sum<W>(wv);
             const int gj = c0 + tid;
-            wl[tid] = (gj > k && gj < m) ? tau * fma(scale, sj, rowa[tid]) : 0.0;
+            const double w = (gj > k && gj < m) ? tau * fma(scale, sj, rowa[tid]) : 0.0;
+            wl[tid] = w;
+            const double r = rowa[tid] - w;
+            rk = (gj >= k + 2 && gj < m) ? r : 0.0;
+            yk = gj == k + 1 ? r : 0.0;
+            rowk[tid] = rk;
         }
         const double u = below ? ck * scale : (i == k ? 1.0 : 0.0);
-        if (k / CPC == rank) {
+        if (k / CPC == rank && i >= k) {
 #pragma unroll
             for (int j = 0; j < CPC; ++j)
-                if (c0 + j == k && i >= k) x[j] = u;
+                if (c0 + j == k) x[j] = u;
         }
         if (rank == 0 && tid == 0) {
             a.d[k] = beta;
             a.tauL[k] = tau;
         }
-        tauL = tau;
-        __syncthreads();  // wl visible; rs / rowa / wred free
+        __syncthreads();  // wl / rowk visible; rs / rowa / wred free
+        if (warp == 0 && k + 2 < m) {
+            // EN: lane t sends the row-norm partial (and A[k][k+1]) to CTA t
+            const double sn = bd_warp_sum(rk * rk);
+            const double y = bd_warp_sum(yk);
+            if (lane < C) {
+                double* pn = pnorm[k & 1];
+                const unsigned rb = bd_mapa(mbn0 + 8 * (k & 1), lane);
+                bd_st_async(bd_mapa(bd_smem_addr(pn + rank), lane), sn, rb);
+                if (rank == (k + 1) / CPC) bd_st_async(bd_mapa(bd_smem_addr(pn + C), lane), y, rb);
+            }
+        }
         return u;
     };
-    // column 0 to everyone
-    if (rank == 0 && i < n) __stcg(colg + i, x[0]);
+    // every CTA reads column 0 itself; the barrier publishes the mbarrier inits
     bd_arrive();
     bd_wait();
-    double ui = reflect(0, i < n ? __ldcg(colg + i) : 0.0);
+    if (tid == 0 && 2 < m) bd_mbar_expect(mbn0, (unsigned)(C + 1) * 8);
+    double ui = reflect(0, i < n ? a.A[i] : 0.0);
     for (int k = 0; k < m; ++k) {
         BD_MARK(0)
-#pragma unroll
-        for (int j = 0; j < CPC; ++j) x[j] = fma(-wl[j], ui, x[j]);
+        const int b = k & 1;
+        const unsigned par = (unsigned)(k & 1);
         const int on = (k + 1) / CPC;  // owner of column k+1
-        double* colg_k = colg + (size_t)((k + 1) & 1) * n;
-        if (k + 2 < m) {
-            // ---- E1: row k's norm partials (+ A[k][k+1]) stored into every
-            // CTA's shared memory by st.async; each CTA waits on its mbarrier.
-            // Meanwhile every row forms T_i = sum_j x_ij rowk_j (the right
-            // reflector's product up to its scale) ----
-            double* pn = pnorm[k & 1];
-            if (tid == 0) bd_mbar_expect(bar, (C + 1) * 8);
-            if (warp == (k >> 5)) {  // the warp holding row k
-                double s4[4] = {0.0, 0.0, 0.0, 0.0}, y = 0.0;
-                if (i == k) {
-#pragma unroll
-                    for (int j = 0; j < CPC; ++j) {
-                        const int gj = c0 + j;
-                        const bool act = gj >= k + 2 && gj < m;
-                        rowk[j] = act ? x[j] : 0.0;
-                        if (act) s4[j & 3] = fma(x[j], x[j], s4[j & 3]);
-                        if (gj == k + 1) y = x[j];
-                    }
-                }
-                // lane t sends the row-norm partial (and A[k][k+1]) to CTA t:
-                // C sends in parallel instead of one thread's 2C in a row
-                const double s = __shfl_sync(0xffffffffu, bd_tree_sum<4>(s4), k & 31);
-                y = __shfl_sync(0xffffffffu, y, k & 31);
-                if (lane < C) {
-                    const unsigned rb = bd_mapa(bar, lane);
-                    bd_st_async(bd_mapa(bd_smem_addr(pn + rank), lane), s, rb);
-                    if (rank == on) bd_st_async(bd_mapa(bd_smem_addr(pn + C), lane), y, rb);
-                }
-            }
-            __syncthreads();  // rowk
-            double T4[4] = {0.0, 0.0, 0.0, 0.0}, xk1 = 0.0;
+        const bool live = i > k && i < n;  // rows of step k's right update
+        const bool wlive = w0 + 31 > k && w0 < n;
+        double T = 0.0, xk1 = 0.0;
+        if (w0 + 31 >= k && w0 < n) {
+            // left update (rows >= k) fused with T_i = sum_j x_ij rowk_j
+            double T4[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
             for (int j = 0; j < CPC; ++j) {
+                x[j] = fma(-wl[j], ui, x[j]);
                 T4[j & 3] = fma(x[j], rowk[j], T4[j & 3]);
-                if (c0 + j == k + 1) xk1 = x[j];
             }
-            const double T = bd_tree_sum<4>(T4);
+            T = bd_tree_sum<4>(T4);
+        }
+        if (k + 1 >= m) break;
+        if (rank == on) {
+#pragma unroll
+            for (int j = 0; j < CPC; ++j)
+                if (c0 + j == k + 1) xk1 = x[j];
+        }
+        BD_MARK(7)
+        double zt = 0.0, ck = 0.0;
+        if (k + 2 < m) {
+            const int cr = max(0, s_hi - max(s_lo, k + 1));  // my slice's rows in (k, n)
+            if (tid == 0) {
+                bd_mbar_expect(mb1, (unsigned)(C + 1) * (unsigned)cr * 8);
+                bd_mbar_expect(mb2, (unsigned)(n - k - 1) * 16);
+                if (k + 3 < m) bd_mbar_expect(mbn0 + 8 * ((k + 1) & 1), (unsigned)(C + 1) * 8);  // EN of step k + 1
+            }
+            // ---- E1 (reduce-scatter): T_i (and the owner's x_i,k+1) to the row's reducer ----
+            if (live) {
+                bd_st_async(bd_mapa(bd_smem_addr(&rsb[b][rank][so]), si), T, r_mb1);
+                if (rank == on) bd_st_async(bd_mapa(bd_smem_addr(&rsx[b][so]), si), xk1, r_mb1);
+            }
             BD_MARK(1)
-            bd_mbar_wait(bar, (unsigned)(k & 1));
-            BD_MARK(2)
+            // the right reflector from EN (sent at the end of reflect(k))
+            bd_mbar_wait(mbn0 + 8 * b, (unsigned)((k >> 1) & 1));
+            BD_MARK(8)
+            const double* pn = pnorm[b];
             double pv[C];
 #pragma unroll
             for (int t = 0; t < C; ++t) pv[t] = pn[t];
@@ -515,49 +641,56 @@ __global__ void __launch_bounds__(kBdThreads, 1) bd_reg_kernel(BdArgs a) {
                 scaleR = fast_rcp(y0 - gamma);
             }
             if (rank == 0 && tid == 0) a.e[k] = gamma;
-            // ---- E2: partial z (rows > k) and, at the owner, column k+1 ----
-            const double z = fma(scaleR, T, xk1);
-            if (i < n) {
-                zg[(size_t)rank * n + i] = (i > k) ? z : 0.0;
-                if (rank == on) __stcg(colg_k + i, xk1);
-            }
-            BD_MARK(3)
-            bd_arrive();  // B3
-            bd_wait();
-            BD_MARK(4)
-            double zt = 0.0, ck = 0.0;
-            if (i < n) {
+            BD_MARK(9)
+            // ---- E2 (all-gather): the reducer's rows (z_i, x_i,k+1 - z_i) to every CTA ----
+            if (live && si == rank) {
+                bd_mbar_wait(mb1, par);
                 double q[C];
 #pragma unroll
-                for (int t = 0; t < C; ++t) q[t] = __ldcg(zg + (size_t)t * n + i);
-                ck = __ldcg(colg_k + i);
-                if (i > k) zt = bd_tree_sum<C>(q) * tauR;
-            }
+                for (int t = 0; t < C; ++t) q[t] = rsb[b][t][so];
+                const double xr = rsx[b][so];
+                const double z = tauR * fma(scaleR, bd_tree_sum<C>(q), xr);
+                const unsigned la = bd_smem_addr(&agb[b][i][0]);
 #pragma unroll
-            for (int j = 0; j < CPC; ++j) {
-                const int gj = c0 + j;
-                const double v = (gj == k + 1) ? 1.0 : rowk[j] * scaleR;
-                x[j] = fma(-zt, v, x[j]);
+                for (int t = 0; t < C; ++t) bd_st_async2(bd_mapa(la, t), z, xr - z, bd_mapa(mb2, t));
+            }
+            BD_MARK(2)
+            bd_mbar_wait(mb2, par);
+            BD_MARK(4)
+            if (wlive) {
+                if (live) {
+                    zt = agb[b][i][0];
+                    ck = agb[b][i][1];
+                }
+                // right update of the columns > k+1 (column k+1 takes the next
+                // left reflector in reflect(k+1); rowk is zero there)
+                const double zs = zt * scaleR;
+#pragma unroll
+                for (int j = 0; j < CPC; ++j) x[j] = fma(-zs, rowk[j], x[j]);
             }
             BD_MARK(5)
-            ui = reflect(k + 1, ck - zt);
-            BD_MARK(6)
-        } else if (k + 1 < m) {
-            // k = m-2: no right reflector; e_k = A[k][k+1]; column k+1 to everyone
-            if (rank == on && i < n) {
+        } else {
+            // k = m-2: no right reflector; e_k = A[k][k+1]; column k+1 from its owner to every CTA
+            if (tid == 0) bd_mbar_expect(mb2, (unsigned)(n - k - 1) * 16);
+            if (rank == on) {
+                if (i == k) a.e[k] = xk1;
+                if (live) {
+                    const unsigned la = bd_smem_addr(&agb[b][i][0]);
 #pragma unroll
-                for (int j = 0; j < CPC; ++j)
-                    if (c0 + j == k + 1) {
-                        __stcg(colg_k + i, x[j]);
-                        if (i == k) a.e[k] = x[j];
-                    }
+                    for (int t = 0; t < C; ++t) bd_st_async2(bd_mapa(la, t), 0.0, xk1, bd_mapa(mb2, t));
+                }
             }
-            bd_arrive();
-            bd_wait();
-            ui = reflect(k + 1, i < n ? __ldcg(colg_k + i) : 0.0);
+            bd_mbar_wait(mb2, par);
+            if (live) ck = agb[b][i][1];
         }
+        ui = reflect(k + 1, ck);
+        BD_MARK(6)
     }
 #undef BD_MARK
+#ifdef TTSVD_BD_PROF
+    if (a.prof && tid == TTSVD_BD_PROF_TID)
+        for (int q = 0; q < 12; ++q) a.prof[rank * 12 + q] = pacc[q];
+#endif
 #pragma unroll
     for (int j = 0; j < CPC; ++j)
         if (i < n && c0 + j < m) a.A[(int64_t)(c0 + j) * n + i] = x[j];
