@@ -387,72 +387,44 @@ __device__ __forceinline__ void bd_st_async2(unsigned raddr, double v0, double v
                  : "memory");
 }
 
-// x[jc] for a warp-uniform jc in [0, CPC): a jump table instead of CPC selects
-template <int CPC>
-__device__ __forceinline__ double bd_pick(const double (&x)[CPC], int jc) {
-    double v = 0.0;
-    switch (jc) {
-#define BD_CASE(c) \
-    case c:        \
-        if constexpr (c < CPC) v = x[c]; \
-        break;
-        BD_CASE(0) BD_CASE(1) BD_CASE(2) BD_CASE(3) BD_CASE(4) BD_CASE(5) BD_CASE(6) BD_CASE(7)
-        BD_CASE(8) BD_CASE(9) BD_CASE(10) BD_CASE(11) BD_CASE(12) BD_CASE(13) BD_CASE(14) BD_CASE(15)
-        BD_CASE(16) BD_CASE(17) BD_CASE(18) BD_CASE(19) BD_CASE(20) BD_CASE(21) BD_CASE(22) BD_CASE(23)
-        BD_CASE(24) BD_CASE(25) BD_CASE(26) BD_CASE(27) BD_CASE(28) BD_CASE(29) BD_CASE(30) BD_CASE(31)
-#undef BD_CASE
-        default: break;
+// Register tile: thread (warp w, lane rq + 8 cg) keeps rows 32 w + rq + 8 r
+// (r < 4) of the CTA's columns cg CC .. cg CC + CC - 1 (CC = CPC / 4).
+// Column sums (w = u^T A) add the four rows inside the thread and reduce
+// over the 8 row lanes; row sums (T = A rowk) add the CC columns inside the
+// thread and reduce over the 4 column lanes, which leaves row 32 w + lane's
+// sum in that lane.  13 64-bit shuffles per warp and step at CPC = 32
+// instead of 36 with a row per thread — the SM issues one 32-bit shuffle
+// per cycle (tools/tput_probe.cu), which bound the row-per-thread layout.
+template <int CC>
+__device__ __forceinline__ double bd_colsum(double (&p)[CC], int lane) {
+#pragma unroll
+    for (int o = 4; o >= CC; o >>= 1)
+#pragma unroll
+        for (int t = 0; t < CC; ++t) p[t] += __shfl_xor_sync(0xffffffffu, p[t], o);
+#pragma unroll
+    for (int o = CC / 2; o >= 1; o >>= 1) {
+        const bool up = (lane & o) != 0;
+#pragma unroll
+        for (int t = 0; t < o; ++t) {
+            const double send = up ? p[t] : p[t + o];
+            const double keep = up ? p[t + o] : p[t];
+            p[t] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+        }
     }
-    return v;
-}
-template <int CPC>
-__device__ __forceinline__ void bd_put(double (&x)[CPC], int jc, double v) {
-    switch (jc) {
-#define BD_CASE(c) \
-    case c:        \
-        if constexpr (c < CPC) x[c] = v; \
-        break;
-        BD_CASE(0) BD_CASE(1) BD_CASE(2) BD_CASE(3) BD_CASE(4) BD_CASE(5) BD_CASE(6) BD_CASE(7)
-        BD_CASE(8) BD_CASE(9) BD_CASE(10) BD_CASE(11) BD_CASE(12) BD_CASE(13) BD_CASE(14) BD_CASE(15)
-        BD_CASE(16) BD_CASE(17) BD_CASE(18) BD_CASE(19) BD_CASE(20) BD_CASE(21) BD_CASE(22) BD_CASE(23)
-        BD_CASE(24) BD_CASE(25) BD_CASE(26) BD_CASE(27) BD_CASE(28) BD_CASE(29) BD_CASE(30) BD_CASE(31)
-#undef BD_CASE
-        default: break;
-    }
+    return p[0];  // column lane & (CC - 1) of the lane's group
 }
 
-// bd_transpose_reduce of cb * x without materialising the CPC products: at
-// CPC = 32 the first halving level forms them pairwise (x and the products
-// together would take every register of the thread)
-template <int CPC>
-__device__ __forceinline__ double bd_transpose_reduce_scaled(const double (&x)[CPC], double cb, int lane) {
-    if constexpr (CPC == 32) {
-        double p[16];
-        const bool up = (lane & 16) != 0;
+__device__ __forceinline__ double bd_rowsum4(double (&t)[4], int lane) {
+    const bool u4 = (lane & 16) != 0, u3 = (lane & 8) != 0;
 #pragma unroll
-        for (int t = 0; t < 16; ++t) {
-            const double lo = cb * x[t], hi = cb * x[t + 16];
-            const double send = up ? lo : hi;
-            const double keep = up ? hi : lo;
-            p[t] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
-        }
-#pragma unroll
-        for (int o = 8; o >= 1; o >>= 1) {
-            const bool u2 = (lane & o) != 0;
-#pragma unroll
-            for (int t = 0; t < o; ++t) {
-                const double send = u2 ? p[t] : p[t + o];
-                const double keep = u2 ? p[t + o] : p[t];
-                p[t] = keep + __shfl_xor_sync(0xffffffffu, send, o);
-            }
-        }
-        return p[0];
-    } else {
-        double p[CPC];
-#pragma unroll
-        for (int j = 0; j < CPC; ++j) p[j] = cb * x[j];
-        return bd_transpose_reduce<CPC>(p, lane);
+    for (int q = 0; q < 2; ++q) {
+        const double send = u4 ? t[q] : t[q + 2];
+        const double keep = u4 ? t[q + 2] : t[q];
+        t[q] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
     }
+    const double send = u3 ? t[0] : t[1];
+    const double keep = u3 ? t[1] : t[0];
+    return keep + __shfl_xor_sync(0xffffffffu, send, 8);  // row r = lane >> 3
 }
 
 template <int CPC, int C = kBdCluster>
@@ -460,24 +432,33 @@ __global__ void __launch_bounds__(kBdThreads, 1) bd_reg_kernel(BdArgs a) {
     cg::cluster_group cl = cg::this_cluster();
     constexpr int W = kBdThreads / 32;
     constexpr int S = kBdThreads / C;  // rows per reduction slice
+    constexpr int CC = CPC / 4;        // columns per thread
     __shared__ double wred[W][CPC], sred[W];
     __shared__ double wl[CPC], rowa[CPC], rowk[CPC];
     __shared__ double pnorm[2][C + 1];                // EN: row-norm partials of all CTAs + A[k][k+1]
-    __shared__ double rsb[2][C][S];                   // E1: T partials of my slice from every CTA
-    __shared__ double rsx[2][S];                      // E1: column k+1 on my slice (its owner's)
+    // E1: T partials of my slice from every CTA; [.][1] of the owner of
+    // column k+1 carries its x_i,k+1 (one 16-byte message)
+    __shared__ __align__(16) double rsb[2][C][S][2];
     __shared__ __align__(16) double agb[2][kBdThreads][2];  // E2: (z_i, column k+1 after the update)
     __shared__ double rs[2];
     __shared__ __align__(8) unsigned long long mbar[4];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int rq = lane & 7, cgp = lane >> 3;
     const int rank = (int)cl.block_rank();
     const int n = a.n, m = a.m;
     const int c0 = rank * CPC;
-    const int i = tid;                 // my row
-    const int si = i / S, so = i % S;  // my row's reducer CTA and slot
+    const int jc0 = cgp * CC;          // my first column (CTA-local)
     const int w0 = 32 * warp;          // my warp's first row
-    double x[CPC];
+    const int si = tid / S, so = tid % S;  // reducer CTA and slot of row tid (the row whose sums this lane sends)
+    int row[4];
 #pragma unroll
-    for (int j = 0; j < CPC; ++j) x[j] = (i < n && c0 + j < m) ? a.A[(int64_t)(c0 + j) * n + i] : 0.0;
+    for (int r = 0; r < 4; ++r) row[r] = w0 + rq + 8 * r;
+    double x[4][CC];
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int c = 0; c < CC; ++c)
+            x[r][c] = (row[r] < n && c0 + jc0 + c < m) ? a.A[(int64_t)(c0 + jc0 + c) * n + row[r]] : 0.0;
 #ifdef TTSVD_BD_PROF
     // diagnostics builds (tools/bd_prof.cu): per-phase cycles of one thread
     // per CTA, kept in registers and written once at the end
@@ -491,6 +472,28 @@ __global__ void __launch_bounds__(kBdThreads, 1) bd_reg_kernel(BdArgs a) {
     }
 #else
 #define BD_MARK(q)
+#endif
+#ifdef TTSVD_BD_TRACE
+    // diagnostics builds: globaltimer of events ev of steps [K0, K0 + 8) for
+    // thread TTSVD_BD_TRACE of every CTA: prof[((rank * 8 + ev) * 8 + k - K0]
+#ifdef TTSVD_BD_TRACE_WARPS
+    // lane 0 of every warp of CTA TTSVD_BD_TRACE_WARPS (indexed by warp)
+#define BD_TR(ev, kk)                                                                          \
+    if (a.prof && rank == TTSVD_BD_TRACE_WARPS && lane == 0 && (kk) >= TTSVD_BD_K0 && (kk) < TTSVD_BD_K0 + 8) { \
+        unsigned long long g_;                                                                 \
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_)::"memory");                       \
+        a.prof[(warp * 8 + (ev)) * 8 + (kk) - TTSVD_BD_K0] = (long long)g_;                     \
+    }
+#else
+#define BD_TR(ev, kk)                                                                          \
+    if (a.prof && tid == TTSVD_BD_TRACE && (kk) >= TTSVD_BD_K0 && (kk) < TTSVD_BD_K0 + 8) {     \
+        unsigned long long g_;                                                                 \
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_)::"memory");                       \
+        a.prof[(rank * 8 + (ev)) * 8 + (kk) - TTSVD_BD_K0] = (long long)g_;                     \
+    }
+#endif
+#else
+#define BD_TR(ev, kk)
 #endif
     // EN needs one mbarrier per step parity: a CTA with no rows left to
     // reduce is not on the E1 -> E2 path that orders the other exchanges
@@ -510,25 +513,44 @@ __global__ void __launch_bounds__(kBdThreads, 1) bd_reg_kernel(BdArgs a) {
     // row k.  Warps whose rows all lie above k contribute zeros without
     // computing.  Also row k after the left update (rowk = rowa - wl, the
     // right reflector's row) and, when step k has a right reflector, its
-    // norm partial to every CTA (EN).  Returns u_i; the owner keeps u in its
-    // column.
-    auto reflect = [&](int k, double ck) -> double {
-        const bool below = i > k && i < n;
+    // norm partial to every CTA (EN).  u gets u_i of my rows; the owner keeps
+    // u in its column.
+    auto reflect = [&](int k, const double (&ck)[4], double (&u)[4]) {
         if (w0 + 31 >= k && w0 < n) {
-            const double cb = below ? ck : 0.0;
-            const double cs = bd_transpose_reduce_scaled<CPC>(x, cb, lane);
-            const double ss = bd_warp_sum(cb * cb);
-            if (lane < CPC) wred[warp][lane] = cs;
-            if (lane == 0) sred[warp] = ss;
-            if (i == k) {
-                rs[0] = ck;
+            double cb[4], ssp = 0.0;
 #pragma unroll
-                for (int j = 0; j < CPC; ++j) rowa[j] = x[j];
+            for (int r = 0; r < 4; ++r) {
+                cb[r] = (row[r] > k && row[r] < n) ? ck[r] : 0.0;
+                ssp = fma(cb[r], cb[r], ssp);
+            }
+            double p[CC];
+#pragma unroll
+            for (int c = 0; c < CC; ++c) {
+                p[c] = cb[0] * x[0][c];
+#pragma unroll
+                for (int r = 1; r < 4; ++r) p[c] = fma(cb[r], x[r][c], p[c]);
+            }
+            const double cs = bd_colsum<CC>(p, lane);
+#pragma unroll
+            for (int o = 1; o <= 4; o <<= 1) ssp += __shfl_xor_sync(0xffffffffu, ssp, o);
+            if (rq < CC) wred[warp][jc0 + rq] = cs;
+            if (lane == 0) sred[warp] = ssp;
+            if ((k >> 5) == warp && rq == (k & 7)) {  // the four lanes holding row k (predicated stores)
+                const int rk = (k >> 3) & 3;
+#pragma unroll
+                for (int r = 0; r < 4; ++r)
+                    if (r == rk) {
+#pragma unroll
+                        for (int c = 0; c < CC; ++c) rowa[jc0 + c] = x[r][c];
+                        if (cgp == 0) rs[0] = ck[r];
+                    }
             }
         } else {
             if (lane < CPC) wred[warp][lane] = 0.0;
             if (lane == 0) sred[warp] = 0.0;
         }
+        BD_MARK(3)
+        BD_TR(0, k)
         __syncthreads();
         double sv[W];
 #pragma unroll
@@ -551,22 +573,21 @@ __global__ void __launch_bounds__(kBdThreads, 1) bd_reg_kernel(BdArgs a) {
             const int gj = c0 + tid;
             const double w = (gj > k && gj < m) ? tau * fma(scale, sj, rowa[tid]) : 0.0;
             wl[tid] = w;
-            const double r = rowa[tid] - w;
-            rk = (gj >= k + 2 && gj < m) ? r : 0.0;
-            yk = gj == k + 1 ? r : 0.0;
+            const double rr = rowa[tid] - w;
+            rk = (gj >= k + 2 && gj < m) ? rr : 0.0;
+            yk = gj == k + 1 ? rr : 0.0;
             rowk[tid] = rk;
         }
-        const double u = below ? ck * scale : (i == k ? 1.0 : 0.0);
-        if (k / CPC == rank && i >= k) {
 #pragma unroll
-            for (int j = 0; j < CPC; ++j)
-                if (c0 + j == k) x[j] = u;
-        }
+        for (int r = 0; r < 4; ++r) u[r] = (row[r] > k && row[r] < n) ? ck[r] * scale : (row[r] == k ? 1.0 : 0.0);
         if (rank == 0 && tid == 0) {
             a.d[k] = beta;
             a.tauL[k] = tau;
         }
+        BD_MARK(10)
         __syncthreads();  // wl / rowk visible; rs / rowa / wred free
+        BD_MARK(11)
+        BD_TR(1, k)
         if (warp == 0 && k + 2 < m) {
             // EN: lane t sends the row-norm partial (and A[k][k+1]) to CTA t
             const double sn = bd_warp_sum(rk * rk);
@@ -578,39 +599,65 @@ __global__ void __launch_bounds__(kBdThreads, 1) bd_reg_kernel(BdArgs a) {
                 if (rank == (k + 1) / CPC) bd_st_async(bd_mapa(bd_smem_addr(pn + C), lane), y, rb);
             }
         }
-        return u;
     };
-    // every CTA reads column 0 itself; the barrier publishes the mbarrier inits
+    // column k of the result takes u on rows >= k: straight to global memory
+    // (no later step reads the column; the final store skips it), by the
+    // owner while it waits for E2; lane (rq, cg) stores row tid = its row cg
+    auto store_u = [&](int k, const double (&u)[4]) {
+        if (k / CPC == rank && tid >= k && tid < n)
+            a.A[(int64_t)k * n + tid] = cgp == 0 ? u[0] : (cgp == 1 ? u[1] : (cgp == 2 ? u[2] : u[3]));
+    };
+    // every CTA reads column 0 itself (before the barrier: step 0 stores u_0
+    // over it); the barrier publishes the mbarrier inits
+    double ui[4], ck[4], xpre[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+    for (int r = 0; r < 4; ++r) ck[r] = row[r] < n ? a.A[row[r]] : 0.0;
+    if (rank == 0 && cgp == 1 / CC) {  // column 1 for step 0
+#pragma unroll
+        for (int r = 0; r < 4; ++r) xpre[r] = x[r][1 % CC];
+    }
     bd_arrive();
     bd_wait();
     if (tid == 0 && 2 < m) bd_mbar_expect(mbn0, (unsigned)(C + 1) * 8);
-    double ui = reflect(0, i < n ? a.A[i] : 0.0);
+    reflect(0, ck, ui);
     for (int k = 0; k < m; ++k) {
         BD_MARK(0)
         const int b = k & 1;
         const unsigned par = (unsigned)(k & 1);
         const int on = (k + 1) / CPC;  // owner of column k+1
-        const bool live = i > k && i < n;  // rows of step k's right update
-        const bool wlive = w0 + 31 > k && w0 < n;
-        double T = 0.0, xk1 = 0.0;
+        const int lk1 = k + 1 - c0;    // its local index (owner)
+        const bool live = tid > k && tid < n;  // row tid takes part in step k's right update
+        double T = 0.0;
         if (w0 + 31 >= k && w0 < n) {
             // left update (rows >= k) fused with T_i = sum_j x_ij rowk_j
             double T4[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-            for (int j = 0; j < CPC; ++j) {
-                x[j] = fma(-wl[j], ui, x[j]);
-                T4[j & 3] = fma(x[j], rowk[j], T4[j & 3]);
-            }
-            T = bd_tree_sum<4>(T4);
-        }
-        if (k + 1 >= m) break;
-        if (rank == on) {
+            for (int c = 0; c < CC; ++c) {
+                const double wc = wl[jc0 + c], rc = rowk[jc0 + c];
 #pragma unroll
-            for (int j = 0; j < CPC; ++j)
-                if (c0 + j == k + 1) xk1 = x[j];
+                for (int r = 0; r < 4; ++r) {
+                    x[r][c] = fma(-wc, ui[r], x[r][c]);
+                    T4[r] = fma(x[r][c], rc, T4[r]);
+                }
+            }
+            T = bd_rowsum4(T4, lane);
+        }
+        if (k + 1 >= m) {
+            store_u(k, ui);
+            break;
+        }
+        // the owner's column k+1 on my rows (lanes of its column group): the
+        // left update of xpre, picked out of x during the previous step's
+        // wait for E2 (a select chain off the critical path)
+        const bool hold1 = rank == on && lk1 / CC == cgp;
+        double xk1[4];
+        {
+            const double w1 = wl[hold1 ? lk1 : 0];
+#pragma unroll
+            for (int r = 0; r < 4; ++r) xk1[r] = hold1 ? fma(-w1, ui[r], xpre[r]) : 0.0;
         }
         BD_MARK(7)
-        double zt = 0.0, ck = 0.0;
+        double zt[4] = {0.0, 0.0, 0.0, 0.0};
         if (k + 2 < m) {
             const int cr = max(0, s_hi - max(s_lo, k + 1));  // my slice's rows in (k, n)
             if (tid == 0) {
@@ -619,14 +666,24 @@ __global__ void __launch_bounds__(kBdThreads, 1) bd_reg_kernel(BdArgs a) {
                 if (k + 3 < m) bd_mbar_expect(mbn0 + 8 * ((k + 1) & 1), (unsigned)(C + 1) * 8);  // EN of step k + 1
             }
             // ---- E1 (reduce-scatter): T_i (and the owner's x_i,k+1) to the row's reducer ----
-            if (live) {
-                bd_st_async(bd_mapa(bd_smem_addr(&rsb[b][rank][so]), si), T, r_mb1);
-                if (rank == on) bd_st_async(bd_mapa(bd_smem_addr(&rsx[b][so]), si), xk1, r_mb1);
+            if (rank == on) {
+                // x_i,k+1 of row tid from the lane of column k+1's group
+                // holding it (its row cg of this lane's rq)
+                const int src = rq + 8 * (lk1 / CC);
+                double v[4];
+#pragma unroll
+                for (int r = 0; r < 4; ++r) v[r] = __shfl_sync(0xffffffffu, xk1[r], src);
+                const double xv = cgp == 0 ? v[0] : (cgp == 1 ? v[1] : (cgp == 2 ? v[2] : v[3]));
+                if (live) bd_st_async2(bd_mapa(bd_smem_addr(&rsb[b][rank][so][0]), si), T, xv, r_mb1);
+            } else if (live) {
+                bd_st_async(bd_mapa(bd_smem_addr(&rsb[b][rank][so][0]), si), T, r_mb1);
             }
             BD_MARK(1)
+            BD_TR(2, k)
             // the right reflector from EN (sent at the end of reflect(k))
             bd_mbar_wait(mbn0 + 8 * b, (unsigned)((k >> 1) & 1));
             BD_MARK(8)
+            BD_TR(3, k)
             const double* pn = pnorm[b];
             double pv[C];
 #pragma unroll
@@ -645,55 +702,98 @@ __global__ void __launch_bounds__(kBdThreads, 1) bd_reg_kernel(BdArgs a) {
             // ---- E2 (all-gather): the reducer's rows (z_i, x_i,k+1 - z_i) to every CTA ----
             if (live && si == rank) {
                 bd_mbar_wait(mb1, par);
+                BD_TR(4, k)
                 double q[C];
 #pragma unroll
-                for (int t = 0; t < C; ++t) q[t] = rsb[b][t][so];
-                const double xr = rsx[b][so];
+                for (int t = 0; t < C; ++t) q[t] = rsb[b][t][so][0];
+                const double xr = rsb[b][(k + 1) / CPC][so][1];
                 const double z = tauR * fma(scaleR, bd_tree_sum<C>(q), xr);
-                const unsigned la = bd_smem_addr(&agb[b][i][0]);
+                const unsigned la = bd_smem_addr(&agb[b][tid][0]);
 #pragma unroll
                 for (int t = 0; t < C; ++t) bd_st_async2(bd_mapa(la, t), z, xr - z, bd_mapa(mb2, t));
             }
             BD_MARK(2)
+            BD_TR(5, k)
+            store_u(k, ui);
+            // column k+2 before this step's right update, for step k+1
+            const int lk2 = k + 2 - c0;
+            const bool hold2 = rank == (k + 2) / CPC && lk2 / CC == cgp;
+            if (hold2) {
+                const int c2 = lk2 % CC;
+#pragma unroll
+                for (int r = 0; r < 4; ++r)
+#pragma unroll
+                    for (int c = 0; c < CC; ++c)
+                        if (c == c2) xpre[r] = x[r][c];
+            }
             bd_mbar_wait(mb2, par);
             BD_MARK(4)
-            if (wlive) {
-                if (live) {
-                    zt = agb[b][i][0];
-                    ck = agb[b][i][1];
-                }
+            BD_TR(6, k)
+            if (w0 + 31 > k && w0 < n) {
+#pragma unroll
+                for (int r = 0; r < 4; ++r)
+                    if (row[r] > k && row[r] < n) {
+                        const double2 v = *reinterpret_cast<const double2*>(&agb[b][row[r]][0]);
+                        zt[r] = v.x;
+                        ck[r] = v.y;
+                    } else {
+                        ck[r] = 0.0;
+                    }
                 // right update of the columns > k+1 (column k+1 takes the next
                 // left reflector in reflect(k+1); rowk is zero there)
-                const double zs = zt * scaleR;
+                double zs[4];
 #pragma unroll
-                for (int j = 0; j < CPC; ++j) x[j] = fma(-zs, rowk[j], x[j]);
+                for (int r = 0; r < 4; ++r) zs[r] = zt[r] * scaleR;
+#pragma unroll
+                for (int c = 0; c < CC; ++c) {
+                    const double rc = rowk[jc0 + c];
+#pragma unroll
+                    for (int r = 0; r < 4; ++r) x[r][c] = fma(-zs[r], rc, x[r][c]);
+                }
+                if (hold2) {
+                    const double rc = rowk[hold2 ? lk2 : 0];
+#pragma unroll
+                    for (int r = 0; r < 4; ++r) xpre[r] = fma(-zs[r], rc, xpre[r]);
+                }
+            } else {
+#pragma unroll
+                for (int r = 0; r < 4; ++r) ck[r] = 0.0;
             }
             BD_MARK(5)
         } else {
             // k = m-2: no right reflector; e_k = A[k][k+1]; column k+1 from its owner to every CTA
             if (tid == 0) bd_mbar_expect(mb2, (unsigned)(n - k - 1) * 16);
-            if (rank == on) {
-                if (i == k) a.e[k] = xk1;
-                if (live) {
-                    const unsigned la = bd_smem_addr(&agb[b][i][0]);
+            store_u(k, ui);
+            if (hold1) {
 #pragma unroll
-                    for (int t = 0; t < C; ++t) bd_st_async2(bd_mapa(la, t), 0.0, xk1, bd_mapa(mb2, t));
+                for (int r = 0; r < 4; ++r) {
+                    if (row[r] == k) a.e[k] = xk1[r];
+                    if (row[r] > k && row[r] < n) {
+                        const unsigned la = bd_smem_addr(&agb[b][row[r]][0]);
+#pragma unroll
+                        for (int t = 0; t < C; ++t) bd_st_async2(bd_mapa(la, t), 0.0, xk1[r], bd_mapa(mb2, t));
+                    }
                 }
             }
             bd_mbar_wait(mb2, par);
-            if (live) ck = agb[b][i][1];
+#pragma unroll
+            for (int r = 0; r < 4; ++r) ck[r] = (row[r] > k && row[r] < n) ? agb[b][row[r]][1] : 0.0;
         }
-        ui = reflect(k + 1, ck);
+        reflect(k + 1, ck, ui);
         BD_MARK(6)
     }
 #undef BD_MARK
+#undef BD_TR
 #ifdef TTSVD_BD_PROF
     if (a.prof && tid == TTSVD_BD_PROF_TID)
         for (int q = 0; q < 12; ++q) a.prof[rank * 12 + q] = pacc[q];
 #endif
+    // rows above the diagonal (the rows >= j of column j hold u_j already)
 #pragma unroll
-    for (int j = 0; j < CPC; ++j)
-        if (i < n && c0 + j < m) a.A[(int64_t)(c0 + j) * n + i] = x[j];
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int c = 0; c < CC; ++c)
+            if (row[r] < c0 + jc0 + c && c0 + jc0 + c < m) a.A[(int64_t)(c0 + jc0 + c) * n + row[r]] = x[r][c];
 }
 
 // off-diagonal t (0..2m-2) of the Golub-Kahan tridiagonal: d0 e0 d1 e1 ... d_{m-1}

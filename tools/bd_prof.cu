@@ -9,7 +9,9 @@
 #include <cmath>
 #include <random>
 #include <cuda_runtime.h>
+#ifndef BD_NOPROF
 #define TTSVD_BD_PROF 1
+#endif
 #ifndef TTSVD_BD_PROF_TID
 #define TTSVD_BD_PROF_TID 0
 #endif
@@ -94,10 +96,10 @@ int main(int argc, char** argv) {
         if (rep < 2) continue;
         for (int r = 0; r < 16; ++r) {
             long long tot = 0;
-            for (int q = 0; q < 10; ++q) tot += p[r * 12 + q];
+            for (int q = 0; q < 12; ++q) tot += p[r * 12 + q];
             if (!tot) continue;
             printf("  cta %2d cycles/step:", r);
-            for (int q = 0; q < 10; ++q) printf(" [%d] %5.0f", q, (double)p[r * 12 + q] / m);
+            for (int q = 0; q < 12; ++q) printf(" [%d] %4.0f", q, (double)p[r * 12 + q] / m);
             printf("  total %.0f\n", (double)tot / m);
         }
     }

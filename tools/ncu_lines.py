@@ -1,5 +1,7 @@
 """Attribute ncu warp-stall samples of one kernel to CUDA source lines.
-usage: python tools/ncu_lines.py report.ncu-rep kernel_regex lib.so [topN]"""
+usage: python tools/ncu_lines.py report.ncu-rep kernel_regex lib.so [topN] [ncu_kernel_regex]
+(kernel_regex matches the mangled SASS section; ncu_kernel_regex, default the
+same, the report's demangled kernel name)"""
 import csv
 import re
 import subprocess
@@ -11,6 +13,7 @@ import os
 def main():
     rep, kre, so = sys.argv[1], sys.argv[2], sys.argv[3]
     top = int(sys.argv[4]) if len(sys.argv) > 4 else 25
+    nkre = sys.argv[5] if len(sys.argv) > 5 else kre
     tmp = tempfile.mkdtemp()
     subprocess.run(["cuobjdump", "-xelf", "all", os.path.abspath(so)], cwd=tmp, check=True, capture_output=True)
     cub = [f for f in os.listdir(tmp) if f.endswith(".cubin")][0]
@@ -31,7 +34,7 @@ def main():
         m = re.search(r"/\*([0-9a-f]{4,})\*/", l)
         if m and cur:
             lines[int(m.group(1), 16)] = cur
-    out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "-k", "regex:" + kre], capture_output=True,
+    out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "-k", "regex:" + nkre], capture_output=True,
                          text=True).stdout
     r = list(csv.reader(out.splitlines()))
     h = r[1]
