@@ -66,7 +66,8 @@ enum {
     TTSVD_K_T128 = 4,  /* 128-row tiles, one CTA per SM */
     TTSVD_K_GQR = 5,   /* cooperative whole-grid QR */
     TTSVD_K_PT = 6,    /* thread streams, m <= 8 */
-    TTSVD_K_GS = 7     /* lane-group streams, 8 < m <= 32 */
+    TTSVD_K_GS = 7,    /* lane-group streams, 8 < m <= 32 */
+    TTSVD_K_SQ = 8     /* levels of 256-row register tile QRs, 32 < m <= 64 */
 };
 
 /* All-gather over the ranks of a distributed run (replaces the in-process

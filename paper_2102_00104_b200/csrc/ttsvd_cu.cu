@@ -32,6 +32,7 @@
 #include "tsqr_t128.cuh"
 #include "tsqr_ws.cuh"
 #include "tsqr_pt.cuh"
+#include "tsqr_sq.cuh"
 
 using namespace ttsvd_b200;
 
@@ -550,12 +551,43 @@ int tsqr_gs_device(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t
     return m <= 16 ? tsqr_gs_levels<16, 4, 8>(ctx, X, n, m, ld, R) : tsqr_gs_levels<32, 8, 8>(ctx, X, n, m, ld, R);
 }
 
+// 32 < m <= 64, small n: levels of 256-row register tile QRs (tsqr_sq.cuh),
+// each cutting the rows by 256 / m, until one tile is left.
+int tsqr_sq_levels(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t ld, double* R) {
+    const double* src = X;
+    int64_t rows = n, sld = ld;
+    int flip = 0;
+    for (;;) {
+        const int64_t T = (rows + kSqRows - 1) / kSqRows;
+        if (T > 1) {
+            TT_TRY(ensure(ctx->ws_R, (size_t)T * m * m * 8));
+            TT_TRY(ensure(ctx->ws_R2, (size_t)T * m * m * 8));
+        }
+        double* out = (T == 1) ? R : as<double>(flip ? ctx->ws_R2 : ctx->ws_R);
+        const int64_t ldo = (T == 1) ? m : T * m;
+        SqArgs sa{src, rows, sld, m, T, out, ldo};
+        tsqr_sq_kernel<<<(unsigned)T, kSqThreads, 0, ctx->stream>>>(sa);
+        TT_TRY(check_launch(ctx, "tsqr_sq_kernel"));
+        if (T == 1) return TTSVD_OK;
+        src = out;
+        rows = T * m;
+        sld = T * m;
+        flip ^= 1;
+    }
+}
+
 int tsqr_device(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t ld, double* R,
                 const double* R_init = nullptr) {
     ctx->last_kernel = TTSVD_K_NONE;
     if (m > kSmallM) {
         const int M = (m + 31) / 32 * 32;
         const int64_t RS = blk_rsize(M);
+        if (!R_init && m <= 64 && n <= kSqMaxRows) {
+            kmark(ctx, 0, TTSVD_K_SQ);
+            const int rc = tsqr_sq_levels(ctx, X, n, m, ld, R);
+            kmark(ctx, 1, TTSVD_K_SQ);
+            return rc;
+        }
         // Short-fat (n <= 256 M, n <= 512 rows per SM): one cooperative grid
         // factorises the whole matrix (gqr.cuh), no merge tree.
         if (!R_init && n >= M && n <= (int64_t)256 * M) {

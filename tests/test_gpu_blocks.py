@@ -109,6 +109,38 @@ def test_tsqr_wide_kernels(tt, n, m, kind):
         assert s_r[rank] <= 1e-13 * s_r[0]
 
 
+# The register tile levels (tsqr_sq_kernel, 32 < m <= 64, n <= 2^16: 256-row
+# tile QRs, their stacked factors the next level's rows): partial tiles, one to five levels, zero / duplicated columns, low
+# rank and subnormal squares.
+@pytest.mark.parametrize("n,m,kind", [(40, 33, "dense"), (64, 64, "dense"), (65, 33, "dup"), (256, 64, "dense"),
+                                      (257, 48, "lowrank"), (1000, 64, "tiny"), (4096, 64, "dup"),
+                                      (16384, 64, "dense"), (65536, 40, "dense"), (50001, 63, "dup")])
+def test_tsqr_register_tiles(tt, n, m, kind):
+    from oracle.oracle import gaussian
+    X = gaussian(n, m, 51 + m).copy(order="F")
+    if kind == "dup":
+        X[:, m - 1] = X[:, 0]
+        X[:, 1] = 0.0
+    if kind == "lowrank":
+        X = np.asfortranarray(gaussian(n, 3, 5) @ gaussian(3, m, 6))
+    if kind == "tiny":
+        X[:, 3] *= 1e-156
+        X[:, 40] = 0.0
+    R = host(tt.tsqr(X))
+    assert np.all(np.isfinite(R))
+    assert np.all(np.tril(R, -1) == 0.0)
+    assert gram_resid(X, R) <= 1e-12
+    s_r = np.linalg.svd(R, compute_uv=False)
+    s_x = np.linalg.svd(X, compute_uv=False)
+    assert np.max(np.abs(s_r - s_x)) <= 1e-10 * s_x[0]
+    if kind in ("dup", "lowrank"):
+        rank = 3 if kind == "lowrank" else m - 2
+        assert s_r[rank] <= 1e-13 * s_r[0]
+    cn_r, cn_x = np.linalg.norm(R, axis=0), np.linalg.norm(X, axis=0)
+    assert np.allclose(cn_r, cn_x, rtol=1e-6 if kind == "tiny" else 1e-12, atol=1e-150)
+    assert np.array_equal(host(tt.tsqr(X)), R)
+
+
 # The thread-stream kernel (tsqr_pt_kernel, m <= 8, n >= 4096: every thread
 # folds 8 strided rows at a time into its own R) and the lane-group kernel
 # (tsqr_gs_kernel, 8 < m <= 32: 4 or 8 lanes share a stream by columns);
