@@ -1193,7 +1193,7 @@ __global__ void __launch_bounds__(kBack4Warps * 32) bd_back4_kernel(const double
 // and reductions instead of an L2 round trip (the register prefetch of
 // bd_back4_kernel looks one reflector ahead, less than the L2 latency).
 constexpr int kB4sChunk = 16;
-constexpr int kB4sWarps = 16;  // warps per CTA
+constexpr int kB4sWarps = 4;  // warps per CTA: 8 CTAs for r = 32 (m = 512 SVD 2.21 -> 2.12 ms; 16 warps: 2 CTAs, 2 warps: 2.14)
 constexpr int kB4sVpw = 1;    // vectors per warp
 
 __device__ __forceinline__ void bd_cp_async16(void* smem_dst, const void* gsrc) {
