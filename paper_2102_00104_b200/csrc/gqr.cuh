@@ -61,6 +61,12 @@ __device__ __forceinline__ double warp_reduce_scatter32(double (&v)[32], int lan
     return (b0 ? v[1] : v[0]) + __shfl_xor_sync(0xffffffffu, b0 ? v[0] : v[1], 1);
 }
 
+__device__ __forceinline__ double gqr_warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
 // sum over q = first, first + step, ... < G of base[q * qstride] (L2 reads,
 // data of other CTAs) in a fixed association order, so every CTA computes
 // bit-identical totals; CH loads in flight per chunk (one L2 round trip per
@@ -160,32 +166,35 @@ __global__ void __launch_bounds__(NT, 1) gqr_kernel(GqrArgs a) {
             const int64_t j = c0 + jj;
             const int buf = jj & 1;
             long long tr0 = pf ? gqr_clock() : 0;
-            // partials over my rows below the pivot: v[0] = sum x_j^2, v[k] = sum x_j x_k (k > jj)
-            double v[32];
+            // partials over my rows below the pivot: value 0 = sum x_j^2, value
+            // k = sum x_j x_k (k > jj).  Warp w takes columns CPW w .. + CPW - 1,
+            // its lanes stride the rows (both loads contiguous across lanes),
+            // then a butterfly per column: CPW x 5 shuffles per warp instead
+            // of a 31-shuffle reduce-scatter of every row's 32 products (the SM
+            // issues one 32-bit shuffle per cycle)
+            {
+                constexpr int NW = NT / 32, CPW = 32 / NW;
+                const int i_lo = (int)(j - r0 + 1 > 0 ? (j - r0 + 1 < rows ? j - r0 + 1 : rows) : 0);
+                if (tid < 32 && j >= r0 && j < r0 + rows && tid >= jj)  // pivot row -> broadcast slot
+                    a.piv[buf * 32 + tid] = Ys[tid * ldy + (int)(j - r0)];
+                const double* yj = Ys + jj * ldy;
+                double sk[CPW];
 #pragma unroll
-            for (int k = 0; k < 32; ++k) v[k] = 0.0;
-            for (int i = tid; i < rows; i += NT) {
-                const int64_t gi = r0 + i;
-                if (gi <= j) {
-                    if (gi == j)  // pivot row -> broadcast slot
-                        for (int k = jj; k < 32; ++k) a.piv[buf * 32 + k] = Ys[k * ldy + i];
-                    continue;
+                for (int q = 0; q < CPW; ++q) sk[q] = 0.0;
+                if (CPW * warp + CPW - 1 >= jj) {
+                    for (int i = i_lo + lane; i < rows; i += 32) {
+                        const double xj = yj[i];
+#pragma unroll
+                        for (int q = 0; q < CPW; ++q) sk[q] = fma(xj, Ys[(CPW * warp + q) * ldy + i], sk[q]);
+                    }
+#pragma unroll
+                    for (int q = 0; q < CPW; ++q) sk[q] = gqr_warp_sum(sk[q]);
                 }
-                const double xj = Ys[jj * ldy + i];
-                v[0] = fma(xj, xj, v[0]);
+                if (lane == 0)
 #pragma unroll
-                for (int k = 1; k < 32; ++k)
-                    if (k > jj) v[k] = fma(xj, Ys[k * ldy + i], v[k]);
-            }
-            // block reduction of the 32 values: warp reduce-scatter (lane k ends
-            // with the warp's total of value k, 31 shuffles), then warps via smem
-            const double vk = warp_reduce_scatter32(v, lane);
-            red[warp * 33 + lane] = vk;
-            __syncthreads();
-            if (tid < 32) {
-                double t = 0.0;
-                for (int w = 0; w < NT / 32; ++w) t += red[w * 33 + tid];
-                part[((int64_t)buf * G + c) * 33 + tid] = t;
+                    for (int q = 0; q < CPW; ++q) red[CPW * warp + q] = sk[q];
+                __syncthreads();
+                if (tid < 32) part[((int64_t)buf * G + c) * 33 + tid] = tid == 0 ? red[jj] : (tid > jj ? red[tid] : 0.0);
             }
             long long tq0 = pf ? gqr_clock() : 0;
             if (pf) a.prof[6] += tq0 - tr0;
