@@ -62,6 +62,17 @@ def test_driver_svd_random(tt, n, m, r):
     check(tt, A, r, ang_tol=1e-9)
 
 
+# the register-tile bidiagonalisation at every (columns per CTA, cluster)
+# instantiation and at row counts that leave warps, lanes or whole reducer
+# slices empty (the DSMEM exchanges count only the live rows)
+@pytest.mark.parametrize("n,m,r", [(33, 33, 8), (129, 129, 16), (250, 250, 32), (257, 257, 32), (511, 511, 32),
+                                   (512, 300, 32), (400, 400, 64), (480, 17, 17), (96, 65, 20)])
+def test_driver_svd_tile_shapes(tt, n, m, r):
+    rng = np.random.default_rng(n * 13 + m)
+    A = np.asfortranarray(rng.standard_normal((n, m)))
+    check(tt, A, r, ang_tol=1e-9)
+
+
 def test_driver_svd_config2_like(tt):
     # exact rank 32 + 1e-8 relative noise (the config-2 work matrices)
     rng = np.random.default_rng(3)
