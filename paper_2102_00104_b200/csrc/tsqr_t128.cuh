@@ -54,121 +54,146 @@ __device__ __forceinline__ void t2_bar_panel() {
 template <int ID = 3>
 __device__ __forceinline__ void t2_bar_t() { asm volatile("bar.sync %0, 128;" ::"n"(ID) : "memory"); }
 
-// panel warps 0..3: factor the 128 x 32 panel in P (ld kT2Pld) against the
+// panel warps: factor the (32 PW) x 32 panel in P (ld 32 PW + 4) against the
 // diagonal R block Rp; leaves V in P, the new block in Rp, tau, striu(S) in Sm.
+// Register tile: lane (rq, cg) = rq + 8 cg of warp w keeps rows
+// 32 w + rq + 8 r (r < 4) of columns 8 cg + c (c < 8).  Reflector j: the four
+// lanes of column j's group broadcast its rows (4 shuffles), each lane forms
+// its eight column dots over its four rows and a transpose-reduce over the 8
+// row lanes leaves column `lane`'s warp partial in lane `lane` (7 shuffles);
+// the PW partials meet in shared memory (one named barrier) and lane c derives
+// column c's scalars as before (it "owns" column c); the f of its 8 register
+// columns come back through a per-warp shared row.  (A column per lane with
+// 32 rows needed the pivot lane to store its 32 values every reflector: ~400
+// of ~1.7 k cycles per reflector.)
 template <int PW, int BAR = 2>
 __device__ __forceinline__ void t2_panel(double* P, double* Rp, double* tau, double* pvall, double* dpart, double* Sm,
                                          int warp, int lane) {
     constexpr int Pld = 32 * PW + 4;
-    double* pv = pvall + 32 * warp;
-    double x[32];
+    const int rq = lane & 7, cg = lane >> 3;
+    double* fb = pvall + 32 * warp;  // per-warp f of the 32 columns
+    double x[4][8];
 #pragma unroll
-    for (int i = 0; i < 32; i += 2) {
-        const double2 t = *reinterpret_cast<const double2*>(P + lane * Pld + 32 * warp + i);
-        x[i] = t.x;
-        x[i + 1] = t.y;
-    }
-    const unsigned s_pv = (unsigned)__cvta_generic_to_shared(pv);
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int c = 0; c < 8; ++c) x[r][c] = P[(8 * cg + c) * Pld + 32 * warp + rq + 8 * r];
+    const unsigned s_fb = (unsigned)__cvta_generic_to_shared(fb);
     const unsigned s_rcol = (unsigned)__cvta_generic_to_shared(Rp + lane * kLaRld);
     const unsigned s_scol = (unsigned)__cvta_generic_to_shared(Sm + lane * kTld);
     const unsigned s_dp = (unsigned)__cvta_generic_to_shared(dpart);
     const unsigned s_rp = (unsigned)__cvta_generic_to_shared(Rp);
     const unsigned s_tau = (unsigned)__cvta_generic_to_shared(tau);
     const bool w0 = (warp == 0);
-    double my_scale = 1.0;
+    double my_scale = 1.0;  // scale of the reflector of column `lane`
     // warp 0 writes row j of the R block one reflector late (the other panel
     // warps may still be reading it)
     double pend_r = 0.0, pend_alpha = 0.0, pend_tau = 0.0;
     bool pend_upd = false;
     int pend_j = -1;
 #pragma unroll 1
-    for (int j = 0; j < 32; ++j) {
-        const int par = j & 1;
-        const bool piv = (lane == j);
+    for (int cgj = 0; cgj < 4; ++cgj) {
 #pragma unroll
-        for (int i = 0; i < 32; i += 2) sts2_if(piv, s_pv + 8 * i, x[i], x[i + 1]);
-        __syncwarp();
-        double a[8];
+        for (int cj = 0; cj < 8; ++cj) {
+            const int j = 8 * cgj + cj;
+            const int par = j & 1;
+            // pivot column j on my four rows
+            double pr[4];
 #pragma unroll
-        for (int i = 0; i < 32; i += 2) {
-            const double2 p0 = lds2(s_pv + 8 * i);
-            if (i < 16) {
-                a[i / 2] = p0.x * x[i];
-                a[i / 2] = fma(p0.y, x[i + 1], a[i / 2]);
-            } else {
-                a[(i - 16) / 2] = fma(p0.x, x[i], a[(i - 16) / 2]);
-                a[(i - 16) / 2] = fma(p0.y, x[i + 1], a[(i - 16) / 2]);
+            for (int r = 0; r < 4; ++r) pr[r] = __shfl_sync(0xffffffffu, x[r][cj], rq + 8 * cgj);
+            double a[8];
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+                a[c] = pr[0] * x[0][c];
+#pragma unroll
+                for (int r = 1; r < 4; ++r) a[c] = fma(pr[r], x[r][c], a[c]);
             }
-        }
-        const double dk = ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
-        sts1_if(true, s_dp + 8 * (par * 32 * PW + warp * 32 + lane), dk);
-        t2_bar_panel<PW, BAR>();
-        if (w0 && pend_j >= 0) {  // everyone is past reflector j-1: publish its R row
-            sts1_if(pend_upd, s_rcol + 8 * pend_j, pend_r);
-            sts1_if(lane == pend_j, s_rp + 8 * pend_j * (kLaRld + 1), pend_alpha);
-            sts1_if(lane == pend_j, s_tau + 8 * pend_j, pend_tau);
-        }
-        double dv[PW], sv[PW];
+            // transpose-reduce over the row lanes (bits 2, 1, 0 of the lane):
+            // lane ends with column 8 cg + rq = lane
 #pragma unroll
-        for (int w = 0; w < PW; ++w) {
-            dv[w] = lds1(s_dp + 8 * (par * 32 * PW + 32 * w + lane));
-            sv[w] = lds1(s_dp + 8 * (par * 32 * PW + 32 * w + j));
-        }
-        if constexpr ((PW & (PW - 1)) == 0) {
+            for (int o = 4; o >= 1; o >>= 1) {
+                const bool up = (lane & o) != 0;
 #pragma unroll
-            for (int h = PW / 2; h >= 1; h >>= 1)
-#pragma unroll
-                for (int w = 0; w < h; ++w) {
-                    dv[w] = dv[w] + dv[w + h];
-                    sv[w] = sv[w] + sv[w + h];
+                for (int t = 0; t < o; ++t) {
+                    const double send = up ? a[t] : a[t + o];
+                    const double keep = up ? a[t + o] : a[t];
+                    a[t] = keep + __shfl_xor_sync(0xffffffffu, send, o);
                 }
-        } else {
-#pragma unroll
-            for (int w = 1; w < PW; ++w) {
-                dv[0] += dv[w];
-                sv[0] += sv[w];
             }
-        }
-        const double d = dv[0], sp = sv[0];
-        const double u0 = lds1(s_rp + 8 * j * (kLaRld + 1));
-        const double rjc = lds1(s_rcol + 8 * j);
-        const double nrm2 = u0 * u0 + sp;
-        const double inv = fast_rsqrt(nrm2);
-        const double nr = nrm2 * inv;
-        const double au = fabs(u0);
-        const double sg = (u0 > 0.0) ? 1.0 : -1.0;
-        double alpha = -sg * nr;
-        double tj = 1.0 + au * inv;
-        double scale = sg * fast_rcp(au + nr);
-        if (sp == 0.0 && u0 != 0.0) {  // H = I
-            alpha = u0;
-            tj = 0.0;
-            scale = 0.0;
-        }
-        if (nrm2 == 0.0) {  // all-zero u
-            alpha = sqrt(2.0 * DBL_MIN);
-            tj = 2.0;
-            scale = 0.0;
-        }
-        const bool upd = lane > j;
-        const double g = tj * (rjc + scale * d);
-        const double f = upd ? g * scale : 0.0;
-        my_scale = piv ? scale : my_scale;
-        if (w0) {
-            sts1_if(lane < j, s_scol + 8 * j, my_scale * scale * d);  // S(c, j) = v_c . v_j
-            pend_r = rjc - g;
-            pend_upd = upd;
-            pend_alpha = alpha;
-            pend_tau = tj;
-            pend_j = j;
-        }
+            sts1_if(true, s_dp + 8 * (par * 32 * PW + warp * 32 + lane), a[0]);
+            t2_bar_panel<PW, BAR>();
+            if (w0 && pend_j >= 0) {  // everyone is past reflector j-1: publish its R row
+                sts1_if(pend_upd, s_rcol + 8 * pend_j, pend_r);
+                sts1_if(lane == pend_j, s_rp + 8 * pend_j * (kLaRld + 1), pend_alpha);
+                sts1_if(lane == pend_j, s_tau + 8 * pend_j, pend_tau);
+            }
+            double dv[PW], sv[PW];
 #pragma unroll
-        for (int i = 0; i < 32; i += 2) {
-            const double2 p0 = lds2(s_pv + 8 * i);
-            x[i] = fma(-f, p0.x, x[i]);
-            x[i + 1] = fma(-f, p0.y, x[i + 1]);
+            for (int w = 0; w < PW; ++w) {
+                dv[w] = lds1(s_dp + 8 * (par * 32 * PW + 32 * w + lane));
+                sv[w] = lds1(s_dp + 8 * (par * 32 * PW + 32 * w + j));
+            }
+            if constexpr ((PW & (PW - 1)) == 0) {
+#pragma unroll
+                for (int h = PW / 2; h >= 1; h >>= 1)
+#pragma unroll
+                    for (int w = 0; w < h; ++w) {
+                        dv[w] = dv[w] + dv[w + h];
+                        sv[w] = sv[w] + sv[w + h];
+                    }
+            } else {
+#pragma unroll
+                for (int w = 1; w < PW; ++w) {
+                    dv[0] += dv[w];
+                    sv[0] += sv[w];
+                }
+            }
+            const double d = dv[0], sp = sv[0];
+            const double u0 = lds1(s_rp + 8 * j * (kLaRld + 1));
+            const double rjc = lds1(s_rcol + 8 * j);
+            const double nrm2 = u0 * u0 + sp;
+            const double inv = fast_rsqrt(nrm2);
+            const double nr = nrm2 * inv;
+            const double au = fabs(u0);
+            const double sg = (u0 > 0.0) ? 1.0 : -1.0;
+            double alpha = -sg * nr;
+            double tj = 1.0 + au * inv;
+            double scale = sg * fast_rcp(au + nr);
+            if (sp == 0.0 && u0 != 0.0) {  // H = I
+                alpha = u0;
+                tj = 0.0;
+                scale = 0.0;
+            }
+            if (nrm2 == 0.0) {  // all-zero u
+                alpha = sqrt(2.0 * DBL_MIN);
+                tj = 2.0;
+                scale = 0.0;
+            }
+            const bool upd = lane > j;
+            const double g = tj * (rjc + scale * d);
+            const double f = upd ? g * scale : 0.0;
+            my_scale = (lane == j) ? scale : my_scale;
+            if (w0) {
+                sts1_if(lane < j, s_scol + 8 * j, my_scale * scale * d);  // S(c, j) = v_c . v_j
+                pend_r = rjc - g;
+                pend_upd = upd;
+                pend_alpha = alpha;
+                pend_tau = tj;
+                pend_j = j;
+            }
+            // f of column `lane` to the lanes holding it
+            sts1_if(true, s_fb + 8 * lane, f);
+            __syncwarp();
+#pragma unroll
+            for (int c = 0; c < 8; c += 2) {
+                const double2 t = lds2(s_fb + 8 * (8 * cg + c));
+#pragma unroll
+                for (int r = 0; r < 4; ++r) {
+                    x[r][c] = fma(-t.x, pr[r], x[r][c]);
+                    x[r][c + 1] = fma(-t.y, pr[r], x[r][c + 1]);
+                }
+            }
+            __syncwarp();
         }
-        __syncwarp();
     }
     t2_bar_panel<PW, BAR>();
     if (w0) {
@@ -176,9 +201,15 @@ __device__ __forceinline__ void t2_panel(double* P, double* Rp, double* tau, dou
         sts1_if(lane == pend_j, s_rp + 8 * pend_j * (kLaRld + 1), pend_alpha);
         sts1_if(lane == pend_j, s_tau + 8 * pend_j, pend_tau);
     }
+    // V = scale_c x (the scale of column c's reflector lives in lane c)
+    sts1_if(true, s_fb + 8 * lane, my_scale);
+    __syncwarp();
 #pragma unroll
-    for (int i = 0; i < 32; i += 2)
-        *reinterpret_cast<double2*>(P + lane * Pld + 32 * warp + i) = make_double2(my_scale * x[i], my_scale * x[i + 1]);
+    for (int c = 0; c < 8; ++c) {
+        const double sc = lds1(s_fb + 8 * (8 * cg + c));
+#pragma unroll
+        for (int r = 0; r < 4; ++r) P[(8 * cg + c) * Pld + 32 * warp + rq + 8 * r] = sc * x[r][c];
+    }
     t2_bar_panel<PW, BAR>();
 }
 
@@ -370,6 +401,8 @@ __global__ void __launch_bounds__(kT2Threads, 1) tsqr_t128_kernel(T2Args a) {
     __syncthreads();
     const int npan = M / 32;
     const bool panel_warp = warp < PW;
+#ifdef TTSVD_T2_PROF
+    // diagnostics builds: per-CTA phase cycles of thread 0
     long long t_prev = 0, t_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 #define T2_PROF(ph)                                   \
     if (a.prof && tid == 0) {                         \
@@ -377,6 +410,9 @@ __global__ void __launch_bounds__(kT2Threads, 1) tsqr_t128_kernel(T2Args a) {
         if (t_prev) t_acc[ph] += t_now - t_prev;      \
         t_prev = t_now;                               \
     }
+#else
+#define T2_PROF(ph)
+#endif
     T2_PROF(7);
     const int uw = warp - PW;  // update warp index
     for (int64_t r0 = row0; r0 < row1; r0 += ROWS) {
@@ -453,8 +489,10 @@ __global__ void __launch_bounds__(kT2Threads, 1) tsqr_t128_kernel(T2Args a) {
             T2_PROF(4);
         }
     }
+#ifdef TTSVD_T2_PROF
     if (a.prof && tid == 0)
         for (int q = 0; q < 8; ++q) a.prof[blockIdx.x * 8 + q] = t_acc[q];
+#endif
 #undef T2_PROF
 }
 
