@@ -32,6 +32,7 @@
 #include "tsqr_t128.cuh"
 #include "tsqr_ws.cuh"
 #include "tsqr_pt.cuh"
+#include "tsqr_gt.cuh"
 #include "tsqr_sq.cuh"
 
 using namespace ttsvd_b200;
@@ -545,7 +546,30 @@ int tsqr_gs_levels(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t
     return tsqr_ws_device(ctx, out, T * m, m, T * m, R, false);
 }
 
+// Tall and 16-byte aligned: the same streams fed by the bulk-copy engine
+// (tsqr_gt.cuh), one 8-warp CTA per SM, every warp at least one full slice.
+template <int M, int P, int U>
+int tsqr_gt_levels(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t ld, double* R) {
+    constexpr int G = 32 / P, SR = G * U;
+    const void* fn = (const void*)tsqr_gt_kernel<M, P, U>;
+    TT_TRY(kattr(ctx, fn, (int)gt_smem_bytes<M, P, U>()));
+    const int64_t slices = (n + SR - 1) / SR;
+    const int64_t ctas = std::min<int64_t>(ctx->num_sms, slices / kGtWarps);
+    const int64_t T = ctas * kGtWarps * G;
+    DevBuf& ob = ctx->ws_gs;
+    TT_TRY(ensure(ob, (size_t)T * m * m * 8));
+    double* out = as<double>(ob);
+    GsArgs ga{X, n, ld, m, T, out, T * m};
+    kmark(ctx, 0, TTSVD_K_GS);
+    tsqr_gt_kernel<M, P, U><<<(unsigned)ctas, kPtThreads, gt_smem_bytes<M, P, U>(), ctx->stream>>>(ga);
+    TT_TRY(check_launch(ctx, "tsqr_gt_kernel"));
+    kmark(ctx, 1, TTSVD_K_GS);
+    return tsqr_ws_device(ctx, out, T * m, m, T * m, R, false);
+}
+
 int tsqr_gs_device(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t ld, double* R) {
+    if (n >= (int64_t)ctx->num_sms * kGtWarps * 64 * 4 && (ld & 1) == 0 && ((uintptr_t)X & 15) == 0)
+        return m <= 16 ? tsqr_gt_levels<16, 4, 8>(ctx, X, n, m, ld, R) : tsqr_gt_levels<32, 8, 8>(ctx, X, n, m, ld, R);
     // measured on B200 (tools/gs_var.sh): 4 lanes per stream at m <= 16, 8 at m <= 32
     // (a whole warp per stream at 32 < m <= 64 measured slower than t128)
     return m <= 16 ? tsqr_gs_levels<16, 4, 8>(ctx, X, n, m, ld, R) : tsqr_gs_levels<32, 8, 8>(ctx, X, n, m, ld, R);

@@ -153,6 +153,20 @@ def test_tsqr_register_tiles(tt, n, m, kind):
                                       (65537, 20, "lowrank"), (300001, 32, "dup"), (8191, 25, "dense"),
                                       (200000, 9, "tiny")])
 def test_tsqr_thread_streams(tt, n, m, kind):
+    _check_streams(tt, n, m, kind)
+
+
+# The bulk-copy (TMA) staged group streams (tsqr_gt_kernel, 8 < m <= 32 and
+# n >= 4 slices per warp of the grid): full and partial last slices, m below
+# the padded width, zero / duplicated columns, low rank, subnormal squares.
+@pytest.mark.parametrize("n,m,kind", [(400003, 12, "dup"), (1 << 19, 32, "dense"), (303200, 20, "lowrank"),
+                                      (500001, 9, "tiny"), (350000, 27, "dup"), (1 << 21, 16, "dense"),
+                                      (303104, 17, "dense")])
+def test_tsqr_bulk_staged_streams(tt, n, m, kind):
+    _check_streams(tt, n, m, kind)
+
+
+def _check_streams(tt, n, m, kind):
     from oracle.oracle import gaussian
     X = gaussian(n, m, 41 + m).copy(order="F")
     if kind == "dup" and m >= 3:
