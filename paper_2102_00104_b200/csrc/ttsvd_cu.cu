@@ -80,6 +80,8 @@ struct ttsvd_cu_ctx {
     std::vector<DevBuf> ws_slab;  // tt_svd_distributed: two ping-pong work buffers per local slab
     DevBuf host_stage;  // pinned
     DevBuf host_cores;  // pinned arena of the steps' V blocks (core_from_vt after the chain)
+    DevBuf ws_rank;     // K6: per step (rank, sum sigma^2) written by rank_epilogue_kernel
+    DevBuf host_sig;    // pinned: per step the sigmas and the K6 record of a speculative chain
     cudaEvent_t ev[9] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
     // svd_work's bidiagonal path leaves the vectors for svd_vectors (the
     // driver knows the rank only after the sigmas): A holds the reflectors
@@ -1090,6 +1092,48 @@ double sigma_norm_h(const double* s, int64_t m) {
     return std::sqrt(t);
 }
 
+// K6, the rank rule on the device (derive_delta / select_rank / choose_rank,
+// small_svd.hpp:41-63, tt_svd.hpp:111-118): one thread repeats
+// choose_rank_h's arithmetic operation by operation (explicit round-to-nearest
+// multiplies and adds, no contraction) on the step's sigmas and leaves
+// (rank, sum sigma^2) in device memory, so a chain can run without a host
+// round trip per step.
+__global__ void rank_epilogue_kernel(const double* __restrict__ sigma, int64_t len, int64_t cols, int64_t nsig,
+                                     double delta, int64_t r_max, int64_t rows, double* __restrict__ rec) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    const double sigma1 = len > 0 ? sigma[0] : 0.0;
+    const double zero_level =
+        __dmul_rn(__dmul_rn(__dmul_rn(32.0, DBL_EPSILON), sigma1), sqrt((double)(rows > cols ? rows : cols)));
+    const double delta_eff = delta > zero_level ? delta : zero_level;
+    const double d2 = __dmul_rn(delta_eff, delta_eff);
+    double tail = 0.0;
+    int64_t r_delta = len;
+    for (int64_t j = len; j-- > 0;) {
+        tail = __dadd_rn(tail, __dmul_rn(sigma[j], sigma[j]));
+        if (tail <= d2) r_delta = j;
+        else break;
+    }
+    int64_t r = r_max < r_delta ? r_max : r_delta;
+    if (r < 1) r = 1;
+    const int64_t cap = len > 1 ? len : 1;
+    if (r > cap) r = cap;
+    if (r > nsig) r = nsig;
+    double t = 0.0;
+    for (int64_t j = 0; j < len; ++j) t = __dadd_rn(t, __dmul_rn(sigma[j], sigma[j]));
+    rec[0] = (double)r;
+    rec[1] = t;  // ||Sigma||_F^2 (sigma_norm_h squares and sums in the same order)
+}
+
+// the rank choose_rank_h returns when no sigma tail falls below delta_eff
+int64_t predicted_rank_h(int64_t len, int64_t nsig, int64_t r_max) {
+    int64_t r = std::min(r_max, len);
+    if (r < 1) r = 1;
+    r = std::min(r, std::max<int64_t>(len, 1));
+    return std::min(r, nsig);
+}
+
+constexpr int kMispredict = -1000;  // internal: a speculative chain met a rank below its prediction
+
 struct Timer {
     ttsvd_cu_ctx* ctx;
     bool on;
@@ -1125,14 +1169,49 @@ int d2h(ttsvd_cu_ctx* ctx, double* dst, const double* src, size_t count) {
 // small_svd.hpp:41 — run_chain takes the spec by reference, tt_svd.hpp:160);
 // out, the one used.  first_sigma_norm_out: ||Sigma||_F of the first step
 // (ChainResult::first_sigma_norm, tt_svd.hpp:153-156).
-int run_chain(ttsvd_cu_ctx* ctx, WorkView cur, const std::vector<int64_t>& dims, int64_t r_max, double eps,
-              int64_t d_for_delta, ttsvd_cu_tt* out, double* delta_io = nullptr,
-              double* first_sigma_norm_out = nullptr) {
+//
+// spec: the chain runs without a host round trip per step.  Every step's
+// rank is PREDICTED on the host (min(r_max, #sigma): what the rule gives
+// unless a sigma tail falls below delta_eff), the true rank is computed on
+// the device by rank_epilogue_kernel (K6) and lands, with the sigmas, in
+// pinned memory; after the one synchronisation that ends the chain the
+// records are compared and a chain that met a smaller rank anywhere returns
+// kMispredict (the caller runs it again step by step).  Only used when delta
+// is known up front (eps = 0, or a given delta of 0).
+int run_chain_impl(ttsvd_cu_ctx* ctx, WorkView cur, const std::vector<int64_t>& dims, int64_t r_max, double eps,
+                   int64_t d_for_delta, ttsvd_cu_tt* out, double* delta_io, double* first_sigma_norm_out,
+                   bool spec) {
     const int64_t d = (int64_t)dims.size();
     out->dims = dims;
     out->cores.assign(d, {});
     out->ranks.assign(d + 1, 1);
+    out->steps.clear();
+    out->sigmas.clear();
     double delta = delta_io ? *delta_io : -1.0;
+    struct SpecStep {
+        size_t off;  // of the step's record in host_sig (doubles): nsig sigmas, then (rank, sum sigma^2)
+        int64_t nsig, pred;
+    };
+    std::vector<SpecStep> spec_steps;
+    size_t spec_off = 0;
+    if (spec) {
+        if (delta < 0.0) {
+            if (d_for_delta < 2) return fail(TTSVD_ERR_DEGENERATE, "derive_delta: requires d >= 2");
+            delta = 0.0;  // eps = 0: delta = 0 whatever the first step's norm is
+        }
+        // the predicted shapes give the size of the pinned record arena
+        size_t need = 0;
+        int64_t rows_s = cur.rows, r_s = 1;
+        for (int64_t i = d - 1; i >= 1; --i) {
+            const int64_t m_s = dims[i] * r_s;
+            const int64_t nsig_s = std::min(m_s, rows_s);
+            need += (size_t)nsig_s + 2;
+            r_s = predicted_rank_h(nsig_s, nsig_s, r_max);
+            rows_s /= dims[i - 1];
+        }
+        TT_TRY(ensure_host(ctx->host_sig, need * 8));
+        TT_TRY(ensure(ctx->ws_rank, (size_t)d * 2 * 8));
+    }
     int64_t r = 1;
     int which = 0;
     Timer tm(ctx);
@@ -1187,14 +1266,27 @@ int run_chain(ttsvd_cu_ctx* ctx, WorkView cur, const std::vector<int64_t>& dims,
         }
         tm.mark(2);
         sig.resize(nsig);
-        TT_TRY(d2h(ctx, sig.data(), d_sigma, nsig));
-        if (i == d - 1 && first_sigma_norm_out) *first_sigma_norm_out = sigma_norm_h(sig.data(), nsig);
-        if (delta < 0.0) {
-            if (d_for_delta < 2) return fail(TTSVD_ERR_DEGENERATE, "derive_delta: requires d >= 2");
-            delta = eps / std::sqrt((double)(d_for_delta - 1)) * sigma_norm_h(sig.data(), nsig);
-            if (delta_io) *delta_io = delta;
+        int64_t rnew;
+        if (spec) {
+            double* rec = as<double>(ctx->ws_rank) + 2 * (size_t)spec_steps.size();
+            rank_epilogue_kernel<<<1, 32, 0, ctx->stream>>>(d_sigma, nsig, cur.cols, nsig, delta, r_max, cur.rows, rec);
+            TT_TRY(check_launch(ctx, "rank_epilogue_kernel"));
+            double* hs = as<double>(ctx->host_sig) + spec_off;
+            TT_CUDA(cudaMemcpyAsync(hs, d_sigma, (size_t)nsig * 8, cudaMemcpyDeviceToHost, ctx->stream));
+            TT_CUDA(cudaMemcpyAsync(hs + nsig, rec, 16, cudaMemcpyDeviceToHost, ctx->stream));
+            rnew = predicted_rank_h(nsig, nsig, r_max);
+            spec_steps.push_back(SpecStep{spec_off, nsig, rnew});
+            spec_off += (size_t)nsig + 2;
+        } else {
+            TT_TRY(d2h(ctx, sig.data(), d_sigma, nsig));
+            if (i == d - 1 && first_sigma_norm_out) *first_sigma_norm_out = sigma_norm_h(sig.data(), nsig);
+            if (delta < 0.0) {
+                if (d_for_delta < 2) return fail(TTSVD_ERR_DEGENERATE, "derive_delta: requires d >= 2");
+                delta = eps / std::sqrt((double)(d_for_delta - 1)) * sigma_norm_h(sig.data(), nsig);
+                if (delta_io) *delta_io = delta;
+            }
+            rnew = choose_rank_h(sig.data(), nsig, cur.cols, nsig, delta, r_max, cur.rows);
         }
-        const int64_t rnew = choose_rank_h(sig.data(), nsig, cur.cols, nsig, delta, r_max, cur.rows);
         st.nsig = nsig;
         st.rank = rnew;
         tm.mark(7);
@@ -1258,12 +1350,41 @@ int run_chain(ttsvd_cu_ctx* ctx, WorkView cur, const std::vector<int64_t>& dims,
         }
     }
     TT_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (spec) {
+        // the device's ranks against the predictions the chain ran with
+        const double* base = as<double>(ctx->host_sig);
+        for (size_t k = 0; k < spec_steps.size(); ++k) {
+            const SpecStep& ss = spec_steps[k];
+            const double* hs = base + ss.off;
+            if ((int64_t)hs[ss.nsig] != ss.pred) {
+                pending.clear();
+                return kMispredict;
+            }
+            out->sigmas[k].assign(hs, hs + ss.nsig);
+            if (k == 0 && first_sigma_norm_out) *first_sigma_norm_out = std::sqrt(hs[ss.nsig + 1]);
+        }
+        if (delta_io) *delta_io = delta;
+    }
     flush_cores();
     out->cores[0] = std::move(first);
     out->ranks[0] = 1;
     out->ranks[1] = r;
     out->ranks[d] = 1;
     return TTSVD_OK;
+}
+
+int run_chain(ttsvd_cu_ctx* ctx, WorkView cur, const std::vector<int64_t>& dims, int64_t r_max, double eps,
+              int64_t d_for_delta, ttsvd_cu_tt* out, double* delta_io = nullptr,
+              double* first_sigma_norm_out = nullptr) {
+    const double delta_in = delta_io ? *delta_io : -1.0;
+    // timing reads its events step by step, so a timed chain runs step by step
+    const bool spec = !ctx->timing && (delta_in < 0.0 ? eps == 0.0 : delta_in == 0.0);
+    if (spec) {
+        const int rc = run_chain_impl(ctx, cur, dims, r_max, eps, d_for_delta, out, delta_io, first_sigma_norm_out, true);
+        if (rc != kMispredict) return rc;
+        if (delta_io) *delta_io = delta_in;
+    }
+    return run_chain_impl(ctx, cur, dims, r_max, eps, d_for_delta, out, delta_io, first_sigma_norm_out, false);
 }
 
 // tsmm.hpp:84-126 transpose_reorder: Y (out_rows x out_cols, ld ldy) <- the
@@ -1484,6 +1605,7 @@ int ttsvd_cu_ctx_destroy(ttsvd_cu_ctx* ctx) {
         if (b.p) cudaFree(b.p);
     if (ctx->host_stage.p) cudaFreeHost(ctx->host_stage.p);
     if (ctx->host_cores.p) cudaFreeHost(ctx->host_cores.p);
+    if (ctx->host_sig.p) cudaFreeHost(ctx->host_sig.p);
     if (ctx->comm && nccl().ok) nccl().comm_destroy(ctx->comm);
     for (auto& e : ctx->ev)
         if (e) cudaEventDestroy(e);

@@ -145,6 +145,36 @@ def test_determinism_c10(tt):
         assert np.array_equal(ca.data, cb.data)
 
 
+def test_speculative_chain_matches_stepwise(tt, orc):
+    # eps = 0: the chain runs on predicted ranks with the rank rule on the
+    # device (K6, choose_rank: small_svd.hpp:49-63, tt_svd.hpp:111-118) and one
+    # synchronisation at its end; a timed context runs step by step with the
+    # host rule.  Same bytes either way — also when a prediction fails (exact
+    # low rank below r_max) and the chain is run again.
+    from oracle.oracle import random_tensor, random_tt, tt_reconstruct
+    import torch
+    ctx = tt.context()
+    for X, dims, r_max in ((random_tensor(77, [4] * 8), [4] * 8, 16),
+                           (tt_reconstruct(random_tt([4] * 6, [1, 2, 3, 3, 2, 1, 1], 53), [4] * 6), [4] * 6, 3),
+                           (tt_reconstruct(random_tt([3] * 7, [1, 2, 2, 2, 2, 2, 2, 1], 5), [3] * 7), [3] * 7, 9)):
+        Xd = torch.from_numpy(np.ascontiguousarray(X.T)).cuda().t()
+        rows = int(np.prod(dims)) // dims[-1]
+        a = tt.tt_svd_tsqr(Xd[:rows], dims, tt.TruncationSpec(r_max=r_max))
+        ctx.set_timing(True)
+        try:
+            b = tt.tt_svd_tsqr(Xd[:rows], dims, tt.TruncationSpec(r_max=r_max))
+        finally:
+            ctx.set_timing(False)
+        assert a.ranks() == b.ranks()
+        r, cores, steps, sig = orc.tt_svd_tsqr(X, dims, X.shape[0], r_max, 0.0, with_sigma=True)
+        assert a.ranks() == r
+        for ca, cb in zip(a.cores, b.cores):
+            assert np.array_equal(ca.data, cb.data)
+        for sa, sb in zip(a.sigmas, b.sigmas):
+            assert np.array_equal(sa, sb)
+        assert [s.rank for s in a.steps] == [s.rank for s in b.steps]
+
+
 def test_host_entry_matches_device_entry(tt, orc):
     # the reference-facing host-buffer path (H2D inside the call) == device path
     dims = [4] * 8
