@@ -1024,7 +1024,15 @@ int tsmm_device(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t ld
         }
         return TTSVD_OK;
     }
-    if (k > 1 && k <= 16 && m <= 32 && n >= (int64_t)1 << 18) {
+    if (n <= (int64_t)1 << 14 && m >= 32 && (size_t)(m + 256) * 8 * 8 <= (size_t)kSmemLimit) {
+        // short X (the last steps of a chain): 32 rows x 8 output columns per
+        // CTA, the contraction split over its warps
+        const size_t smem = (size_t)(m + 256) * 8 * 8;
+        TT_TRY(kattr(ctx, (const void*)tsmm_small_kernel<8>, kSmemLimit));
+        dim3 grid((unsigned)((n + 31) / 32), (unsigned)((k + 7) / 8));
+        tsmm_small_kernel<8><<<grid, 256, smem, ctx->stream>>>(X, n, m, ldx, V, ldv, k, Y, out_rows, ldy);
+        rc = check_launch(ctx, "tsmm_small_kernel");
+    } else if (k > 1 && k <= 16 && m <= 32 && n >= (int64_t)1 << 18) {
         // narrow X: rows staged by cp.async (tsmm_async_kernel; measured
         // against TMA bulk staging, tools/tsmm_bulk_experiment.cuh)
         rc = k <= 4 ? launch_tsmm_async<4>(ctx, X, n, m, ldx, V, ldv, k, Y, out_rows, ldy)

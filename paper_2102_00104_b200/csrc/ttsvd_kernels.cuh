@@ -605,6 +605,57 @@ __global__ void __launch_bounds__(256) tsmm_kernel(const double* __restrict__ X,
     }
 }
 
+// K_TSMM for short X (n <= 2^14 rows: the last steps of a chain, where the
+// row-per-thread kernel leaves one to sixteen CTAs walking all m columns with
+// four loads in flight each).  CTA (b, y) owns 32 rows and KC output columns;
+// its eight warps split the contraction index (warp w: columns
+// [w jw, (w+1) jw) of X, lane = row), the eight partial sums meet in shared
+// memory and are added in warp order.  Output placement as tsmm_kernel.
+template <int KC>
+__global__ void __launch_bounds__(256) tsmm_small_kernel(const double* __restrict__ X, int64_t n, int m, int64_t ldx,
+                                                         const double* __restrict__ V, int64_t ldv, int k,
+                                                         double* __restrict__ Y, int64_t out_rows, int64_t ldy) {
+    static_assert(KC <= 8, "one finishing thread per (column, row)");
+    extern __shared__ __align__(16) double Vs[];
+    double* red = Vs + m * KC;  // 8 x KC x 32
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int c0 = blockIdx.y * KC;
+    const int kc = min(KC, k - c0);
+    for (int e = tid; e < m * KC; e += 256) {
+        const int j = e / KC, c = e % KC;
+        Vs[e] = (c < kc) ? V[(int64_t)(c0 + c) * ldv + j] : 0.0;
+    }
+    __syncthreads();
+    const int64_t i = (int64_t)blockIdx.x * 32 + lane;
+    const int jw = (m + 7) / 8;
+    const int j0 = warp * jw, j1 = min(m, j0 + jw);
+    double acc[KC];
+#pragma unroll
+    for (int c = 0; c < KC; ++c) acc[c] = 0.0;
+    if (i < n) {
+        const double* xi = X + i;
+#pragma unroll 8
+        for (int j = j0; j < j1; ++j) {
+            const double x = __ldg(xi + (int64_t)j * ldx);
+            const double* vj = Vs + j * KC;
+#pragma unroll
+            for (int c = 0; c < KC; ++c) acc[c] = fma(vj[c], x, acc[c]);
+        }
+    }
+#pragma unroll
+    for (int c = 0; c < KC; ++c) red[(warp * KC + c) * 32 + lane] = acc[c];
+    __syncthreads();
+    const int c = warp;  // finishing thread: column c0 + warp, row `lane`
+    if (c < kc && i < n) {
+        double t = red[c * 32 + lane];
+#pragma unroll
+        for (int w = 1; w < 8; ++w) t += red[(w * KC + c) * 32 + lane];
+        const int64_t p = i + n * (int64_t)(c0 + c);
+        const int64_t col = p / out_rows;
+        Y[col * ldy + (p - col * out_rows)] = t;
+    }
+}
+
 // K_TSMM for narrow X (m <= 32) and few output columns: the streamed rows are
 // staged in shared memory by cp.async (each thread copies its own row's m
 // values, 8 bytes apiece, one chunk of 256 rows ahead), so the bytes in

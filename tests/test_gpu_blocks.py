@@ -449,7 +449,11 @@ def test_tsmm_frobenius_and_padding(tt):
 
 
 @pytest.mark.parametrize("n,m,k,nn", [(1 << 20, 16, 16, 16), (1 << 16, 256, 32, 16), (4096, 512, 32, 16),
-                                      (30000, 50, 40, 10), (1000, 3, 2, 1)])
+                                      (30000, 50, 40, 10), (1000, 3, 2, 1),
+                                      # short X (tsmm_small_kernel): partial row blocks and column chunks,
+                                      # m not a multiple of the warp split, a non-dividing reshape
+                                      (256, 512, 32, 16), (16, 512, 16, 16), (16384, 64, 16, 4), (1000, 77, 13, 10),
+                                      (33, 40, 9, 3), (4097, 100, 5, 17)])
 def test_tsmm_shapes_vs_oracle(tt, orc, n, m, k, nn):
     from oracle.oracle import gaussian, orthonormal
     x = gaussian(n, m, n + m)
