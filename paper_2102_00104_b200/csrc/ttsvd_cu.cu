@@ -33,6 +33,7 @@
 #include "tsqr_ws.cuh"
 #include "tsqr_pt.cuh"
 #include "tsqr_gt.cuh"
+#include "tsmm_dt.cuh"
 #include "tsqr_sq.cuh"
 
 using namespace ttsvd_b200;
@@ -1011,10 +1012,24 @@ int tsmm_device(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t ld
     int rc;
     // measured (tools/config3_sweep.py): the tensor-core path wins only once the
     // FFMA kernel turns compute-bound (k > 16 output columns, m >= 32)
-    const bool dmma = k > 16 && m >= 32 && n >= (int64_t)1 << 18 &&
+    const bool dmma = k > 16 && m >= 32 && n >= (int64_t)1 << 16 &&
                       (size_t)((m + 3) & ~3) * tsmm_vld(4) * 8 <= 200 * 1024;
     if (dmma) {
-        rc = launch_tsmm_dmma<4>(ctx, X, n, m, ldx, V, ldv, k, Y, out_rows, ldy);
+        const int dt_stages = dt_smem_bytes(m, 4) <= (size_t)kSmemLimit - 2048 ? 4 : 2;
+        if (n % kDtRows == 0 && m % kDtCols == 0 && (ldx & 1) == 0 && ((uintptr_t)X & 15) == 0 &&
+            dt_smem_bytes(m, dt_stages) <= (size_t)kSmemLimit - 2048) {
+            // rows staged by TMA bulk copies (tsmm_dt.cuh), one persistent CTA per SM
+            const void* fn = dt_stages == 4 ? (const void*)tsmm_dt_kernel<4> : (const void*)tsmm_dt_kernel<2>;
+            TT_TRY(kattr(ctx, fn, kSmemLimit - 2048));
+            dim3 grid((unsigned)std::min<int64_t>(ctx->num_sms, (n / kDtRows + 7) / 8), (unsigned)((k + 31) / 32));
+            if (dt_stages == 4)
+                tsmm_dt_kernel<4><<<grid, 256, dt_smem_bytes(m, 4), ctx->stream>>>(X, n, m, ldx, V, ldv, k, Y, out_rows, ldy);
+            else
+                tsmm_dt_kernel<2><<<grid, 256, dt_smem_bytes(m, 2), ctx->stream>>>(X, n, m, ldx, V, ldv, k, Y, out_rows, ldy);
+            rc = check_launch(ctx, "tsmm_dt_kernel");
+        } else {
+            rc = launch_tsmm_dmma<4>(ctx, X, n, m, ldx, V, ldv, k, Y, out_rows, ldy);
+        }
         if (rc != TTSVD_OK) return rc;
         if (ldy > out_rows) {
             const int64_t pad = (ldy - out_rows) * out_cols;

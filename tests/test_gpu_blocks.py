@@ -427,6 +427,18 @@ def test_tsmm_column_selection_is_exact(tt):
     assert np.array_equal(y.reshape(-1, order="F"), flat)
 
 
+def test_tsmm_dt_non_dividing_reshape(tt, orc):
+    # tsmm_dt_kernel with out_rows that does not divide n (per-element placement)
+    from oracle.oracle import gaussian
+    n, m, k = 1 << 16, 48, 24
+    x = gaussian(n, m, 5)
+    v = np.linalg.qr(gaussian(m, k, 6))[0]
+    out_rows, out_cols = 3 << 14, 32
+    y = host(tt.tsmm_reshape(x, v, out_rows, out_cols))
+    yo = orc.tsmm_reshape(x, v, out_rows, out_cols)[:out_rows]
+    assert np.max(np.abs(y - yo)) <= 1e-13 * np.linalg.norm(yo)
+
+
 def test_tsmm_guards(tt):
     with pytest.raises(tt.ShapeError):
         tt.tsmm_reshape(np.zeros((10, 4)), np.zeros((4, 2)), 7, 3)
@@ -453,7 +465,11 @@ def test_tsmm_frobenius_and_padding(tt):
                                       # short X (tsmm_small_kernel): partial row blocks and column chunks,
                                       # m not a multiple of the warp split, a non-dividing reshape
                                       (256, 512, 32, 16), (16, 512, 16, 16), (16384, 64, 16, 4), (1000, 77, 13, 10),
-                                      (33, 40, 9, 3), (4097, 100, 5, 17)])
+                                      (33, 40, 9, 3), (4097, 100, 5, 17),
+                                      # TMA-staged DMMA kernel (tsmm_dt_kernel): n % 64 == 0, m % 8 == 0, k > 16,
+                                      # two column chunks, two stages (m > 256)
+                                      (1 << 18, 64, 24, 4), (1 << 16, 40, 32, 2), (262208, 96, 20, 16),
+                                      (1 << 16, 264, 40, 8), (1 << 16, 512, 32, 16)])
 def test_tsmm_shapes_vs_oracle(tt, orc, n, m, k, nn):
     from oracle.oracle import gaussian, orthonormal
     x = gaussian(n, m, n + m)
