@@ -27,23 +27,25 @@ constexpr int kDtMt = 8;                 // 8-row tiles per warp block
 constexpr int kDtRows = 8 * kDtMt;       // rows per warp block
 constexpr int kDtCols = 8;               // columns of X per stage
 constexpr int kDtCs = kDtRows + 4;       // column stride of a stage (doubles)
-constexpr int kDtVld = 36;               // smem ld of the V chunk (32 output columns + 4)
 
-inline size_t dt_smem_bytes(int m, int stages) {
-    return ((size_t)m * kDtVld + (size_t)8 * stages * kDtCols * kDtCs) * sizeof(double);
+// NT: 8-column tiles of the output chunk a CTA computes (4: k > 16; 2: k <= 16)
+inline size_t dt_smem_bytes(int m, int stages, int nt = 4) {
+    return ((size_t)m * (8 * nt + 4) + (size_t)8 * stages * kDtCols * kDtCs) * sizeof(double);
 }
 
-template <int kDtStages>
+template <int kDtStages, int NT = 4>
 __global__ void __launch_bounds__(256, 1) tsmm_dt_kernel(const double* __restrict__ X, int64_t n, int m, int64_t ldx,
                                                          const double* __restrict__ V, int64_t ldv, int k,
                                                          double* __restrict__ Y, int64_t out_rows, int64_t ldy) {
     extern __shared__ __align__(128) double dsm[];
     __shared__ __align__(8) unsigned long long mbar[8][kDtStages];
-    double* Vs = dsm;  // m x kDtVld
+    constexpr int kDtVld = 8 * NT + 4;  // smem ld of the V chunk
+    constexpr int KCH = 8 * NT;         // output columns per chunk
+    double* Vs = dsm;                   // m x kDtVld
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     double* xb = dsm + (size_t)m * kDtVld + (size_t)warp * kDtStages * kDtCols * kDtCs;
-    const int c0 = blockIdx.y * 32;
-    const int kc = min(32, k - c0);
+    const int c0 = blockIdx.y * KCH;
+    const int kc = min(KCH, k - c0);
     for (int e = tid; e < m * kDtVld; e += 256) {
         const int j = e / kDtVld, c = e % kDtVld;
         Vs[e] = (c < kc) ? V[(int64_t)(c0 + c) * ldv + j] : 0.0;
@@ -78,11 +80,11 @@ __global__ void __launch_bounds__(256, 1) tsmm_dt_kernel(const double* __restric
     int64_t idx = 0;
     for (int64_t t = 0; t < my_blocks; ++t) {
         const int64_t rb = (wg + t * W) * kDtRows;
-        double acc[kDtMt][4][2];
+        double acc[kDtMt][NT][2];
 #pragma unroll
         for (int mt = 0; mt < kDtMt; ++mt)
 #pragma unroll
-            for (int nt = 0; nt < 4; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
+            for (int nt = 0; nt < NT; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
         for (int g = 0; g < spb; ++g, ++idx) {
             gt_mbar_wait(bar(s), phase);
             const double* xs = xb + (size_t)s * kDtCols * kDtCs + r;
@@ -90,15 +92,15 @@ __global__ void __launch_bounds__(256, 1) tsmm_dt_kernel(const double* __restric
 #pragma unroll
             for (int kk = 0; kk < kDtCols / 4; ++kk) {
                 const int col = 4 * kk + q;
-                double a[kDtMt], b[4];
+                double a[kDtMt], b[NT];
 #pragma unroll
                 for (int mt = 0; mt < kDtMt; ++mt) a[mt] = xs[col * kDtCs + 8 * mt];
 #pragma unroll
-                for (int nt = 0; nt < 4; ++nt) b[nt] = vs[col * kDtVld + 8 * nt];
+                for (int nt = 0; nt < NT; ++nt) b[nt] = vs[col * kDtVld + 8 * nt];
 #pragma unroll
                 for (int mt = 0; mt < kDtMt; ++mt)
 #pragma unroll
-                    for (int nt = 0; nt < 4; ++nt) dmma884(acc[mt][nt], a[mt], b[nt]);
+                    for (int nt = 0; nt < NT; ++nt) dmma884(acc[mt][nt], a[mt], b[nt]);
             }
             __syncwarp();  // the stage has been read: refill it
             if (idx + kDtStages < total) issue(idx + kDtStages, s);
@@ -121,7 +123,7 @@ __global__ void __launch_bounds__(256, 1) tsmm_dt_kernel(const double* __restric
                 double* yb = Y + (b + n_next * c0) * ldy + ii;
                 const int64_t cstep = n_next * ldy;
 #pragma unroll
-                for (int nt = 0; nt < 4; ++nt)
+                for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
                     for (int e = 0; e < 2; ++e) {
                         const int c = 8 * nt + 2 * q + e;
@@ -133,7 +135,7 @@ __global__ void __launch_bounds__(256, 1) tsmm_dt_kernel(const double* __restric
             for (int mt = 0; mt < kDtMt; ++mt) {
                 const int64_t i = rb + 8 * mt + r;
 #pragma unroll
-                for (int nt = 0; nt < 4; ++nt)
+                for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
                     for (int e = 0; e < 2; ++e) {
                         const int c = 8 * nt + 2 * q + e;

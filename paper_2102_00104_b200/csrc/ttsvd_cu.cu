@@ -1010,22 +1010,26 @@ int launch_tsmm_dmma(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64
 int tsmm_device(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t ldx, const double* V, int64_t ldv, int k,
                 double* Y, int64_t out_rows, int64_t out_cols, int64_t ldy) {
     int rc;
-    // measured (tools/config3_sweep.py): the tensor-core path wins only once the
-    // FFMA kernel turns compute-bound (k > 16 output columns, m >= 32)
-    const bool dmma = k > 16 && m >= 32 && n >= (int64_t)1 << 16 &&
+    // FP64 tensor cores once the FMA kernels turn compute-bound (k > 8 output
+    // columns, m >= 32): rows staged by TMA bulk copies (tsmm_dt.cuh), one
+    // persistent CTA per SM; fragments straight from X (tsmm_dmma_kernel) when
+    // the staged kernel's alignment / divisibility conditions do not hold
+    const int dt_nt = k > 16 ? 4 : 2;
+    const int dt_stages = dt_smem_bytes(m, 4, dt_nt) <= (size_t)kSmemLimit - 2048 ? 4 : 2;
+    const bool dt = k > 8 && m >= 32 && n >= (int64_t)1 << 16 && n % kDtRows == 0 && m % kDtCols == 0 &&
+                    (ldx & 1) == 0 && ((uintptr_t)X & 15) == 0 &&
+                    dt_smem_bytes(m, dt_stages, dt_nt) <= (size_t)kSmemLimit - 2048;
+    const bool dmma = !dt && k > 16 && m >= 32 && n >= (int64_t)1 << 18 &&
                       (size_t)((m + 3) & ~3) * tsmm_vld(4) * 8 <= 200 * 1024;
-    if (dmma) {
-        const int dt_stages = dt_smem_bytes(m, 4) <= (size_t)kSmemLimit - 2048 ? 4 : 2;
-        if (n % kDtRows == 0 && m % kDtCols == 0 && (ldx & 1) == 0 && ((uintptr_t)X & 15) == 0 &&
-            dt_smem_bytes(m, dt_stages) <= (size_t)kSmemLimit - 2048) {
-            // rows staged by TMA bulk copies (tsmm_dt.cuh), one persistent CTA per SM
-            const void* fn = dt_stages == 4 ? (const void*)tsmm_dt_kernel<4> : (const void*)tsmm_dt_kernel<2>;
-            TT_TRY(kattr(ctx, fn, kSmemLimit - 2048));
-            dim3 grid((unsigned)std::min<int64_t>(ctx->num_sms, (n / kDtRows + 7) / 8), (unsigned)((k + 31) / 32));
-            if (dt_stages == 4)
-                tsmm_dt_kernel<4><<<grid, 256, dt_smem_bytes(m, 4), ctx->stream>>>(X, n, m, ldx, V, ldv, k, Y, out_rows, ldy);
-            else
-                tsmm_dt_kernel<2><<<grid, 256, dt_smem_bytes(m, 2), ctx->stream>>>(X, n, m, ldx, V, ldv, k, Y, out_rows, ldy);
+    if (dt || dmma) {
+        if (dt) {
+            void (*fn)(const double*, int64_t, int, int64_t, const double*, int64_t, int, double*, int64_t, int64_t) =
+                dt_nt == 4 ? (dt_stages == 4 ? tsmm_dt_kernel<4, 4> : tsmm_dt_kernel<2, 4>)
+                           : (dt_stages == 4 ? tsmm_dt_kernel<4, 2> : tsmm_dt_kernel<2, 2>);
+            TT_TRY(kattr(ctx, (const void*)fn, kSmemLimit - 2048));
+            dim3 grid((unsigned)std::min<int64_t>(ctx->num_sms, (n / kDtRows + 7) / 8),
+                      (unsigned)((k + 8 * dt_nt - 1) / (8 * dt_nt)));
+            fn<<<grid, 256, dt_smem_bytes(m, dt_stages, dt_nt), ctx->stream>>>(X, n, m, ldx, V, ldv, k, Y, out_rows, ldy);
             rc = check_launch(ctx, "tsmm_dt_kernel");
         } else {
             rc = launch_tsmm_dmma<4>(ctx, X, n, m, ldx, V, ldv, k, Y, out_rows, ldy);
