@@ -162,112 +162,178 @@ __global__ void __launch_bounds__(NT, 1) gqr_kernel(GqrArgs a) {
         __syncthreads();
         // ---- 32 reflectors, one grid barrier each ----
         GQR_PROF(0);
-        for (int jj = 0; jj < 32; ++jj) {
-            const int64_t j = c0 + jj;
-            const int buf = jj & 1;
-            long long tr0 = pf ? gqr_clock() : 0;
-            // partials over my rows below the pivot: value 0 = sum x_j^2, value
-            // k = sum x_j x_k (k > jj).  Warp w takes columns CPW w .. + CPW - 1,
-            // its lanes stride the rows (both loads contiguous across lanes),
-            // then a butterfly per column: CPW x 5 shuffles per warp instead
-            // of a 31-shuffle reduce-scatter of every row's 32 products (the SM
-            // issues one 32-bit shuffle per cycle)
-            {
-                constexpr int NW = NT / 32, CPW = 32 / NW;
-                const int i_lo = (int)(j - r0 + 1 > 0 ? (j - r0 + 1 < rows ? j - r0 + 1 : rows) : 0);
-                if (tid < 32 && j >= r0 && j < r0 + rows && tid >= jj)  // pivot row -> broadcast slot
-                    a.piv[buf * 32 + tid] = Ys[tid * ldy + (int)(j - r0)];
-                const double* yj = Ys + jj * ldy;
-                double sk[CPW];
+        // The CTA's rows of the panel live in registers for the 32 reflectors
+        // (warp w: rows 32 w .. 32 w + 31 as 4-row x 8-column tiles, lane
+        // rq + 8 cg: rows 32 w + rq + 8 r, columns 8 cg + c — the layout of
+        // tsqr_t128's panel): the pivot column reaches the other column groups
+        // by 4 shuffles, a 7-shuffle transpose-reduce leaves column `lane`'s
+        // warp dot in lane `lane`, and the rank-1 update is 32 register FMAs
+        // per lane.  (With the panel in shared memory the update was two
+        // shared-memory accesses per FMA: ~3 k of the ~10.5 k cycles per
+        // reflector, and the dots another 1.4 k.)  Rows above the pivot are
+        // zero in the registers (their panel entries stay in Ys); a pivot row
+        // is written to Ys and zeroed as soon as its reflector has been applied.
+        constexpr int NW = NT / 32;
+        const int rq = lane & 7, cg = lane >> 3;
+        double* dpart = Wsc;  // 2 x NW x 32 warp partials (Wsc is free until the blocked update)
+        double x[4][8];
 #pragma unroll
-                for (int q = 0; q < CPW; ++q) sk[q] = 0.0;
-                if (CPW * warp + CPW - 1 >= jj) {
-                    for (int i = i_lo + lane; i < rows; i += 32) {
-                        const double xj = yj[i];
+        for (int r = 0; r < 4; ++r) {
+            const int i = 32 * warp + rq + 8 * r;
+            const bool live = i < rows && r0 + i >= c0;
 #pragma unroll
-                        for (int q = 0; q < CPW; ++q) sk[q] = fma(xj, Ys[(CPW * warp + q) * ldy + i], sk[q]);
-                    }
-#pragma unroll
-                    for (int q = 0; q < CPW; ++q) sk[q] = gqr_warp_sum(sk[q]);
-                }
-                if (lane == 0)
-#pragma unroll
-                    for (int q = 0; q < CPW; ++q) red[CPW * warp + q] = sk[q];
-                __syncthreads();
-                if (tid < 32) part[((int64_t)buf * G + c) * 33 + tid] = tid == 0 ? red[jj] : (tid > jj ? red[tid] : 0.0);
-            }
-            long long tq0 = pf ? gqr_clock() : 0;
-            if (pf) a.prof[6] += tq0 - tr0;
-            // grid.sync orders the partials: its barrier is preceded by a
-            // device-scope fence on behalf of the whole CTA
-            gsync();
-            // totals in a fixed order (identical on every CTA): value k = tid & 31,
-            // slice s = tid >> 5 sums CTAs q = s, s + 8, ...; then the 8 slices
-            {
-                const int k = tid & 31, sl = tid >> 5;
-                const double pv = (sl == 0) ? __ldcg(&a.piv[buf * 32 + k]) : 0.0;  // in flight with the sums
-                red[(NT / 32) * 33 + sl * 33 + k] = gqr_sum_inflight<20>(part + (int64_t)buf * G * 33 + k, 33, G, sl, NT / 32);
-                if (sl == 0) red[33 + k] = pv;
-            }
-            __syncthreads();
-            // warp 0: the totals, the reflector (every CTA derives the same
-            // bits) and gamma_k = tau (A(j,k) + scale d_k) for the columns
-            // k > jj, once per CTA instead of once per thread
-            if (tid < 32) {
-                double t = 0.0;
-#pragma unroll
-                for (int sl = 0; sl < NT / 32; ++sl) t += red[(NT / 32) * 33 + sl * 33 + tid];
-                const double pk = red[33 + tid];
-                const double sp = __shfl_sync(0xffffffffu, t, 0);
-                const double u0 = __shfl_sync(0xffffffffu, pk, jj);
-                const double nrm2 = u0 * u0 + sp;
-                const double inv = fast_rsqrt(nrm2);
-                const double nr = nrm2 * inv;
-                const double au = fabs(u0);
-                const double sg = (u0 > 0.0) ? 1.0 : -1.0;
-                double alpha = -sg * nr, tj = 1.0 + au * inv, scale = sg * fast_rcp(au + nr);
-                if (sp == 0.0 && u0 != 0.0) {
-                    alpha = u0;
-                    tj = 0.0;
-                    scale = 0.0;
-                }
-                if (nrm2 == 0.0) {
-                    alpha = sqrt(2.0 * DBL_MIN);
-                    tj = 2.0;
-                    scale = 0.0;
-                }
-                gsm[tid] = (tid > jj) ? tj * (pk + scale * t) : 0.0;
-                if (tid == 0) {
-                    gsm[32] = scale;
-                    gsm[33] = alpha;
-                    tau[jj] = tj;
-                }
-            }
-            __syncthreads();
-            if (pf) {
-                const long long tq1 = gqr_clock();
-                a.prof[7] += tq1 - tq0;
-            }
-            const double scale = gsm[32], alpha = gsm[33];
-            for (int i = tid; i < rows; i += NT) {
-                const int64_t gi = r0 + i;
-                if (gi < j) continue;
-                if (gi == j) {
-#pragma unroll
-                    for (int k = 0; k < 32; ++k)
-                        if (k > jj) Ys[k * ldy + i] -= gsm[k];
-                    Ys[jj * ldy + i] = alpha;
-                    continue;
-                }
-                const double xj = Ys[jj * ldy + i];
-                const double f = xj * scale;
-#pragma unroll
-                for (int k = 0; k < 32; ++k)
-                    if (k > jj) Ys[k * ldy + i] = fma(-gsm[k], f, Ys[k * ldy + i]);
-                Ys[jj * ldy + i] = f;  // v
-            }
-            __syncthreads();
+            for (int cc = 0; cc < 8; ++cc) x[r][cc] = live ? Ys[(8 * cg + cc) * ldy + i] : 0.0;
         }
+#pragma unroll 1
+        for (int cgj = 0; cgj < 4; ++cgj) {
+#pragma unroll
+            for (int cj = 0; cj < 8; ++cj) {
+                const int jj = 8 * cgj + cj;
+                const int64_t j = c0 + jj;
+                const int buf = jj & 1;
+                long long tr0 = pf ? gqr_clock() : 0;
+                const int li = (int)(j - r0);  // the pivot's row among mine (if 0 <= li < rows)
+                const bool mine = li >= 0 && li < rows && (li >> 5) == warp && (li & 7) == rq;  // my rows hold it
+                const int rp = (li >> 3) & 3;
+                double pr[4];
+#pragma unroll
+                for (int r = 0; r < 4; ++r) pr[r] = __shfl_sync(0xffffffffu, x[r][cj], rq + 8 * cgj);
+                if (mine) {  // pivot row -> broadcast slot
+#pragma unroll
+                    for (int cc = 0; cc < 8; ++cc) {
+                        const double v = rp == 0 ? x[0][cc] : (rp == 1 ? x[1][cc] : (rp == 2 ? x[2][cc] : x[3][cc]));
+                        a.piv[buf * 32 + 8 * cg + cc] = v;
+                    }
+                }
+                // dots over the rows below the pivot: value 0 = sum x_j^2, value k = sum x_j x_k
+                double acc[8];
+#pragma unroll
+                for (int r = 0; r < 4; ++r) pr[r] = (mine && r == rp) ? 0.0 : pr[r];  // the pivot row stays out
+#pragma unroll
+                for (int cc = 0; cc < 8; ++cc) {
+                    acc[cc] = pr[0] * x[0][cc];
+#pragma unroll
+                    for (int r = 1; r < 4; ++r) acc[cc] = fma(pr[r], x[r][cc], acc[cc]);
+                }
+                // transpose-reduce over the row lanes: lane ends with column 8 cg + rq = lane
+#pragma unroll
+                for (int o = 4; o >= 1; o >>= 1) {
+                    const bool up = (lane & o) != 0;
+#pragma unroll
+                    for (int t = 0; t < o; ++t) {
+                        const double send = up ? acc[t] : acc[t + o];
+                        const double keep = up ? acc[t + o] : acc[t];
+                        acc[t] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+                    }
+                }
+                dpart[(buf * NW + warp) * 32 + lane] = acc[0];
+                __syncthreads();
+                if (tid < 32) {
+                    double t = 0.0;
+#pragma unroll
+                    for (int w = 0; w < NW; ++w) t += dpart[(buf * NW + w) * 32 + tid];
+                    const double tj = __shfl_sync(0xffffffffu, t, jj);
+                    part[((int64_t)buf * G + c) * 33 + tid] = tid == 0 ? tj : (tid > jj ? t : 0.0);
+                }
+                long long tq0 = pf ? gqr_clock() : 0;
+                if (pf) a.prof[6] += tq0 - tr0;
+                // grid.sync orders the partials: its barrier is preceded by a
+                // device-scope fence on behalf of the whole CTA
+                gsync();
+                // totals in a fixed order (identical on every CTA): value k = tid & 31,
+                // slice s = tid >> 5 sums CTAs q = s, s + 8, ...; then the 8 slices
+                {
+                    const int k = tid & 31, sl = tid >> 5;
+                    const double pv = (sl == 0) ? __ldcg(&a.piv[buf * 32 + k]) : 0.0;  // in flight with the sums
+                    // (columns 1 .. jj carry no value: no loads for them)
+                    red[(NT / 32) * 33 + sl * 33 + k] =
+                        (k == 0 || k > jj) ? gqr_sum_inflight<20>(part + (int64_t)buf * G * 33 + k, 33, G, sl, NT / 32)
+                                           : 0.0;
+                    if (sl == 0) red[33 + k] = pv;
+                }
+                __syncthreads();
+                // warp 0: the totals, the reflector (every CTA derives the same
+                // bits) and gamma_k = tau (A(j,k) + scale d_k) for the columns
+                // k > jj, once per CTA instead of once per thread
+                if (tid < 32) {
+                    double t = 0.0;
+#pragma unroll
+                    for (int sl = 0; sl < NT / 32; ++sl) t += red[(NT / 32) * 33 + sl * 33 + tid];
+                    const double pk = red[33 + tid];
+                    const double sp = __shfl_sync(0xffffffffu, t, 0);
+                    const double u0 = __shfl_sync(0xffffffffu, pk, jj);
+                    const double nrm2 = u0 * u0 + sp;
+                    const double inv = fast_rsqrt(nrm2);
+                    const double nr = nrm2 * inv;
+                    const double au = fabs(u0);
+                    const double sg = (u0 > 0.0) ? 1.0 : -1.0;
+                    double alpha = -sg * nr, tj = 1.0 + au * inv, scale = sg * fast_rcp(au + nr);
+                    if (sp == 0.0 && u0 != 0.0) {
+                        alpha = u0;
+                        tj = 0.0;
+                        scale = 0.0;
+                    }
+                    if (nrm2 == 0.0) {
+                        alpha = sqrt(2.0 * DBL_MIN);
+                        tj = 2.0;
+                        scale = 0.0;
+                    }
+                    gsm[tid] = (tid > jj) ? tj * (pk + scale * t) : 0.0;
+                    if (tid == 0) {
+                        gsm[32] = scale;
+                        gsm[33] = alpha;
+                        tau[jj] = tj;
+                    }
+                }
+                __syncthreads();
+                if (pf) {
+                    const long long tq1 = gqr_clock();
+                    a.prof[7] += tq1 - tq0;
+                }
+                // rank-1 update of my rows in registers: x_k -= gamma_k f with
+                // f = x_j scale (the pivot row: f = 1); column j keeps v = f
+                // (the pivot row: alpha).  gamma_k = 0 for k <= jj.
+                {
+                    const double scale = gsm[32], alpha = gsm[33];
+                    double f[4];
+#pragma unroll
+                    for (int r = 0; r < 4; ++r) f[r] = (mine && r == rp) ? 1.0 : pr[r] * scale;
+#pragma unroll
+                    for (int cc = 0; cc < 8; ++cc) {
+                        const double gk = gsm[8 * cg + cc];
+#pragma unroll
+                        for (int r = 0; r < 4; ++r) x[r][cc] = fma(-gk, f[r], x[r][cc]);
+                    }
+                    if (cg == cgj) {
+#pragma unroll
+                        for (int r = 0; r < 4; ++r) x[r][cj] = (mine && r == rp) ? alpha : f[r];
+                    }
+                    if (mine) {  // the pivot row is final: to Ys, and out of the later dots and updates
+#pragma unroll
+                        for (int cc = 0; cc < 8; ++cc) {
+                            const double v = rp == 0 ? x[0][cc] : (rp == 1 ? x[1][cc] : (rp == 2 ? x[2][cc] : x[3][cc]));
+                            Ys[(8 * cg + cc) * ldy + li] = v;
+                        }
+#pragma unroll
+                        for (int r = 0; r < 4; ++r)
+                            if (r == rp) {
+#pragma unroll
+                                for (int cc = 0; cc < 8; ++cc) x[r][cc] = 0.0;
+                            }
+                    }
+                }
+            }
+        }
+        // the rows below the panel's last pivot (v of all 32 reflectors) back to Ys
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            const int i = 32 * warp + rq + 8 * r;
+            if (i < rows && r0 + i >= c0 + 32) {
+#pragma unroll
+                for (int cc = 0; cc < 8; ++cc) Ys[(8 * cg + cc) * ldy + i] = x[r][cc];
+            }
+        }
+        __syncthreads();
         GQR_PROF(1);
         // ---- write back the panel (R rows and v), then the structured Y in smem ----
         for (int e = tid; e < 32 * ldy; e += NT) {

@@ -67,5 +67,7 @@ void run(int64_t n, int m, int G) {
 int main() {
     run<256>(4096, 512, 64);
     run<512>(65536, 512, 148);
+    run<256>(37888, 256, 148);
+    run<256>(65536, 512, 256);
     return 0;
 }
