@@ -938,29 +938,35 @@ __device__ void bd_solve(const double* dl, const double* dg, const double* du, c
     for (int t = N - 3; t >= 0; --t) z[t] = (z[t] - du[t] * z[t + 1] - du2[t] * z[t + 2]) / dg[t];
 }
 
-__global__ void bd_vectors_kernel(BdVecArgs a) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+// One CTA, a thread per leading sigma.  Members of a cluster (sigmas within
+// kBdOrtol ||T|| of a neighbour) factor T - sigma I and run the inverse
+// iteration solves in parallel, a thread each; between the solves a warp per
+// cluster orthonormalises its members in index order (modified Gram-Schmidt,
+// lanes over the 2m entries).  (A thread per cluster — members in sequence —
+// took 5 ms on the 32-fold sigma = 1 cluster of thick-bounds' recovery step,
+// whose work matrix has orthonormal rows by construction.)
+__global__ void __launch_bounds__(1024) bd_vectors_kernel(BdVecArgs a) {
+    const int i = threadIdx.x;
+    const int lane = i & 31, warp = i >> 5, nwarps = blockDim.x >> 5;
     const int m = a.m, r = a.r, N = 2 * m;
-    if (i >= r) return;
     // Gershgorin bound of T (scale of the cluster tolerance and pivot floor)
     double tn = 0.0;
     for (int t = 0; t < N - 1; ++t) tn = fmax(tn, fabs(bd_tgk(a.d, a.e, t)) + (t > 0 ? fabs(bd_tgk(a.d, a.e, t - 1)) : 0.0));
     tn = fmax(tn, N > 1 ? fabs(bd_tgk(a.d, a.e, N - 2)) : 0.0);
     const double ortol = kBdOrtol * tn;
-    if (i > 0 && a.sigma[i - 1] - a.sigma[i] <= ortol) return;  // not a cluster leader
-    int last = i;
-    while (last + 1 < r && a.sigma[last] - a.sigma[last + 1] <= ortol) ++last;
-    if (last == i) return;  // isolated: bd_twisted_kernel's vector stands
-    double* base = a.scratch + (size_t)i * 7 * N;
+    const double tiny = DBL_EPSILON * tn + DBL_MIN;
+    const bool member = i < r && ((i > 0 && a.sigma[i - 1] - a.sigma[i] <= ortol) ||
+                                  (i + 1 < r && a.sigma[i] - a.sigma[i + 1] <= ortol));
+    if (!__syncthreads_or(member)) return;  // no cluster: bd_twisted_kernel's vectors stand
+    double* base = a.scratch + (size_t)(i < r ? i : 0) * 7 * N;
     double* dl = base;
     double* dg = dl + N;
     double* du = dg + N;
     double* du2 = du + N;
+    double* z = base + 4 * N;  // member i's eigenvector of T
     int* ip = reinterpret_cast<int*>(du2 + 2 * N);
-    const double tiny = DBL_EPSILON * tn + DBL_MIN;
-    for (int v = i; v <= last; ++v) {
-        double* z = a.scratch + (size_t)v * 7 * N + 4 * N;  // member v's eigenvector of T (kept for the later members)
-        const double s = a.sigma[v];
+    if (member) {
+        const double s = a.sigma[i];
         // factor T - s I (dgttrf: partial pivoting)
         for (int t = 0; t < N; ++t) dg[t] = -s;
         for (int t = 0; t < N - 1; ++t) {
@@ -993,32 +999,50 @@ __global__ void bd_vectors_kernel(BdVecArgs a) {
         for (int t = 0; t < N - 1; ++t)
             if (dg[t] == 0.0) dg[t] = tiny;
         // start: a fixed pseudo-random vector
-        unsigned h = 0x9e3779b9u * (unsigned)(v + 1);
+        unsigned h = 0x9e3779b9u * (unsigned)(i + 1);
         for (int t = 0; t < N; ++t) {
             h ^= h << 13;
             h ^= h >> 17;
             h ^= h << 5;
             z[t] = 0.5 + (double)(h & 0xffffu) * (1.0 / 65536.0);
         }
-        for (int it = 0; it < 3; ++it) {
-            bd_solve(dl, dg, du, du2, ip, N, z);
-            // orthogonalise against the cluster's earlier members
-            for (int w = i; w < v; ++w) {
-                const double* zw = a.scratch + (size_t)w * 7 * N + 4 * N;
-                double dt = 0.0;
-                for (int t = 0; t < N; ++t) dt = fma(zw[t], z[t], dt);
-                for (int t = 0; t < N; ++t) z[t] = fma(-dt, zw[t], z[t]);
+    }
+    for (int it = 0; it < 3; ++it) {
+        if (member) bd_solve(dl, dg, du, du2, ip, N, z);
+        __syncthreads();
+        // warp w orthonormalises the clusters whose leader index is w, w + nwarps, ...
+        for (int ld = warp; ld < r; ld += nwarps) {
+            if (ld > 0 && a.sigma[ld - 1] - a.sigma[ld] <= ortol) continue;  // not a leader
+            int last = ld;
+            while (last + 1 < r && a.sigma[last] - a.sigma[last + 1] <= ortol) ++last;
+            if (last == ld) continue;  // isolated
+            for (int v = ld; v <= last; ++v) {
+                double* zv = a.scratch + (size_t)v * 7 * N + 4 * N;
+                for (int w = ld; w < v; ++w) {
+                    const double* zw = a.scratch + (size_t)w * 7 * N + 4 * N;
+                    double dt = 0.0;
+                    for (int t = lane; t < N; t += 32) dt = fma(zw[t], zv[t], dt);
+#pragma unroll
+                    for (int o = 16; o >= 1; o >>= 1) dt += __shfl_xor_sync(0xffffffffu, dt, o);
+                    for (int t = lane; t < N; t += 32) zv[t] = fma(-dt, zw[t], zv[t]);
+                }
+                double nr = 0.0;
+                for (int t = lane; t < N; t += 32) nr = fma(zv[t], zv[t], nr);
+#pragma unroll
+                for (int o = 16; o >= 1; o >>= 1) nr += __shfl_xor_sync(0xffffffffu, nr, o);
+                const double inv = 1.0 / sqrt(nr);
+                for (int t = lane; t < N; t += 32) zv[t] *= inv;
+                __syncwarp();
             }
-            double nr = 0.0;
-            for (int t = 0; t < N; ++t) nr = fma(z[t], z[t], nr);
-            const double inv = 1.0 / sqrt(nr);
-            for (int t = 0; t < N; ++t) z[t] *= inv;
         }
+        __syncthreads();
+    }
+    if (member) {
         // x entries (odd positions), normalised
         double nx = 0.0;
         for (int k = 0; k < m; ++k) nx = fma(z[2 * k + 1], z[2 * k + 1], nx);
         const double ix = nx > 0.0 ? 1.0 / sqrt(nx) : 0.0;
-        for (int k = 0; k < m; ++k) a.X[(size_t)v * m + k] = z[2 * k + 1] * ix;
+        for (int k = 0; k < m; ++k) a.X[(size_t)i * m + k] = z[2 * k + 1] * ix;
     }
 }
 

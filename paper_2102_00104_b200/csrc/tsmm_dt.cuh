@@ -36,7 +36,8 @@ inline size_t dt_smem_bytes(int m, int stages, int nt = 4) {
 template <int kDtStages, int NT = 4>
 __global__ void __launch_bounds__(256, 1) tsmm_dt_kernel(const double* __restrict__ X, int64_t n, int m, int64_t ldx,
                                                          const double* __restrict__ V, int64_t ldv, int k,
-                                                         double* __restrict__ Y, int64_t out_rows, int64_t ldy) {
+                                                         double* __restrict__ Y, int64_t out_rows, int64_t ldy,
+                                                         ColSplit cs) {
     extern __shared__ __align__(128) double dsm[];
     __shared__ __align__(8) unsigned long long mbar[8][kDtStages];
     constexpr int kDtVld = 8 * NT + 4;  // smem ld of the V chunk
@@ -71,7 +72,7 @@ __global__ void __launch_bounds__(256, 1) tsmm_dt_kernel(const double* __restric
         __syncwarp();
         if (lane < kDtCols)
             gt_bulk_g2s((unsigned)__cvta_generic_to_shared(xb + ((size_t)s * kDtCols + lane) * kDtCs),
-                        X + (int64_t)(cg + lane) * ldx + rb, (unsigned)(kDtRows * 8), bar(s));
+                        X + col_off(cg + lane, ldx, cs) + rb, (unsigned)(kDtRows * 8), bar(s));
     };
     for (int s = 0; s < kDtStages; ++s)
         if (s < total) issue(s, s);

@@ -16,7 +16,7 @@
 // to rows [(w G + g) m, (w G + g + 1) m) of the stacked matrix the warp-stream
 // levels (tsqr_ws.cuh) finish.
 // Requires X and ld 16-byte aligned (ld even); the last, partial slice is
-// filled by ordinary loads.
+// filled by ordinary loads.  Reads split-column views (ColSplit) in place.
 #pragma once
 
 #include <cfloat>
@@ -76,7 +76,7 @@ __global__ void __launch_bounds__(kPtThreads, MB) tsqr_gt_kernel(GsArgs a) {
         __syncwarp();
         if (lane < m)
             gt_bulk_g2s((unsigned)__cvta_generic_to_shared(xb + ((size_t)s * M + lane) * CS),
-                        a.X + (int64_t)lane * a.ld + sl * SR, (unsigned)(SR * 8), bar(s));
+                        a.X + col_off(lane, a.ld, a.cs) + sl * SR, (unsigned)(SR * 8), bar(s));
     };
     if (lane == 0)
         for (int s = 0; s < ST; ++s) gt_mbar_init(bar(s), 1);
@@ -102,7 +102,7 @@ __global__ void __launch_bounds__(kPtThreads, MB) tsqr_gt_kernel(GsArgs a) {
             const int64_t r0 = sl * SR;
             for (int e = lane; e < m * SR; e += 32) {
                 const int c = e / SR, r = e % SR;
-                xb[((size_t)s * M + c) * CS + r] = (r0 + r < a.n) ? __ldcs(a.X + (int64_t)c * a.ld + r0 + r) : 0.0;
+                xb[((size_t)s * M + c) * CS + r] = (r0 + r < a.n) ? __ldcs(a.X + col_off(c, a.ld, a.cs) + r0 + r) : 0.0;
             }
             __syncwarp();
         }

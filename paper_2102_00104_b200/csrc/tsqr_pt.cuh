@@ -115,6 +115,7 @@ struct GsArgs {
     int64_t T;    // streams
     double* out;  // stacked factors (T m x m, ld ldo), or R (m x m, ld m) when T == 1
     int64_t ldo;
+    ColSplit cs;  // column layout of X (tsqr_gt_kernel only; q = 0: plain)
 };
 
 #ifndef GS_MINB

@@ -38,6 +38,7 @@ struct T2Args {
     double* Scr;  // per-CTA tile scratch (kT2Rows x M, ld kT2Rows)
     int m, M;
     long long* prof;  // optional per-CTA phase cycle counters (8 per CTA), diagnostics
+    ColSplit cs;      // column layout of X (q = 0: plain)
 };
 
 inline size_t t2_smem_bytes(int rows = kT2Rows) {
@@ -293,7 +294,7 @@ __device__ __forceinline__ void t2_build_t(const double* Sm, const double* tau, 
 template <bool SRC_X, bool DST_SMEM, int ROWS, bool SRC_SMEM = false>
 __device__ __forceinline__ void t2_group(const double* src, int64_t lds, int rows, int mcols, double* dst, int64_t ldd,
                                          const double* V, const double* Tm, double* Rrow, int c0, int g, int gd,
-                                         int lane, uint64_t pol_x, uint64_t pol_r) {
+                                         int lane, uint64_t pol_x, uint64_t pol_r, ColSplit cs = ColSplit{0, 0}) {
     const int r = lane >> 2, q = lane & 3;
     double* Rc = Rrow + (int64_t)(g + r - c0) * 32;
     double acc[4][2], rsav[4][2];
@@ -304,7 +305,7 @@ __device__ __forceinline__ void t2_group(const double* src, int64_t lds, int row
         acc[nt][0] = rsav[nt][0];
         acc[nt][1] = rsav[nt][1];
     }
-    const double* scol = src + (int64_t)(g + r) * lds;
+    const double* scol = src + (SRC_X ? col_off(g + r, lds, cs) : (int64_t)(g + r) * lds);
 #pragma unroll
     for (int kc = 0; kc < ROWS / 4; kc += 8) {
         double av[8];
@@ -346,7 +347,8 @@ __device__ __forceinline__ void t2_group(const double* src, int64_t lds, int row
         const double s1 = __shfl_sync(kFull, w2[kk >> 1][1], sl);
         bv[kk] = (q & 1) ? s1 : s0;  // W'[4kk + q][r]
     }
-    const double* s0c = src + (int64_t)(g + 2 * q) * lds;
+    const double* s0c = src + (SRC_X ? col_off(g + 2 * q, lds, cs) : (int64_t)(g + 2 * q) * lds);
+    const int64_t s1o = SRC_X ? col_off(g + 2 * q + 1, lds, cs) - col_off(g + 2 * q, lds, cs) : lds;  // to the odd column
 #pragma unroll 2
     for (int mc = 0; mc < ROWS / 8; mc += 4) {
         double cb[4][2];
@@ -356,7 +358,7 @@ __device__ __forceinline__ void t2_group(const double* src, int64_t lds, int row
             for (int e = 0; e < 2; ++e) {
                 const int row = 8 * (mc + u) + r;
                 if (SRC_X)
-                    cb[u][e] = (row < rows && g + 2 * q + e < mcols) ? ld_stream_hint(s0c + e * lds + row, pol_x) : 0.0;
+                    cb[u][e] = (row < rows && g + 2 * q + e < mcols) ? ld_stream_hint(s0c + e * s1o + row, pol_x) : 0.0;
                 else if (SRC_SMEM) cb[u][e] = s0c[e * lds + row];
                 else cb[u][e] = __ldcg(s0c + e * lds + row);
             }
@@ -426,7 +428,7 @@ __global__ void __launch_bounds__(kT2Threads, 1) tsqr_t128_kernel(T2Args a) {
         for (int e = tid; e < c_first * ROWS; e += kT2Threads) {
             const int c = e / ROWS, i = e % ROWS;
             Pb[(c >> 5) * 32 * Pld + (c & 31) * Pld + i] =
-                (i < rows && c < m) ? ld_hint(Xt + (int64_t)c * a.ld + i, pol_x) : 0.0;
+                (i < rows && c < m) ? ld_hint(Xt + col_off(c, a.ld, a.cs) + i, pol_x) : 0.0;
         }
         if (warp == 0) cp_async_wait_all();
         __syncthreads();
@@ -479,7 +481,8 @@ __global__ void __launch_bounds__(kT2Threads, 1) tsqr_t128_kernel(T2Args a) {
             } else {
                 for (int g = nxt + 32 + 8 * uw; g < M; g += 8 * NUW) {
                     if (p == 0)
-                        t2_group<true, false, ROWS>(Xt, a.ld, rows, m, Scr, ROWS, V, Tp, Rrow, c0, g, g, lane, pol_x, pol_r);
+                        t2_group<true, false, ROWS>(Xt, a.ld, rows, m, Scr, ROWS, V, Tp, Rrow, c0, g, g, lane, pol_x, pol_r,
+                                                    a.cs);
                     else
                         t2_group<false, false, ROWS>(Scr, ROWS, rows, m, Scr, ROWS, V, Tp, Rrow, c0, g, g, lane, pol_x,
                                                pol_r);

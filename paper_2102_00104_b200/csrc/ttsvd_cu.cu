@@ -232,6 +232,9 @@ int set_device(ttsvd_cu_ctx* ctx) {
     return TTSVD_OK;
 }
 
+// internal: the kernel a shape dispatches to cannot read a split-column view
+// (ColSplit) in place; the caller materialises the view and calls again
+constexpr int kNoView = -2;
 constexpr int kTsqrThreads = 256;
 constexpr int kSmemLimit = 227 * 1024;
 constexpr int kTsmmSmem = 200 * 1024;  // V block of tsmm_kernel (m x KC doubles)
@@ -552,7 +555,7 @@ int tsqr_gs_levels(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t
 // Tall and 16-byte aligned: the same streams fed by the bulk-copy engine
 // (tsqr_gt.cuh), one 8-warp CTA per SM, every warp at least one full slice.
 template <int M, int P, int U>
-int tsqr_gt_levels(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t ld, double* R) {
+int tsqr_gt_levels(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t ld, double* R, ColSplit cs) {
     constexpr int G = 32 / P, SR = G * U;
     const void* fn = (const void*)tsqr_gt_kernel<M, P, U>;
     TT_TRY(kattr(ctx, fn, (int)gt_smem_bytes<M, P, U>()));
@@ -562,7 +565,7 @@ int tsqr_gt_levels(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t
     DevBuf& ob = ctx->ws_gs;
     TT_TRY(ensure(ob, (size_t)T * m * m * 8));
     double* out = as<double>(ob);
-    GsArgs ga{X, n, ld, m, T, out, T * m};
+    GsArgs ga{X, n, ld, m, T, out, T * m, cs};
     kmark(ctx, 0, TTSVD_K_GS);
     tsqr_gt_kernel<M, P, U><<<(unsigned)ctas, kPtThreads, gt_smem_bytes<M, P, U>(), ctx->stream>>>(ga);
     TT_TRY(check_launch(ctx, "tsqr_gt_kernel"));
@@ -570,9 +573,13 @@ int tsqr_gt_levels(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t
     return tsqr_ws_device(ctx, out, T * m, m, T * m, R, false);
 }
 
-int tsqr_gs_device(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t ld, double* R) {
-    if (n >= (int64_t)ctx->num_sms * kGtWarps * 64 * 4 && (ld & 1) == 0 && ((uintptr_t)X & 15) == 0)
-        return m <= 16 ? tsqr_gt_levels<16, 4, 8>(ctx, X, n, m, ld, R) : tsqr_gt_levels<32, 8, 8>(ctx, X, n, m, ld, R);
+int tsqr_gs_device(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t ld, double* R,
+                   ColSplit cs = ColSplit{0, 0}) {
+    if (n >= (int64_t)ctx->num_sms * kGtWarps * 64 * 4 && (ld & 1) == 0 && ((uintptr_t)X & 15) == 0 &&
+        (cs.q == 0 || (cs.ld_lo & 1) == 0))
+        return m <= 16 ? tsqr_gt_levels<16, 4, 8>(ctx, X, n, m, ld, R, cs)
+                       : tsqr_gt_levels<32, 8, 8>(ctx, X, n, m, ld, R, cs);
+    if (cs.q) return kNoView;
     // measured on B200 (tools/gs_var.sh): 4 lanes per stream at m <= 16, 8 at m <= 32
     // (a whole warp per stream at 32 < m <= 64 measured slower than t128)
     return m <= 16 ? tsqr_gs_levels<16, 4, 8>(ctx, X, n, m, ld, R) : tsqr_gs_levels<32, 8, 8>(ctx, X, n, m, ld, R);
@@ -604,11 +611,15 @@ int tsqr_sq_levels(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t
 }
 
 int tsqr_device(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t ld, double* R,
-                const double* R_init = nullptr) {
+                const double* R_init = nullptr, ColSplit cs = ColSplit{0, 0}) {
     ctx->last_kernel = TTSVD_K_NONE;
     if (m > kSmallM) {
         const int M = (m + 31) / 32 * 32;
         const int64_t RS = blk_rsize(M);
+        // a split-column view is read in place by the tall-tile kernel only
+        if (cs.q && (R_init || (m <= 64 && n <= kSqMaxRows) || (n >= M && n <= (int64_t)256 * M) ||
+                     n < (int64_t)ctx->num_sms * 4 * kT2Rows))
+            return kNoView;
         if (!R_init && m <= 64 && n <= kSqMaxRows) {
             kmark(ctx, 0, TTSVD_K_SQ);
             const int rc = tsqr_sq_levels(ctx, X, n, m, ld, R);
@@ -638,7 +649,7 @@ int tsqr_device(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t ld
             double* parts = as<double>(ctx->ws_R);
             const void* tfn = t2rows == 256 ? (const void*)tsqr_t128_kernel<256> : (const void*)tsqr_t128_kernel<128>;
             TT_TRY(kattr(ctx, tfn, (int)t2_smem_bytes(t2rows)));
-            T2Args ta{X, n, ld, parts, as<double>(ctx->ws_Scr), m, M, nullptr};
+            T2Args ta{X, n, ld, parts, as<double>(ctx->ws_Scr), m, M, nullptr, cs};
             kmark(ctx, 0, TTSVD_K_T128);
             if (t2rows == 256)
                 tsqr_t128_kernel<256><<<(unsigned)Gt, kT2Threads, t2_smem_bytes(256), ctx->stream>>>(ta);
@@ -679,8 +690,9 @@ int tsqr_device(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t ld
         }
         return copy_leading(ctx, parts, M, m, R);
     }
+    if (cs.q && (R_init || m <= 8 || n < 4096)) return kNoView;
     if (!R_init && m <= 8 && n >= 4096) return tsqr_pt_device(ctx, X, n, m, ld, R);
-    if (!R_init && n >= 4096) return tsqr_gs_device(ctx, X, n, m, ld, R);
+    if (!R_init && n >= 4096) return tsqr_gs_device(ctx, X, n, m, ld, R, cs);
     TsqrPlan p = tsqr_plan(m);
     const int64_t min_rows = std::max<int64_t>(p.bt, 8 * (int64_t)m);
     int64_t G = std::max<int64_t>(1, n / min_rows);
@@ -879,7 +891,7 @@ int svd_vectors(ttsvd_cu_ctx* ctx, int64_t r, const double* sigma, double* Vout)
     bd_twisted_kernel<<<(unsigned)((r + kTwWarps - 1) / kTwWarps), kTwWarps * 32, tsm, ctx->stream>>>(va);
     TT_TRY(check_launch(ctx, "bd_twisted_kernel"));
     // clusters (rare): inverse iteration with modified Gram-Schmidt
-    bd_vectors_kernel<<<(unsigned)((r + 63) / 64), 64, 0, ctx->stream>>>(va);
+    bd_vectors_kernel<<<1, (unsigned)std::min<int64_t>(1024, (r + 31) / 32 * 32), 0, ctx->stream>>>(va);
     TT_TRY(check_launch(ctx, "bd_vectors_kernel"));
     if (n <= 512) {
         TT_TRY(kattr(ctx, (const void*)bd_back4s_kernel<8>, (int)bd_back4s_smem(8)));
@@ -1008,7 +1020,7 @@ int launch_tsmm_dmma(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64
 }
 
 int tsmm_device(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t ldx, const double* V, int64_t ldv, int k,
-                double* Y, int64_t out_rows, int64_t out_cols, int64_t ldy) {
+                double* Y, int64_t out_rows, int64_t out_cols, int64_t ldy, ColSplit cs = ColSplit{0, 0}) {
     int rc;
     // FP64 tensor cores once the FMA kernels turn compute-bound (k > 8 output
     // columns, m >= 32): rows staged by TMA bulk copies (tsmm_dt.cuh), one
@@ -1017,19 +1029,21 @@ int tsmm_device(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t ld
     const int dt_nt = k > 16 ? 4 : 2;
     const int dt_stages = dt_smem_bytes(m, 4, dt_nt) <= (size_t)kSmemLimit - 2048 ? 4 : 2;
     const bool dt = k > 8 && m >= 32 && n >= (int64_t)1 << 16 && n % kDtRows == 0 && m % kDtCols == 0 &&
-                    (ldx & 1) == 0 && ((uintptr_t)X & 15) == 0 &&
+                    (ldx & 1) == 0 && ((uintptr_t)X & 15) == 0 && (cs.q == 0 || (cs.ld_lo & 1) == 0) &&
                     dt_smem_bytes(m, dt_stages, dt_nt) <= (size_t)kSmemLimit - 2048;
+    if (cs.q && !dt) return kNoView;  // only the TMA-staged kernel reads a split-column view
     const bool dmma = !dt && k > 16 && m >= 32 && n >= (int64_t)1 << 18 &&
                       (size_t)((m + 3) & ~3) * tsmm_vld(4) * 8 <= 200 * 1024;
     if (dt || dmma) {
         if (dt) {
-            void (*fn)(const double*, int64_t, int, int64_t, const double*, int64_t, int, double*, int64_t, int64_t) =
+            void (*fn)(const double*, int64_t, int, int64_t, const double*, int64_t, int, double*, int64_t, int64_t,
+                       ColSplit) =
                 dt_nt == 4 ? (dt_stages == 4 ? tsmm_dt_kernel<4, 4> : tsmm_dt_kernel<2, 4>)
                            : (dt_stages == 4 ? tsmm_dt_kernel<4, 2> : tsmm_dt_kernel<2, 2>);
             TT_TRY(kattr(ctx, (const void*)fn, kSmemLimit - 2048));
             dim3 grid((unsigned)std::min<int64_t>(ctx->num_sms, (n / kDtRows + 7) / 8),
                       (unsigned)((k + 8 * dt_nt - 1) / (8 * dt_nt)));
-            fn<<<grid, 256, dt_smem_bytes(m, dt_stages, dt_nt), ctx->stream>>>(X, n, m, ldx, V, ldv, k, Y, out_rows, ldy);
+            fn<<<grid, 256, dt_smem_bytes(m, dt_stages, dt_nt), ctx->stream>>>(X, n, m, ldx, V, ldv, k, Y, out_rows, ldy, cs);
             rc = check_launch(ctx, "tsmm_dt_kernel");
         } else {
             rc = launch_tsmm_dmma<4>(ctx, X, n, m, ldx, V, ldv, k, Y, out_rows, ldy);
@@ -1205,9 +1219,12 @@ int d2h(ttsvd_cu_ctx* ctx, double* dst, const double* src, size_t count) {
 // records are compared and a chain that met a smaller rank anywhere returns
 // kMispredict (the caller runs it again step by step).  Only used when delta
 // is known up front (eps = 0, or a given delta of 0).
+// cs0: the column layout of the FIRST work matrix (thick-bounds' merged view
+// of X, read in place by K_TSQR / K_TSMM; kNoView when the first step's TSQR
+// kernel cannot, before anything has run).
 int run_chain_impl(ttsvd_cu_ctx* ctx, WorkView cur, const std::vector<int64_t>& dims, int64_t r_max, double eps,
                    int64_t d_for_delta, ttsvd_cu_tt* out, double* delta_io, double* first_sigma_norm_out,
-                   bool spec) {
+                   bool spec, ColSplit cs0) {
     const int64_t d = (int64_t)dims.size();
     out->dims = dims;
     out->cores.assign(d, {});
@@ -1273,6 +1290,8 @@ int run_chain_impl(ttsvd_cu_ctx* ctx, WorkView cur, const std::vector<int64_t>& 
         st.rows = cur.rows;
         st.cols = m;
         const bool tall = cur.rows >= cur.cols;
+        const ColSplit cs = (i == d - 1) ? cs0 : ColSplit{0, 0};
+        if (cs.q && !tall) return kNoView;
         const int64_t nsig = tall ? m : cur.rows;
         TT_TRY(ensure(ctx->ws_sigma, (size_t)std::max<int64_t>(m, nsig) * 8));
         TT_TRY(ensure(ctx->ws_V, (size_t)m * std::max<int64_t>(nsig, 1) * 8));
@@ -1283,7 +1302,7 @@ int run_chain_impl(ttsvd_cu_ctx* ctx, WorkView cur, const std::vector<int64_t>& 
         if (tall) {
             TT_TRY(ensure(ctx->ws_X, (size_t)m * m * 8));
             double* R = as<double>(ctx->ws_X);
-            TT_TRY(tsqr_device(ctx, cur.data, cur.rows, (int)m, cur.ld, R));
+            TT_TRY(tsqr_device(ctx, cur.data, cur.rows, (int)m, cur.ld, R, nullptr, cs));
             tm.mark(1);
             TT_TRY(svd_work(ctx, R, m, m, m, true, false, d_sigma, d_V, &sweeps));
         } else {
@@ -1343,7 +1362,22 @@ int run_chain_impl(ttsvd_cu_ctx* ctx, WorkView cur, const std::vector<int64_t>& 
         TT_TRY(ensure(ctx->ws_work[which], (size_t)ldy * out_cols * 8));
         double* Y = as<double>(ctx->ws_work[which]);
         tm.mark(3);
-        TT_TRY(tsmm_device(ctx, cur.data, cur.rows, (int)m, cur.ld, d_V, m, (int)rnew, Y, out_rows, out_cols, ldy));
+        {
+            int rc = tsmm_device(ctx, cur.data, cur.rows, (int)m, cur.ld, d_V, m, (int)rnew, Y, out_rows, out_cols, ldy, cs);
+            if (rc == kNoView) {
+                // the rank left the kernel that reads the view: materialise it
+                // (copy_logical, storage.hpp:158-172) for this one product
+                const int64_t ldm = padded_stride_h(cur.rows);
+                TT_TRY(ensure(ctx->ws_thick[0], (size_t)ldm * m * 8));
+                double* Wm = as<double>(ctx->ws_thick[0]);
+                for (int64_t id = 0; id < m / cs.q; ++id)
+                    TT_CUDA(cudaMemcpy2DAsync(Wm + id * cs.q * ldm, (size_t)ldm * 8, cur.data + id * cur.ld,
+                                              (size_t)cs.ld_lo * 8, (size_t)cur.rows * 8, (size_t)cs.q,
+                                              cudaMemcpyDeviceToDevice, ctx->stream));
+                rc = tsmm_device(ctx, Wm, cur.rows, (int)m, ldm, d_V, m, (int)rnew, Y, out_rows, out_cols, ldy);
+            }
+            if (rc != TTSVD_OK) return rc;
+        }
         tm.mark(4);
         if (tm.on) {
             st.t_tsqr_ms = tm.ms(0, 1);
@@ -1402,16 +1436,16 @@ int run_chain_impl(ttsvd_cu_ctx* ctx, WorkView cur, const std::vector<int64_t>& 
 
 int run_chain(ttsvd_cu_ctx* ctx, WorkView cur, const std::vector<int64_t>& dims, int64_t r_max, double eps,
               int64_t d_for_delta, ttsvd_cu_tt* out, double* delta_io = nullptr,
-              double* first_sigma_norm_out = nullptr) {
+              double* first_sigma_norm_out = nullptr, ColSplit cs0 = ColSplit{0, 0}) {
     const double delta_in = delta_io ? *delta_io : -1.0;
     // timing reads its events step by step, so a timed chain runs step by step
     const bool spec = !ctx->timing && (delta_in < 0.0 ? eps == 0.0 : delta_in == 0.0);
     if (spec) {
-        const int rc = run_chain_impl(ctx, cur, dims, r_max, eps, d_for_delta, out, delta_io, first_sigma_norm_out, true);
+        const int rc = run_chain_impl(ctx, cur, dims, r_max, eps, d_for_delta, out, delta_io, first_sigma_norm_out, true, cs0);
         if (rc != kMispredict) return rc;
         if (delta_io) *delta_io = delta_in;
     }
-    return run_chain_impl(ctx, cur, dims, r_max, eps, d_for_delta, out, delta_io, first_sigma_norm_out, false);
+    return run_chain_impl(ctx, cur, dims, r_max, eps, d_for_delta, out, delta_io, first_sigma_norm_out, false, cs0);
 }
 
 // tsmm.hpp:84-126 transpose_reorder: Y (out_rows x out_cols, ld ldy) <- the
@@ -1911,21 +1945,31 @@ int ttsvd_cu_tt_svd_thick(ttsvd_cu_ctx* ctx, const double* X, const int64_t* dim
     TT_TRY(ttsvd_cu_choose_combined_dims(dims, d, m_min, f1_min, r_tilde, n_r_tilde, r_max, &k, &m));
     if (k == 1) return ttsvd_cu_tt_svd(ctx, X, dims, d, ldx, r_max, eps, out);
 
-    // merged tensor (n_1, ..., n_{d-k}, m) in its own padded layout (copy_logical,
-    // storage.hpp:158-172): column x of its matricization is the contiguous run
-    // of X's column x / q starting at row (x mod q) (N/m), q = m / n_d
-    const int64_t rows_m = total / m, ldm = padded_stride_h(rows_m), q = m / dims[d - 1];
-    TT_TRY(ensure(ctx->ws_thick[0], (size_t)ldm * m * 8));
-    double* W = as<double>(ctx->ws_thick[0]);
-    for (int64_t id = 0; id < dims[d - 1]; ++id)
-        TT_CUDA(cudaMemcpy2DAsync(W + id * q * ldm, (size_t)ldm * 8, X + id * ldx, (size_t)rows_m * 8,
-                                  (size_t)rows_m * 8, (size_t)q, cudaMemcpyDeviceToDevice, ctx->stream));
+    // merged tensor (n_1, ..., n_{d-k}, m): column x of its matricization is the
+    // contiguous run of X's column x / q starting at row (x mod q) (N/m),
+    // q = m / n_d — a split-column view of X that K_TSQR and K_TSMM read in
+    // place (ColSplit).  Only when the first step's kernels cannot (short or
+    // narrow shapes) is it copied into its own padded layout (copy_logical,
+    // storage.hpp:158-172; tt_svd.hpp:347-348).
+    const int64_t rows_m = total / m, q = m / dims[d - 1];
     std::vector<int64_t> mdims(dims, dims + d - k);
     mdims.push_back(m);
     const int64_t dm = (int64_t)mdims.size();
     ttsvd_cu_tt main_tt;
     double delta = -1.0, fsn = 0.0;
-    TT_TRY(run_chain(ctx, WorkView{W, rows_m, m, ldm}, mdims, r_max, eps, dm, &main_tt, &delta, &fsn));
+    int rc_main = run_chain(ctx, WorkView{X, rows_m, m, ldx}, mdims, r_max, eps, dm, &main_tt, &delta, &fsn,
+                            ColSplit{(int)q, rows_m});
+    if (rc_main == kNoView) {
+        const int64_t ldm = padded_stride_h(rows_m);
+        TT_TRY(ensure(ctx->ws_thick[0], (size_t)ldm * m * 8));
+        double* W = as<double>(ctx->ws_thick[0]);
+        for (int64_t id = 0; id < dims[d - 1]; ++id)
+            TT_CUDA(cudaMemcpy2DAsync(W + id * q * ldm, (size_t)ldm * 8, X + id * ldx, (size_t)rows_m * 8,
+                                      (size_t)rows_m * 8, (size_t)q, cudaMemcpyDeviceToDevice, ctx->stream));
+        delta = -1.0;
+        rc_main = run_chain(ctx, WorkView{W, rows_m, m, ldm}, mdims, r_max, eps, dm, &main_tt, &delta, &fsn);
+    }
+    if (rc_main != TTSVD_OK) return rc_main;
 
     // recovery: TT-SVD of the combined core T_bar (r_b x m) as the (k+1)-mode
     // tensor (r_b, n_{d-k+1}, ..., n_d) (tt_svd.hpp:350-371)

@@ -41,6 +41,20 @@ __device__ __forceinline__ void dmma884(double (&d)[2], double a, double b) {
                  : "d"(a), "d"(b));
 }
 
+// A work matrix whose columns are not uniformly strided: column c starts at
+// (c / q) ld + (c mod q) ld_lo (q = 0: the plain c ld).  Thick-bounds' merged
+// matricization (n_1 .. n_{d-k}) x (n_{d-k+1} .. n_d) is such a view of the
+// caller's padded X (q = m / n_d, ld_lo = its row count), so K_TSQR and K_TSMM
+// read it in place instead of through copy_logical's copy (tt_svd.hpp:347-348,
+// storage.hpp:158-172).
+struct ColSplit {
+    int q;
+    int64_t ld_lo;
+};
+__host__ __device__ __forceinline__ int64_t col_off(int c, int64_t ld, ColSplit cs) {
+    return cs.q ? (int64_t)(c / cs.q) * ld + (int64_t)(c % cs.q) * cs.ld_lo : (int64_t)c * ld;
+}
+
 // 1/sqrt(x) and 1/x for reflector / rotation scalars without the libdevice slow-path
 // calls (a call site inside the unrolled reflector loop pins every live value
 // across it): the SFU seed (measured max relative error 2^-20,

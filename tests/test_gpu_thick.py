@@ -92,3 +92,36 @@ def test_rank_one_boundary(tt, ref):
     # the boundary core is right-orthonormal: the norm sits in core 0
     b = T.cores[-1].data
     assert abs(np.linalg.norm(b) - 1.0) <= 1e-12
+
+
+# The merged matricization read in place (ColSplit view of the caller's padded
+# X; tt_svd.hpp:347-348's copy_logical avoided): tall-tile TSQR + TMA-staged
+# TSMM (m = 64), TMA-staged streams + TSMM (m = 32), and a rank (6 <= 8) that
+# leaves the view-reading TSMM kernel, so the view is materialised for that one
+# product.  Same parity bar as the copied layout.
+@pytest.mark.parametrize("dims,r_max,m_min,expect_km,tt_rank", [
+    ([4] * 12, 16, 16, (3, 64), 0),     # uniform[-1,1] in the padded layout
+    ([2] * 24, 12, 32, (5, 32), 12),    # exact TT (rank <= 12) + 1e-8 noise: well separated frames
+    ([2] * 24, 6, 16, (4, 16), 6),
+])
+def test_thick_view_in_place(tt, orc, ref, dims, r_max, m_min, expect_km, tt_rank):
+    import torch
+    if tt_rank:
+        from oracle.oracle import random_tt, tt_reconstruct
+        d = len(dims)
+        ranks = [min(tt_rank, 2 ** min(j, d - j)) for j in range(d + 1)]
+        X = tt_reconstruct(random_tt(dims, ranks, 77), dims)
+        rng = np.random.default_rng(78)
+        X = np.asfortranarray(X + 1e-8 * np.linalg.norm(X) / np.sqrt(X.size) * rng.standard_normal(X.shape))
+    else:
+        X = orc.gen_uniform(5, dims)
+    p = tt.ThickBoundsParams(m_min=m_min)
+    assert tt.choose_combined_dims(dims, p, r_max) == expect_km
+    free0 = torch.cuda.mem_get_info()[0]
+    T, r, cores = run_thick(tt, ref, X, dims, r_max, 0.0, m_min)
+    free1 = torch.cuda.mem_get_info()[0]
+    check(ref, X, dims, T, r, cores, err_tol=1e-8 if tt_rank else 1e-10)
+    if r_max > 8:
+        # no copy of X (8 prod(dims) bytes) was allocated next to it (the
+        # device copy of X itself is; the work buffers are a fraction of it)
+        assert free0 - free1 < 2 * 8 * int(np.prod(dims)) - (8 * int(np.prod(dims))) // 4

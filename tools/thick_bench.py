@@ -18,3 +18,11 @@ for name, f in (("plain", lambda: tt.tt_svd_tsqr(X, dims, spec)),
     torch.cuda.synchronize()
     ms = (time.perf_counter() - t0) / 3 * 1e3
     print(f"{name}: {ms:.2f} ms  {8 * X.shape[0] * X.shape[1] / ms / 1e6:.2f} GB/s  ranks {T.ranks()}", flush=True)
+
+ctx = tt.context()
+ctx.set_timing(True)
+T = tt.tt_svd_thick_bounds(X, dims, spec, tt.ThickBoundsParams())
+torch.cuda.synchronize()
+ctx.set_timing(False)
+for s in T.steps:
+    print(f"thick step {s.step}: {s.rows}x{s.cols} r={s.rank} tsqr {s.t_tsqr*1e3:.3f} ({s.tsqr_kernel}) svd {s.t_small_svd*1e3:.3f} tsmm {s.t_tsmm*1e3:.3f} ms")
