@@ -35,6 +35,11 @@ __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
     const unsigned s = (unsigned)__cvta_generic_to_shared(smem_dst);
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gsrc) : "memory");
 }
+// 8-byte asynchronous copy with an L2 eviction policy (streamed input rows)
+__device__ __forceinline__ void cp_async8_hint(void* smem_dst, const void* gsrc, uint64_t pol) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem_dst);
+    asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 8, %2;" ::"r"(s), "l"(gsrc), "l"(pol) : "memory");
+}
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
 // warp: the 32 x 32 diagonal block of a row panel (packed layout: column k at

@@ -425,12 +425,16 @@ __global__ void __launch_bounds__(kT2Threads, 1) tsqr_t128_kernel(T2Args a) {
         // (and panel 1's raw columns into the second buffer, for phase A of
         // p = 0 from shared memory; all loads of both panels in flight at once)
         const int c_first = npan > 1 ? 64 : 32;
+        // (cp.async: every thread's loads in flight at once — a load followed
+        // by its shared-memory store serialised 32 HBM round trips per thread
+        // and tile)
         for (int e = tid; e < c_first * ROWS; e += kT2Threads) {
             const int c = e / ROWS, i = e % ROWS;
-            Pb[(c >> 5) * 32 * Pld + (c & 31) * Pld + i] =
-                (i < rows && c < m) ? ld_hint(Xt + col_off(c, a.ld, a.cs) + i, pol_x) : 0.0;
+            double* dst = &Pb[(c >> 5) * 32 * Pld + (c & 31) * Pld + i];
+            if (i < rows && c < m) cp_async8_hint(dst, Xt + col_off(c, a.ld, a.cs) + i, pol_x);
+            else *dst = 0.0;
         }
-        if (warp == 0) cp_async_wait_all();
+        cp_async_wait_all();
         __syncthreads();
         T2_PROF(0);
         if (panel_warp) {
