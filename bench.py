@@ -264,7 +264,7 @@ def run_ours(args, rank: int, world: int):
         mp = peaks()
         traffic = None
         try:  # DRAM bytes of the same kernel from the committed ncu --set full capture
-            tr = json.load(open(os.path.join(ROOT, "profiles", "r01_traffic.json")))
+            tr = json.load(open(os.path.join(ROOT, "profiles", "r02_traffic.json")))
             if tr["kernel"] == st.tsqr_kernel:
                 traffic = tr["dram_bytes_per_launch"]
         except Exception:

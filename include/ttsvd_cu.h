@@ -67,7 +67,8 @@ enum {
     TTSVD_K_GQR = 5,   /* cooperative whole-grid QR */
     TTSVD_K_PT = 6,    /* thread streams, m <= 8 */
     TTSVD_K_GS = 7,    /* lane-group streams, 8 < m <= 32 */
-    TTSVD_K_SQ = 8     /* levels of 256-row register tile QRs, 32 < m <= 64 */
+    TTSVD_K_SQ = 8,    /* levels of 256-row register tile QRs, 32 < m <= 64 */
+    TTSVD_K_GT = 9     /* lane-group streams fed by TMA bulk copies, 8 < m <= 32, tall */
 };
 
 /* All-gather over the ranks of a distributed run (replaces the in-process

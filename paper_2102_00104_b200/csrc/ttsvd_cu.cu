@@ -566,10 +566,10 @@ int tsqr_gt_levels(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t
     TT_TRY(ensure(ob, (size_t)T * m * m * 8));
     double* out = as<double>(ob);
     GsArgs ga{X, n, ld, m, T, out, T * m, cs};
-    kmark(ctx, 0, TTSVD_K_GS);
+    kmark(ctx, 0, TTSVD_K_GT);
     tsqr_gt_kernel<M, P, U><<<(unsigned)ctas, kPtThreads, gt_smem_bytes<M, P, U>(), ctx->stream>>>(ga);
     TT_TRY(check_launch(ctx, "tsqr_gt_kernel"));
-    kmark(ctx, 1, TTSVD_K_GS);
+    kmark(ctx, 1, TTSVD_K_GT);
     return tsqr_ws_device(ctx, out, T * m, m, T * m, R, false);
 }
 

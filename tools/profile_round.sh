@@ -21,4 +21,10 @@ ncu --set full --import-source on --clock-control none -k regex:bd_reg --launch-
     -o gpurun_out/${TAG}_bd512 python bench.py --steps 1 --warmup 0 --no-cpu-baseline --north-star off > /dev/null 2>&1 || true
 ncu --set full --import-source on --clock-control none -k regex:tsqr_t128 --launch-count 1 \
     -o gpurun_out/${TAG}_t256 python bench.py --steps 1 --warmup 0 --no-cpu-baseline --north-star off > /dev/null 2>&1 || true
+ncu --set full --import-source on --clock-control none -k regex:tsmm_dt --launch-count 1 \
+    -o gpurun_out/${TAG}_tsmm_dt python bench.py --steps 1 --warmup 0 --no-cpu-baseline --north-star off > /dev/null 2>&1 || true
+ncu --set full --import-source on --clock-control none -k regex:gqr_kernel --launch-skip 1 --launch-count 1 \
+    -o gpurun_out/${TAG}_gqr512 python bench.py --steps 1 --warmup 0 --no-cpu-baseline --north-star off > /dev/null 2>&1 || true
+ncu --set full --import-source on --clock-control none -k regex:tsqr_gt --launch-count 1 \
+    -o gpurun_out/${TAG}_gt16 python bench.py --steps 1 --warmup 0 --no-cpu-baseline --north-star off > /dev/null 2>&1 || true
 echo done
