@@ -107,6 +107,9 @@ def test_tsqr_wide_kernels(tt, n, m, kind):
     if kind != "dense":
         rank = 7 if kind == "lowrank" else m - 2
         assert s_r[rank] <= 1e-13 * s_r[0]
+    # the same bytes give the same R (fixed reduction orders; a race in the
+    # register-panel exchanges would show here)
+    assert np.array_equal(host(tt.tsqr(X)), R)
 
 
 # The register tile levels (tsqr_sq_kernel, 32 < m <= 64, n <= 2^16: 256-row
@@ -478,3 +481,4 @@ def test_tsmm_shapes_vs_oracle(tt, orc, n, m, k, nn):
     y = host(tt.tsmm_reshape(x, v, out_rows, out_cols))
     yo = orc.tsmm_reshape(x, v, out_rows, out_cols)[:out_rows]
     assert np.max(np.abs(y - yo)) <= 1e-13 * max(np.linalg.norm(yo), 1.0)
+    assert np.array_equal(host(tt.tsmm_reshape(x, v, out_rows, out_cols)), y)
