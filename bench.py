@@ -218,11 +218,12 @@ def run_ours(args, rank: int, world: int):
     ranks_out = T.ranks()
 
     # ---- timed region: K steps, device events on the launching stream ----
-    ctx.set_timing(True)
+    # (the library's per-phase events stay OFF here: they synchronise inside
+    # a step and switch the chain to its step-by-step form; the phases are
+    # taken from separate steps after the timed region)
     stream = torch.cuda.current_stream()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     launches0 = ctx.launches
-    phase = []
     with Clocks(dev) as clk:
         if dist:
             dist.barrier()
@@ -230,13 +231,18 @@ def run_ours(args, rank: int, world: int):
         ev0.record(stream)
         for _ in range(args.steps):
             T = step()
-            phase.append(T.steps)
         ev1.record(stream)
         torch.cuda.synchronize()
         if dist:
             dist.barrier()
-    ctx.set_timing(False)
     launches = ctx.launches - launches0
+    # per-phase times (library events around every TSQR / SVD / TSMM), untimed
+    ctx.set_timing(True)
+    phase = []
+    for _ in range(min(args.steps, 3)):
+        phase.append(step().steps)
+    torch.cuda.synchronize()
+    ctx.set_timing(False)
     ms = ev0.elapsed_time(ev1) / args.steps
     if dist:
         t = torch.tensor([ms], dtype=torch.float64, device="cuda")
@@ -326,6 +332,26 @@ def run_ours(args, rank: int, world: int):
                                             "bandwidth, flops / measured FP64 peak) divided by ms_per_step; the "
                                             "small SVD (svd_ms per step) is the latency term outside the roofline"},
         }
+    # ---- the reference's thick-bounds variant (Alg. 3) on the same tensor, for information ----
+    if world == 1 and out is not None:
+        import torch
+        tb = tt.ThickBoundsParams()
+        spec = tt.TruncationSpec(r_max=r_max, eps=eps)
+        for _ in range(2):
+            Tt = tt.tt_svd_thick_bounds(X, dims, spec, tb)
+        torch.cuda.synchronize()
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0.record(stream)
+        for _ in range(3):
+            Tt = tt.tt_svd_thick_bounds(X, dims, spec, tb)
+        t1.record(stream)
+        torch.cuda.synchronize()
+        tms = t0.elapsed_time(t1) / 3
+        k_m = tt.choose_combined_dims(dims, tb, r_max)
+        out["thick_bounds"] = {"api": "tt_svd_thick_bounds (Alg. 3, tt_svd.hpp:292-400), merged view read in place",
+                               "combined_dims": list(k_m), "ms_per_step": round(tms, 4),
+                               "value": round(nbytes_local / (tms * 1e-3) / 1e9, 3), "unit": UNIT,
+                               "ranks": Tt.ranks()}
     # ---- e2e: the public host-buffer entry, H2D inside the timed region ----
     if world == 1:
         import torch
