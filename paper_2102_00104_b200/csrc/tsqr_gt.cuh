@@ -91,11 +91,19 @@ __global__ void __launch_bounds__(kPtThreads, MB) tsqr_gt_kernel(GsArgs a) {
     for (int i = 0; i < M; ++i)
 #pragma unroll
         for (int k = 0; k < MC; ++k) R[i][k] = 0.0;
-    int64_t sl = wg;
+    const int64_t sl_end = a.sl_hi > 0 ? a.sl_hi : slices;
+    double* st = a.state + ((size_t)wg * 32 + lane) * (M * MC);
+    if (a.flags & 1) {
+#pragma unroll
+        for (int i = 0; i < M; ++i)
+#pragma unroll
+            for (int k = 0; k < MC; ++k) R[i][k] = st[i * MC + k];
+    }
+    int64_t sl = a.sl_lo + wg;
     for (int s = 0; s < ST; ++s)
-        if (sl + (int64_t)s * W < slices) issue(sl + (int64_t)s * W, s);
+        if (sl + (int64_t)s * W < sl_end) issue(sl + (int64_t)s * W, s);
     unsigned phase = 0;
-    for (int s = 0; sl < slices; sl += W) {
+    for (int s = 0; sl < sl_end; sl += W) {
         if (full(sl)) {
             gt_mbar_wait(bar(s), phase);
         } else {
@@ -115,7 +123,7 @@ __global__ void __launch_bounds__(kPtThreads, MB) tsqr_gt_kernel(GsArgs a) {
                 for (int k = 0; k < MC; ++k) x[u][k] = xs[(q + P * k) * CS + G * u];
         }
         __syncwarp();  // the stage has been read: refill it
-        issue(sl + (int64_t)ST * W, s);
+        if (sl + (int64_t)ST * W < sl_end) issue(sl + (int64_t)ST * W, s);
 #pragma unroll
         for (int j = 0; j < M; ++j) {
             const int qj = j % P, kj = j / P;
@@ -165,6 +173,13 @@ __global__ void __launch_bounds__(kPtThreads, MB) tsqr_gt_kernel(GsArgs a) {
             s = 0;
             phase ^= 1;
         }
+    }
+    if (a.flags & 2) {  // a chunk that is not the last: keep the running factors
+#pragma unroll
+        for (int i = 0; i < M; ++i)
+#pragma unroll
+            for (int k = 0; k < MC; ++k) st[i * MC + k] = R[i][k];
+        return;
     }
     double* o = a.out + (wg * G + g) * m;
 #pragma unroll

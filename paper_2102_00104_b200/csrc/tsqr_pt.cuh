@@ -116,6 +116,14 @@ struct GsArgs {
     double* out;  // stacked factors (T m x m, ld ldo), or R (m x m, ld m) when T == 1
     int64_t ldo;
     ColSplit cs;  // column layout of X (tsqr_gt_kernel only; q = 0: plain)
+    // tsqr_gt_kernel in row chunks (the host entry overlaps the H2D of X with
+    // the sweep): this launch folds slices [sl_lo, sl_hi) (sl_lo a multiple of
+    // the grid's warp count; sl_hi = 0: all), the streams' running R factors
+    // are loaded from `state` first (flag 1) and saved there instead of being
+    // written out (flag 2) — bit-identical to one launch over all slices
+    int64_t sl_lo, sl_hi;
+    double* state;
+    int flags;
 };
 
 #ifndef GS_MINB

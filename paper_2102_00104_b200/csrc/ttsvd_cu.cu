@@ -81,6 +81,9 @@ struct ttsvd_cu_ctx {
     std::vector<DevBuf> ws_slab;  // tt_svd_distributed: two ping-pong work buffers per local slab
     DevBuf host_stage;  // pinned
     DevBuf host_cores;  // pinned arena of the steps' V blocks (core_from_vt after the chain)
+    DevBuf ws_gt_state;  // tsqr_gt_kernel in row chunks: the streams' running R factors between launches
+    cudaStream_t copy_stream = nullptr;  // host entry: H2D of X in row chunks under the first TSQR
+    cudaEvent_t copy_ev = nullptr;
     DevBuf ws_rank;     // K6: per step (rank, sum sigma^2) written by rank_epilogue_kernel
     DevBuf host_sig;    // pinned: per step the sigmas and the K6 record of a speculative chain
     cudaEvent_t ev[9] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
@@ -571,6 +574,42 @@ int tsqr_gt_levels(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t
     TT_TRY(check_launch(ctx, "tsqr_gt_kernel"));
     kmark(ctx, 1, TTSVD_K_GT);
     return tsqr_ws_device(ctx, out, T * m, m, T * m, R, false);
+}
+
+// The same sweep in `chunks` launches over consecutive row ranges (whole
+// rounds of the grid's warps, so every stream folds the same slices in the
+// same order as in one launch: identical bits); before(row_lo, row_hi) runs
+// ahead of each launch — the host entry enqueues that range's H2D there.
+template <int M, int P, int U, class Before>
+int tsqr_gt_chunked(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t ld, double* R, int chunks,
+                    Before before) {
+    constexpr int G = 32 / P, SR = G * U, MC = M / P;
+    const void* fn = (const void*)tsqr_gt_kernel<M, P, U>;
+    TT_TRY(kattr(ctx, fn, (int)gt_smem_bytes<M, P, U>()));
+    const int64_t slices = (n + SR - 1) / SR;
+    const int64_t ctas = std::min<int64_t>(ctx->num_sms, slices / kGtWarps);
+    const int64_t Wt = ctas * kGtWarps, T = Wt * G;
+    TT_TRY(ensure(ctx->ws_gs, (size_t)T * m * m * 8));
+    TT_TRY(ensure(ctx->ws_gt_state, (size_t)Wt * 32 * M * MC * 8));
+    double* out = as<double>(ctx->ws_gs);
+    const int64_t rounds = (slices + Wt - 1) / Wt, rpc = (rounds + chunks - 1) / chunks;
+    kmark(ctx, 0, TTSVD_K_GT);
+    for (int64_t c = 0; c * rpc * Wt < slices; ++c) {
+        const int64_t lo = c * rpc * Wt, hi = std::min(slices, (c + 1) * rpc * Wt);
+        TT_TRY(before(lo * SR, std::min(n, hi * SR)));
+        GsArgs ga{X, n, ld, m, T, out, T * m, ColSplit{0, 0}, lo, hi, as<double>(ctx->ws_gt_state),
+                  (c > 0 ? 1 : 0) | (hi < slices ? 2 : 0)};
+        tsqr_gt_kernel<M, P, U><<<(unsigned)ctas, kPtThreads, gt_smem_bytes<M, P, U>(), ctx->stream>>>(ga);
+        TT_TRY(check_launch(ctx, "tsqr_gt_kernel"));
+    }
+    kmark(ctx, 1, TTSVD_K_GT);
+    return tsqr_ws_device(ctx, out, T * m, m, T * m, R, false);
+}
+
+// tsqr_gs_device dispatches a shape to the TMA-staged kernel under these conditions
+bool gt_eligible(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t ld) {
+    return m > 8 && m <= kSmallM && n >= (int64_t)ctx->num_sms * kGtWarps * 64 * 4 && (ld & 1) == 0 &&
+           ((uintptr_t)X & 15) == 0;
 }
 
 int tsqr_gs_device(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t ld, double* R,
@@ -1224,7 +1263,7 @@ int d2h(ttsvd_cu_ctx* ctx, double* dst, const double* src, size_t count) {
 // kernel cannot, before anything has run).
 int run_chain_impl(ttsvd_cu_ctx* ctx, WorkView cur, const std::vector<int64_t>& dims, int64_t r_max, double eps,
                    int64_t d_for_delta, ttsvd_cu_tt* out, double* delta_io, double* first_sigma_norm_out,
-                   bool spec, ColSplit cs0) {
+                   bool spec, ColSplit cs0, const double* R_first) {
     const int64_t d = (int64_t)dims.size();
     out->dims = dims;
     out->cores.assign(d, {});
@@ -1302,7 +1341,13 @@ int run_chain_impl(ttsvd_cu_ctx* ctx, WorkView cur, const std::vector<int64_t>& 
         if (tall) {
             TT_TRY(ensure(ctx->ws_X, (size_t)m * m * 8));
             double* R = as<double>(ctx->ws_X);
-            TT_TRY(tsqr_device(ctx, cur.data, cur.rows, (int)m, cur.ld, R, nullptr, cs));
+            if (i == d - 1 && R_first) {
+                // the host entry factored the first work matrix while X was arriving
+                if (R_first != R) TT_CUDA(cudaMemcpyAsync(R, R_first, (size_t)m * m * 8, cudaMemcpyDeviceToDevice, ctx->stream));
+                ctx->last_kernel = TTSVD_K_GT;
+            } else {
+                TT_TRY(tsqr_device(ctx, cur.data, cur.rows, (int)m, cur.ld, R, nullptr, cs));
+            }
             tm.mark(1);
             TT_TRY(svd_work(ctx, R, m, m, m, true, false, d_sigma, d_V, &sweeps));
         } else {
@@ -1436,16 +1481,19 @@ int run_chain_impl(ttsvd_cu_ctx* ctx, WorkView cur, const std::vector<int64_t>& 
 
 int run_chain(ttsvd_cu_ctx* ctx, WorkView cur, const std::vector<int64_t>& dims, int64_t r_max, double eps,
               int64_t d_for_delta, ttsvd_cu_tt* out, double* delta_io = nullptr,
-              double* first_sigma_norm_out = nullptr, ColSplit cs0 = ColSplit{0, 0}) {
+              double* first_sigma_norm_out = nullptr, ColSplit cs0 = ColSplit{0, 0},
+              const double* R_first = nullptr) {
     const double delta_in = delta_io ? *delta_io : -1.0;
     // timing reads its events step by step, so a timed chain runs step by step
     const bool spec = !ctx->timing && (delta_in < 0.0 ? eps == 0.0 : delta_in == 0.0);
     if (spec) {
-        const int rc = run_chain_impl(ctx, cur, dims, r_max, eps, d_for_delta, out, delta_io, first_sigma_norm_out, true, cs0);
+        const int rc = run_chain_impl(ctx, cur, dims, r_max, eps, d_for_delta, out, delta_io, first_sigma_norm_out, true, cs0, R_first);
         if (rc != kMispredict) return rc;
         if (delta_io) *delta_io = delta_in;
+        R_first = nullptr;  // its buffer has been reused by the later steps: factor again
     }
-    return run_chain_impl(ctx, cur, dims, r_max, eps, d_for_delta, out, delta_io, first_sigma_norm_out, false, cs0);
+    return run_chain_impl(ctx, cur, dims, r_max, eps, d_for_delta, out, delta_io, first_sigma_norm_out, false, cs0,
+                          R_first);
 }
 
 // tsmm.hpp:84-126 transpose_reorder: Y (out_rows x out_cols, ld ldy) <- the
@@ -1667,6 +1715,9 @@ int ttsvd_cu_ctx_destroy(ttsvd_cu_ctx* ctx) {
     if (ctx->host_stage.p) cudaFreeHost(ctx->host_stage.p);
     if (ctx->host_cores.p) cudaFreeHost(ctx->host_cores.p);
     if (ctx->host_sig.p) cudaFreeHost(ctx->host_sig.p);
+    if (ctx->ws_gt_state.p) cudaFree(ctx->ws_gt_state.p);
+    if (ctx->copy_ev) cudaEventDestroy(ctx->copy_ev);
+    if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
     if (ctx->comm && nccl().ok) nccl().comm_destroy(ctx->comm);
     for (auto& e : ctx->ev)
         if (e) cudaEventDestroy(e);
@@ -1811,8 +1862,25 @@ int ttsvd_cu_tsmm_reshape(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int64_t
     return tsmm_device(ctx, X, n, (int)m, ldx, V, ldv, (int)k, Y, out_rows, out_cols, ldy);
 }
 
+} // extern "C"
+
+namespace {
+int tt_svd_impl(ttsvd_cu_ctx* ctx, const double* X, const int64_t* dims, int64_t d, int64_t ldx, int64_t r_max,
+                double eps, ttsvd_cu_tt** out, const double* R_first);
+}
+
+extern "C" {
+
 int ttsvd_cu_tt_svd(ttsvd_cu_ctx* ctx, const double* X, const int64_t* dims, int64_t d, int64_t ldx, int64_t r_max,
                     double eps, ttsvd_cu_tt** out) {
+    return tt_svd_impl(ctx, X, dims, d, ldx, r_max, eps, out, nullptr);
+}
+
+} // extern "C"
+
+namespace {
+int tt_svd_impl(ttsvd_cu_ctx* ctx, const double* X, const int64_t* dims, int64_t d, int64_t ldx, int64_t r_max,
+                double eps, ttsvd_cu_tt** out, const double* R_first) {
     TT_TRY(set_device(ctx));
     if (!out || !dims || !X) return fail(TTSVD_ERR_INVALID, "tt_svd: null argument");
     *out = nullptr;
@@ -1826,7 +1894,8 @@ int ttsvd_cu_tt_svd(ttsvd_cu_ctx* ctx, const double* X, const int64_t* dims, int
     if (ldx < rows) return fail(TTSVD_ERR_LAYOUT, "tt_svd: leading stride below the row count");
     auto* tt = new ttsvd_cu_tt();
     std::vector<int64_t> dv(dims, dims + d);
-    int rc = run_chain(ctx, WorkView{X, rows, dims[d - 1], ldx}, dv, r_max, eps, d, tt);
+    int rc = run_chain(ctx, WorkView{X, rows, dims[d - 1], ldx}, dv, r_max, eps, d, tt, nullptr, nullptr,
+                       ColSplit{0, 0}, R_first);
     if (rc != TTSVD_OK) {
         delete tt;
         return rc;
@@ -1834,6 +1903,9 @@ int ttsvd_cu_tt_svd(ttsvd_cu_ctx* ctx, const double* X, const int64_t* dims, int
     *out = tt;
     return TTSVD_OK;
 }
+} // namespace
+
+extern "C" {
 
 int ttsvd_cu_run_chain(ttsvd_cu_ctx* ctx, const double* W, int64_t rows, int64_t cols, int64_t ldw, const int64_t* dims,
                        int64_t d, int64_t r_max, double eps, int64_t d_for_delta, double* delta_io,
@@ -2035,8 +2107,39 @@ int ttsvd_cu_tt_svd_host(ttsvd_cu_ctx* ctx, const double* X_host, const int64_t*
     const size_t bytes = (size_t)ldx * dims[d - 1] * 8;
     (void)total;
     TT_TRY(ensure(ctx->ws_recv, bytes));
-    TT_CUDA(cudaMemcpyAsync(ctx->ws_recv.p, X_host, bytes, cudaMemcpyHostToDevice, ctx->stream));
-    return ttsvd_cu_tt_svd(ctx, as<double>(ctx->ws_recv), dims, d, ldx, r_max, eps, out);
+    double* dX = as<double>(ctx->ws_recv);
+    const int64_t rows = d >= 2 && dims[d - 1] > 0 ? total / dims[d - 1] : 0;
+    const int m1 = (int)dims[d - 1];
+    // First step on the TMA-staged stream kernel and tall enough: X arrives
+    // in row chunks on a second stream and every chunk is folded as soon as it
+    // has landed (the streams' running factors carried between the launches),
+    // so the first TSQR hides under the H2D.  Same bits as the device entry.
+    if (d >= 2 && ldx >= rows && gt_eligible(ctx, dX, rows, m1, ldx) &&
+        rows >= (int64_t)ctx->num_sms * kGtWarps * 64 * 8 && !ctx->timing) {
+        if (!ctx->copy_stream) {
+            TT_CUDA(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+            TT_CUDA(cudaEventCreateWithFlags(&ctx->copy_ev, cudaEventDisableTiming));
+        }
+        TT_TRY(ensure(ctx->ws_X, (size_t)m1 * m1 * 8));
+        double* R = as<double>(ctx->ws_X);
+        // the copies must not overtake earlier work on the context's stream that still reads the buffer
+        TT_CUDA(cudaEventRecord(ctx->copy_ev, ctx->stream));
+        TT_CUDA(cudaStreamWaitEvent(ctx->copy_stream, ctx->copy_ev, 0));
+        auto before = [&](int64_t r_lo, int64_t r_hi) -> int {
+            TT_CUDA(cudaMemcpy2DAsync(dX + r_lo, (size_t)ldx * 8, X_host + r_lo, (size_t)ldx * 8, (size_t)(r_hi - r_lo) * 8,
+                                      (size_t)m1, cudaMemcpyHostToDevice, ctx->copy_stream));
+            TT_CUDA(cudaEventRecord(ctx->copy_ev, ctx->copy_stream));
+            TT_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->copy_ev, 0));
+            return TTSVD_OK;
+        };
+        int rc_q;
+        if (m1 <= 16) rc_q = tsqr_gt_chunked<16, 4, 8>(ctx, dX, rows, m1, ldx, R, 8, before);
+        else rc_q = tsqr_gt_chunked<32, 8, 8>(ctx, dX, rows, m1, ldx, R, 8, before);
+        if (rc_q != TTSVD_OK) return rc_q;
+        return tt_svd_impl(ctx, dX, dims, d, ldx, r_max, eps, out, R);
+    }
+    TT_CUDA(cudaMemcpyAsync(dX, X_host, bytes, cudaMemcpyHostToDevice, ctx->stream));
+    return ttsvd_cu_tt_svd(ctx, dX, dims, d, ldx, r_max, eps, out);
 }
 
 int ttsvd_cu_tt_svd_distributed(ttsvd_cu_ctx* ctx, const double* const* slabs, int64_t n_slabs, int64_t part0,

@@ -185,6 +185,28 @@ def test_host_entry_matches_device_entry(tt, orc):
         assert np.array_equal(ca.data, cb.data)
 
 
+def test_host_entry_chunked_h2d_matches_device_entry(tt, orc):
+    # a first step on the TMA-staged stream kernel (2^20 x 16): the host entry
+    # copies X in row chunks under the first TSQR (running factors carried
+    # between the chunk launches) — same bytes out as the device entry
+    import torch
+    dims = [16] * 6
+    X = orc.gen_uniform(13, dims)
+    a = tt.tt_svd_tsqr(X, dims, (8, 0.0))
+    Xd = torch.from_numpy(np.ascontiguousarray(X.T)).cuda().t()
+    rows = int(np.prod(dims)) // dims[-1]
+    b = tt.tt_svd_tsqr(Xd[:rows], dims, tt.TruncationSpec(r_max=8))
+    assert a.ranks() == b.ranks()
+    for ca, cb in zip(a.cores, b.cores):
+        assert np.array_equal(ca.data, cb.data)
+    for sa, sb in zip(a.sigmas, b.sigmas):
+        assert np.array_equal(sa, sb)
+    # and again (the chunk state buffer is reused)
+    c = tt.tt_svd_tsqr(X, dims, (8, 0.0))
+    for ca, cc in zip(a.cores, c.cores):
+        assert np.array_equal(ca.data, cc.data)
+
+
 def test_zero_tensor(tt, orc):
     dims = [3, 4, 5]
     X = np.zeros((64, 5), order="F")
