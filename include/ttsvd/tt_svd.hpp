@@ -360,15 +360,16 @@ inline TensorTrain tt_svd_thick_bounds(const DenseTensor& X, TruncationSpec spec
                                        const ExecContext& ctx = {}) {
     const index_t d = X.shape().d();
     if (d < 2) throw DegenerateDimension("tt_svd_thick_bounds: requires d >= 2");
-    const b200::DeviceBuffer dx = b200::stage(X);
     ttsvd_cu_ctx* c = b200::context();
     b200::Result res;
     {
+        // the host-buffer entry: X goes H2D inside the call (in row chunks
+        // under the merged first TSQR where its shape allows)
         b200::TimingScope t(c, ctx.recorder != nullptr);
-        b200::check(ttsvd_cu_tt_svd_thick(c, dx.get(), X.shape().dims().data(), d, X.leading_stride(), spec.r_max,
-                                          spec.eps, params.m_min, params.f1_min,
-                                          params.r_tilde.empty() ? nullptr : params.r_tilde.data(),
-                                          static_cast<index_t>(params.r_tilde.size()), res.out()));
+        b200::check(ttsvd_cu_tt_svd_thick_host(c, X.data(), X.shape().dims().data(), d, X.leading_stride(), spec.r_max,
+                                               spec.eps, params.m_min, params.f1_min,
+                                               params.r_tilde.empty() ? nullptr : params.r_tilde.data(),
+                                               static_cast<index_t>(params.r_tilde.size()), res.out()));
     }
     b200::account(res, ctx);
     TensorTrain tt = res.train(X.shape().dims());

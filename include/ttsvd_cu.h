@@ -168,10 +168,25 @@ int ttsvd_cu_choose_combined_dims(const int64_t* dims, int64_t d, int64_t m_min,
 int ttsvd_cu_tt_svd_thick(ttsvd_cu_ctx* ctx, const double* X, const int64_t* dims, int64_t d, int64_t ldx,
                           int64_t r_max, double eps, int64_t m_min, double f1_min, const int64_t* r_tilde,
                           int64_t n_r_tilde, ttsvd_cu_tt** out);
-/* Same, from a HOST buffer (pinned or pageable): the H2D copy is part of the
- * call — this is the reference-facing end-to-end entry. */
+/* ttsvd_cu_tt_svd from a HOST buffer (pinned or pageable, the same padded
+ * layout): the H2D copy is part of the call — this is the reference-facing
+ * end-to-end entry (tt_svd_tsqr(const DenseTensor&), tt_svd.hpp:281-290).
+ * When the first step runs on the TMA-staged stream kernel, X is copied in
+ * row chunks on a second stream and every chunk is folded as soon as it has
+ * landed, so the first TSQR runs under the transfer; the result is
+ * bit-identical to ttsvd_cu_tt_svd on the uploaded tensor. */
 int ttsvd_cu_tt_svd_host(ttsvd_cu_ctx* ctx, const double* X_host, const int64_t* dims, int64_t d, int64_t ldx,
                          int64_t r_max, double eps, ttsvd_cu_tt** out);
+/* ttsvd_cu_tt_svd_thick from a HOST buffer (tt_svd_thick_bounds(const
+ * DenseTensor&), tt_svd.hpp:338).  When the merged first step runs on the
+ * tall-tile kernel, X arrives in row chunks of the merged matricization and
+ * each chunk is folded as it lands (per-CTA factors carried between the
+ * launches): the dominant TSQR of Alg. 3 runs under the H2D.  Same algorithm
+ * as the device entry with other tile boundaries: equal within rounding, not
+ * bit for bit. */
+int ttsvd_cu_tt_svd_thick_host(ttsvd_cu_ctx* ctx, const double* X_host, const int64_t* dims, int64_t d, int64_t ldx,
+                               int64_t r_max, double eps, int64_t m_min, double f1_min, const int64_t* r_tilde,
+                               int64_t n_r_tilde, ttsvd_cu_tt** out);
 /* tt_svd.hpp:520 tt_svd_distributed() (Alg. 5).  This process owns n_slabs
  * slabs (device pointers, each the padded layout of the local shape ldims,
  * leading stride ld_slab) which are global partitions part0 .. part0+n_slabs-1

@@ -63,6 +63,8 @@ _SIGS = {
     "ttsvd_cu_choose_combined_dims": (C.c_int, [i64p, i64, i64, C.c_double, C.c_void_p, i64, i64, i64p, i64p]),
     "ttsvd_cu_tt_svd_thick": (C.c_int, [C.c_void_p, C.c_void_p, i64p, i64, i64, i64, C.c_double, i64, C.c_double,
                                         C.c_void_p, i64, C.POINTER(C.c_void_p)]),
+    "ttsvd_cu_tt_svd_thick_host": (C.c_int, [C.c_void_p, C.c_void_p, i64p, i64, i64, i64, C.c_double, i64, C.c_double,
+                                             C.c_void_p, i64, C.POINTER(C.c_void_p)]),
     "ttsvd_cu_tt_svd_host": (C.c_int, [C.c_void_p, dptr, i64p, i64, i64, i64, C.c_double, C.POINTER(C.c_void_p)]),
     "ttsvd_cu_tt_svd_distributed": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p), i64, i64, i64, i64p, i64, i64, i64,
                                               C.c_double, EXCHANGE_FN, C.c_void_p, C.POINTER(C.c_void_p)]),

@@ -39,6 +39,12 @@ struct T2Args {
     int m, M;
     long long* prof;  // optional per-CTA phase cycle counters (8 per CTA), diagnostics
     ColSplit cs;      // column layout of X (q = 0: plain)
+    // row chunks (the thick-bounds host entry folds X as it arrives): this
+    // launch factors rows [n_lo, n_hi) (n_hi = 0: all rows), split over the
+    // CTAs as usual; keep != 0: the per-CTA factors continue from the previous
+    // launch instead of starting at zero
+    int64_t n_lo, n_hi;
+    int keep;
 };
 
 inline size_t t2_smem_bytes(int rows = kT2Rows) {
@@ -392,14 +398,16 @@ __global__ void __launch_bounds__(kT2Threads, 1) tsqr_t128_kernel(T2Args a) {
     double* dpart = pvall + PW * 32;           // 2 x PW x 32 partial dots
 
     const int64_t job = blockIdx.x, G = gridDim.x;
-    const int64_t base = a.n / G, rem = a.n % G;
-    const int64_t row0 = job * base + (job < rem ? job : rem);
+    const int64_t n_end = a.n_hi > 0 ? a.n_hi : a.n, n_len = n_end - a.n_lo;
+    const int64_t base = n_len / G, rem = n_len % G;
+    const int64_t row0 = a.n_lo + job * base + (job < rem ? job : rem);
     const int64_t row1 = row0 + base + (job < rem ? 1 : 0);
     const int64_t RS = blk_rsize(M);
     double* R = a.Rws + job * RS;
     double* Scr = a.Scr + job * (int64_t)ROWS * M;
     const uint64_t pol_x = l2_policy_evict_first(), pol_r = l2_policy_evict_last();
-    for (int64_t e = tid; e < RS; e += kT2Threads) st_hint(R + e, 0.0, pol_r);
+    if (!a.keep)
+        for (int64_t e = tid; e < RS; e += kT2Threads) st_hint(R + e, 0.0, pol_r);
     __syncthreads();
     const int npan = M / 32;
     const bool panel_warp = warp < PW;

@@ -649,6 +649,54 @@ int tsqr_sq_levels(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t
     }
 }
 
+// Tall tiles (tsqr_t128_kernel, one CTA per SM) + one cooperative QR of the
+// 148 stacked factors.  chunk_rows > 0: the sweep runs in launches over
+// consecutive row ranges, the per-CTA factors carried from launch to launch;
+// before(row_lo, row_hi) runs ahead of each launch (the thick-bounds host
+// entry enqueues that range's H2D there).
+template <class Before>
+int tsqr_t128_run(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t ld, double* R, ColSplit cs,
+                  int64_t chunk_rows, Before before) {
+    const int M = (m + 31) / 32 * 32;
+    const int64_t RS = blk_rsize(M);
+    // 256-row tiles (8 panel + 8 update warps of a 512-thread CTA): the
+    // reflector chain per row is half the 128-row tile's (config 2 step 2
+    // sweep: 13.7 ms at 128 rows / 384 threads, 12.35 at 192 / 384, 11.8
+    // at 256 / 512; 12.8 at 320 / 512).
+    const int t2rows = n >= (int64_t)ctx->num_sms * 4 * 256 ? 256 : 128;
+    const int64_t Gt = ctx->num_sms;
+    TT_TRY(ensure(ctx->ws_R, (size_t)Gt * RS * 8));
+    TT_TRY(ensure(ctx->ws_Scr, (size_t)Gt * t2rows * M * 8));
+    double* parts = as<double>(ctx->ws_R);
+    const void* tfn = t2rows == 256 ? (const void*)tsqr_t128_kernel<256> : (const void*)tsqr_t128_kernel<128>;
+    TT_TRY(kattr(ctx, tfn, (int)t2_smem_bytes(t2rows)));
+    kmark(ctx, 0, TTSVD_K_T128);
+    const int64_t step = chunk_rows > 0 ? chunk_rows : n;
+    for (int64_t lo = 0; lo < n; lo += step) {
+        const int64_t hi = std::min(n, lo + step);
+        TT_TRY(before(lo, hi));
+        T2Args ta{X, n, ld, parts, as<double>(ctx->ws_Scr), m, M, nullptr, cs, lo, hi, lo > 0 ? 1 : 0};
+        if (t2rows == 256)
+            tsqr_t128_kernel<256><<<(unsigned)Gt, kT2Threads, t2_smem_bytes(256), ctx->stream>>>(ta);
+        else
+            tsqr_t128_kernel<128><<<(unsigned)Gt, kT2Threads, t2_smem_bytes(128), ctx->stream>>>(ta);
+        TT_TRY(check_launch(ctx, "tsqr_t128_kernel"));
+    }
+    kmark(ctx, 1, TTSVD_K_T128);
+    const int rc = merge_stack_gqr(ctx, parts, Gt, m, M, R);
+    if (rc != -1) return rc;
+    TT_TRY(ensure(ctx->ws_P, (size_t)RS * 8));
+    TT_TRY(merge_tree_blk(ctx, parts, Gt, m, M, as<double>(ctx->ws_P)));
+    return copy_leading(ctx, as<double>(ctx->ws_P), M, m, R);
+}
+
+// the shapes tsqr_device sends to tsqr_t128_run
+bool t128_eligible(ttsvd_cu_ctx* ctx, int64_t n, int m) {
+    const int M = (m + 31) / 32 * 32;
+    return m > kSmallM && !(m <= 64 && n <= kSqMaxRows) && !(n >= M && n <= (int64_t)256 * M) &&
+           n >= (int64_t)ctx->num_sms * 4 * kT2Rows;
+}
+
 int tsqr_device(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t ld, double* R,
                 const double* R_init = nullptr, ColSplit cs = ColSplit{0, 0}) {
     ctx->last_kernel = TTSVD_K_NONE;
@@ -680,28 +728,8 @@ int tsqr_device(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t ld
         // reflector chain per row is half the 128-row tile's (config 2 step 2
         // sweep: 13.7 ms at 128 rows / 384 threads, 12.35 at 192 / 384, 11.8
         // at 256 / 512; 12.8 at 320 / 512).
-        const int t2rows = n >= (int64_t)ctx->num_sms * 4 * 256 ? 256 : 128;
-        if (!R_init && n >= (int64_t)ctx->num_sms * 4 * kT2Rows) {
-            const int64_t Gt = ctx->num_sms;
-            TT_TRY(ensure(ctx->ws_R, (size_t)Gt * RS * 8));
-            TT_TRY(ensure(ctx->ws_Scr, (size_t)Gt * t2rows * M * 8));
-            double* parts = as<double>(ctx->ws_R);
-            const void* tfn = t2rows == 256 ? (const void*)tsqr_t128_kernel<256> : (const void*)tsqr_t128_kernel<128>;
-            TT_TRY(kattr(ctx, tfn, (int)t2_smem_bytes(t2rows)));
-            T2Args ta{X, n, ld, parts, as<double>(ctx->ws_Scr), m, M, nullptr, cs};
-            kmark(ctx, 0, TTSVD_K_T128);
-            if (t2rows == 256)
-                tsqr_t128_kernel<256><<<(unsigned)Gt, kT2Threads, t2_smem_bytes(256), ctx->stream>>>(ta);
-            else
-                tsqr_t128_kernel<128><<<(unsigned)Gt, kT2Threads, t2_smem_bytes(128), ctx->stream>>>(ta);
-            TT_TRY(check_launch(ctx, "tsqr_t128_kernel"));
-            kmark(ctx, 1, TTSVD_K_T128);
-            const int rc = merge_stack_gqr(ctx, parts, Gt, m, M, R);
-            if (rc != -1) return rc;
-            TT_TRY(ensure(ctx->ws_P, (size_t)RS * 8));
-            TT_TRY(merge_tree_blk(ctx, parts, Gt, m, M, as<double>(ctx->ws_P)));
-            return copy_leading(ctx, as<double>(ctx->ws_P), M, m, R);
-        }
+        if (!R_init && n >= (int64_t)ctx->num_sms * 4 * kT2Rows)
+            return tsqr_t128_run(ctx, X, n, m, ld, R, cs, 0, [](int64_t, int64_t) { return TTSVD_OK; });
         int per_sm = 1;
         TT_TRY(set_la_attr(ctx));
         TT_TRY(koccupancy(ctx, (const void*)tsqr_la_kernel, kLaThreads, la_smem_bytes(M), &per_sm));
@@ -1999,9 +2027,17 @@ int ttsvd_cu_choose_combined_dims(const int64_t* dims, int64_t d, int64_t m_min,
     return TTSVD_OK;
 }
 
-int ttsvd_cu_tt_svd_thick(ttsvd_cu_ctx* ctx, const double* X, const int64_t* dims, int64_t d, int64_t ldx,
-                          int64_t r_max, double eps, int64_t m_min, double f1_min, const int64_t* r_tilde,
-                          int64_t n_r_tilde, ttsvd_cu_tt** out) {
+} // extern "C"
+
+namespace {
+// X: device tensor (padded layout).  X_host != nullptr: X is still empty and
+// the tensor is at X_host (same layout): when the merged first step runs on
+// the tall-tile kernel, X arrives in row chunks of the merged matricization
+// on a second stream and tsqr_t128 folds every chunk as soon as it has landed
+// (the first TSQR under the H2D); otherwise it is copied whole first.
+int thick_impl(ttsvd_cu_ctx* ctx, const double* X, const double* X_host, const int64_t* dims, int64_t d, int64_t ldx,
+               int64_t r_max, double eps, int64_t m_min, double f1_min, const int64_t* r_tilde, int64_t n_r_tilde,
+               ttsvd_cu_tt** out) {
     TT_TRY(set_device(ctx));
     if (!out || !dims || !X) return fail(TTSVD_ERR_INVALID, "tt_svd_thick: null argument");
     *out = nullptr;
@@ -2015,7 +2051,10 @@ int ttsvd_cu_tt_svd_thick(ttsvd_cu_ctx* ctx, const double* X, const int64_t* dim
     if (ldx < rows0) return fail(TTSVD_ERR_LAYOUT, "tt_svd_thick: leading stride below the row count");
     int64_t k = 1, m = dims[d - 1];
     TT_TRY(ttsvd_cu_choose_combined_dims(dims, d, m_min, f1_min, r_tilde, n_r_tilde, r_max, &k, &m));
-    if (k == 1) return ttsvd_cu_tt_svd(ctx, X, dims, d, ldx, r_max, eps, out);
+    if (k == 1) {
+        if (X_host) return ttsvd_cu_tt_svd_host(ctx, X_host, dims, d, ldx, r_max, eps, out);
+        return ttsvd_cu_tt_svd(ctx, X, dims, d, ldx, r_max, eps, out);
+    }
 
     // merged tensor (n_1, ..., n_{d-k}, m): column x of its matricization is the
     // contiguous run of X's column x / q starting at row (x mod q) (N/m),
@@ -2029,8 +2068,40 @@ int ttsvd_cu_tt_svd_thick(ttsvd_cu_ctx* ctx, const double* X, const int64_t* dim
     const int64_t dm = (int64_t)mdims.size();
     ttsvd_cu_tt main_tt;
     double delta = -1.0, fsn = 0.0;
+    const double* R_first = nullptr;
+    if (X_host) {
+        double* dX = const_cast<double*>(X);
+        const int64_t unit = (int64_t)ctx->num_sms * 256;  // a 256-row tile per CTA
+        if (t128_eligible(ctx, rows_m, (int)m) && rows_m >= 8 * unit && !ctx->timing) {
+            if (!ctx->copy_stream) {
+                TT_CUDA(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+                TT_CUDA(cudaEventCreateWithFlags(&ctx->copy_ev, cudaEventDisableTiming));
+            }
+            TT_TRY(ensure(ctx->ws_X, (size_t)m * m * 8));
+            double* R = as<double>(ctx->ws_X);
+            TT_CUDA(cudaEventRecord(ctx->copy_ev, ctx->stream));
+            TT_CUDA(cudaStreamWaitEvent(ctx->copy_stream, ctx->copy_ev, 0));
+            const int64_t n_d = dims[d - 1];
+            auto before = [&](int64_t r_lo, int64_t r_hi) -> int {
+                // rows [r_lo, r_hi) of the merged matricization: q runs in each of X's n_d columns
+                for (int64_t id = 0; id < n_d; ++id)
+                    TT_CUDA(cudaMemcpy2DAsync(dX + id * ldx + r_lo, (size_t)rows_m * 8, X_host + id * ldx + r_lo,
+                                              (size_t)rows_m * 8, (size_t)(r_hi - r_lo) * 8, (size_t)q,
+                                              cudaMemcpyHostToDevice, ctx->copy_stream));
+                TT_CUDA(cudaEventRecord(ctx->copy_ev, ctx->copy_stream));
+                TT_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->copy_ev, 0));
+                return TTSVD_OK;
+            };
+            const int64_t chunk = std::max<int64_t>(1, rows_m / (8 * unit)) * unit;
+            const int rc_q = tsqr_t128_run(ctx, dX, rows_m, (int)m, ldx, R, ColSplit{(int)q, rows_m}, chunk, before);
+            if (rc_q != TTSVD_OK) return rc_q;
+            R_first = R;
+        } else {
+            TT_CUDA(cudaMemcpyAsync(dX, X_host, (size_t)ldx * dims[d - 1] * 8, cudaMemcpyHostToDevice, ctx->stream));
+        }
+    }
     int rc_main = run_chain(ctx, WorkView{X, rows_m, m, ldx}, mdims, r_max, eps, dm, &main_tt, &delta, &fsn,
-                            ColSplit{(int)q, rows_m});
+                            ColSplit{(int)q, rows_m}, R_first);
     if (rc_main == kNoView) {
         const int64_t ldm = padded_stride_h(rows_m);
         TT_TRY(ensure(ctx->ws_thick[0], (size_t)ldm * m * 8));
@@ -2096,6 +2167,27 @@ int ttsvd_cu_tt_svd_thick(ttsvd_cu_ctx* ctx, const double* X, const int64_t* dim
     tt->sigmas.insert(tt->sigmas.end(), rec_tt.sigmas.begin(), rec_tt.sigmas.end());
     *out = tt;
     return TTSVD_OK;
+}
+} // namespace
+
+extern "C" {
+
+int ttsvd_cu_tt_svd_thick(ttsvd_cu_ctx* ctx, const double* X, const int64_t* dims, int64_t d, int64_t ldx,
+                          int64_t r_max, double eps, int64_t m_min, double f1_min, const int64_t* r_tilde,
+                          int64_t n_r_tilde, ttsvd_cu_tt** out) {
+    return thick_impl(ctx, X, nullptr, dims, d, ldx, r_max, eps, m_min, f1_min, r_tilde, n_r_tilde, out);
+}
+
+int ttsvd_cu_tt_svd_thick_host(ttsvd_cu_ctx* ctx, const double* X_host, const int64_t* dims, int64_t d, int64_t ldx,
+                               int64_t r_max, double eps, int64_t m_min, double f1_min, const int64_t* r_tilde,
+                               int64_t n_r_tilde, ttsvd_cu_tt** out) {
+    TT_TRY(set_device(ctx));
+    if (!X_host || !dims || d < 1) return fail(TTSVD_ERR_INVALID, "tt_svd_thick_host: null argument");
+    for (int64_t i = 0; i < d; ++i)
+        if (dims[i] < 1) return fail(TTSVD_ERR_DIMENSION, "Shape: extents must be >= 1");
+    TT_TRY(ensure(ctx->ws_recv, (size_t)ldx * dims[d - 1] * 8));
+    return thick_impl(ctx, as<double>(ctx->ws_recv), X_host, dims, d, ldx, r_max, eps, m_min, f1_min, r_tilde,
+                      n_r_tilde, out);
 }
 
 int ttsvd_cu_tt_svd_host(ttsvd_cu_ctx* ctx, const double* X_host, const int64_t* dims, int64_t d, int64_t ldx,

@@ -584,7 +584,9 @@ def choose_combined_dims(dims, params: ThickBoundsParams | None = None, r_max: i
 def tt_svd_thick_bounds(X, dims, spec: TruncationSpec | tuple | None = None,
                         params: ThickBoundsParams | None = None) -> TensorTrain:
     """tt_svd.hpp:338 (Alg. 3) on a device tensor in the padded layout (as
-    tt_svd_tsqr; host numpy buffers are staged to the device first)."""
+    tt_svd_tsqr), or on a host numpy buffer of shape (ld, n_d) in Fortran
+    order (copied H2D inside the call, in row chunks under the merged first
+    TSQR where its shape allows: ttsvd_cu_tt_svd_thick_host)."""
     spec = _spec(spec)
     params = params or ThickBoundsParams()
     dims = [int(x) for x in dims]
@@ -592,15 +594,24 @@ def tt_svd_thick_bounds(X, dims, spec: TruncationSpec | tuple | None = None,
     if d < 2:
         raise DegenerateDimension("tt_svd_thick_bounds: requires d >= 2")
     r_max = int(spec.r_max)
-    X = to_device_matrix(X)
     dv = np.asarray(dims, dtype=np.int64)
     rt = np.asarray(params.r_tilde, dtype=np.int64)
-    ctx = context(X.device.index)
-    p, rows, cols, ld = _mat(X)
     h = C.c_void_p()
-    _check(_lib.lib().ttsvd_cu_tt_svd_thick(ctx.handle, p, dv.ctypes.data_as(_lib.i64p), d, ld, r_max,
-                                            float(spec.eps), int(params.m_min), float(params.f1_min),
-                                            rt.ctypes.data if len(rt) else None, len(rt), C.byref(h)))
+    if isinstance(X, torch.Tensor) and X.is_cuda:
+        ctx = context(X.device.index)
+        p, rows, cols, ld = _mat(X)
+        _check(_lib.lib().ttsvd_cu_tt_svd_thick(ctx.handle, p, dv.ctypes.data_as(_lib.i64p), d, ld, r_max,
+                                                float(spec.eps), int(params.m_min), float(params.f1_min),
+                                                rt.ctypes.data if len(rt) else None, len(rt), C.byref(h)))
+    else:
+        a = np.asarray(X, dtype=np.float64)
+        if not a.flags.f_contiguous:
+            a = np.asfortranarray(a)
+        ctx = context()
+        _check(_lib.lib().ttsvd_cu_tt_svd_thick_host(ctx.handle, a.ctypes.data, dv.ctypes.data_as(_lib.i64p), d,
+                                                     a.shape[0], r_max, float(spec.eps), int(params.m_min),
+                                                     float(params.f1_min), rt.ctypes.data if len(rt) else None,
+                                                     len(rt), C.byref(h)))
     return _finish(h, dims)
 
 

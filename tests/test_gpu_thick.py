@@ -125,3 +125,30 @@ def test_thick_view_in_place(tt, orc, ref, dims, r_max, m_min, expect_km, tt_ran
         # no copy of X (8 prod(dims) bytes) was allocated next to it (the
         # device copy of X itself is; the work buffers are a fraction of it)
         assert free0 - free1 < 2 * 8 * int(np.prod(dims)) - (8 * int(np.prod(dims))) // 4
+
+
+def test_thick_host_entry_chunked_h2d(tt, ref):
+    # host buffer in: X arrives in row chunks of the merged matricization
+    # (2^19 x 64) and tsqr_t128 folds each chunk as it lands; same parity bar
+    # against the reference's tt_svd_thick_bounds, and agreement with the
+    # device entry within rounding (other tile boundaries, not bit for bit)
+    import torch
+    from oracle.oracle import random_tt, tt_reconstruct
+    dims = [2] * 25
+    d = len(dims)
+    ranks = [min(12, 2 ** min(j, d - j)) for j in range(d + 1)]
+    X = tt_reconstruct(random_tt(dims, ranks, 81), dims)
+    rng = np.random.default_rng(82)
+    X = np.asfortranarray(X + 1e-8 * np.linalg.norm(X) / np.sqrt(X.size) * rng.standard_normal(X.shape))
+    p = tt.ThickBoundsParams(m_min=64)
+    assert tt.choose_combined_dims(dims, p, 12) == (6, 64)
+    Th = tt.tt_svd_thick_bounds(X, dims, tt.TruncationSpec(r_max=12), p)          # host entry
+    Xd = torch.from_numpy(np.ascontiguousarray(X.T)).cuda().t()
+    rows = int(np.prod(dims)) // dims[-1]
+    Td = tt.tt_svd_thick_bounds(Xd[:rows], dims, tt.TruncationSpec(r_max=12), p)  # device entry
+    r, cores = ref.tt_svd_thick_bounds(X, dims, X.shape[0], 12, 0.0, 64, 0.5, ())
+    check(ref, X, dims, Th, r, cores, err_tol=1e-8)
+    assert Th.ranks() == Td.ranks()
+    for sh, sd in zip(Th.sigmas, Td.sigmas):
+        assert np.max(np.abs(sh - sd)) <= 1e-10 * sd[0]
+    assert max(frame_angles([c.data for c in Th.cores], [c.data for c in Td.cores])) <= 1e-8
