@@ -1302,7 +1302,16 @@ int run_chain_impl(ttsvd_cu_ctx* ctx, WorkView cur, const std::vector<int64_t>& 
     struct SpecStep {
         size_t off;  // of the step's record in host_sig (doubles): nsig sigmas, then (rank, sum sigma^2)
         int64_t nsig, pred;
+        size_t step;  // index into out->steps / out->sigmas
     };
+    // Which steps run ahead of their rank: only those whose prediction is the
+    // cap r_max, and only once a step checked on the host has reached the cap
+    // (a train that saturates r_max at one unfolding does so at the next);
+    // while the ranks still grow with the matrix, and after any checked step
+    // came out below its prediction (a rank-deficient tensor), the step waits
+    // for its sigmas as before.  A speculated step that misses still costs a
+    // rerun of the chain.
+    bool trust = false;
     std::vector<SpecStep> spec_steps;
     size_t spec_off = 0;
     if (spec) {
@@ -1386,15 +1395,16 @@ int run_chain_impl(ttsvd_cu_ctx* ctx, WorkView cur, const std::vector<int64_t>& 
         tm.mark(2);
         sig.resize(nsig);
         int64_t rnew;
-        if (spec) {
+        const int64_t pred = predicted_rank_h(nsig, nsig, r_max);
+        if (spec && trust && pred == r_max) {
             double* rec = as<double>(ctx->ws_rank) + 2 * (size_t)spec_steps.size();
             rank_epilogue_kernel<<<1, 32, 0, ctx->stream>>>(d_sigma, nsig, cur.cols, nsig, delta, r_max, cur.rows, rec);
             TT_TRY(check_launch(ctx, "rank_epilogue_kernel"));
             double* hs = as<double>(ctx->host_sig) + spec_off;
             TT_CUDA(cudaMemcpyAsync(hs, d_sigma, (size_t)nsig * 8, cudaMemcpyDeviceToHost, ctx->stream));
             TT_CUDA(cudaMemcpyAsync(hs + nsig, rec, 16, cudaMemcpyDeviceToHost, ctx->stream));
-            rnew = predicted_rank_h(nsig, nsig, r_max);
-            spec_steps.push_back(SpecStep{spec_off, nsig, rnew});
+            rnew = pred;
+            spec_steps.push_back(SpecStep{spec_off, nsig, rnew, out->steps.size()});
             spec_off += (size_t)nsig + 2;
         } else {
             TT_TRY(d2h(ctx, sig.data(), d_sigma, nsig));
@@ -1405,6 +1415,8 @@ int run_chain_impl(ttsvd_cu_ctx* ctx, WorkView cur, const std::vector<int64_t>& 
                 if (delta_io) *delta_io = delta;
             }
             rnew = choose_rank_h(sig.data(), nsig, cur.cols, nsig, delta, r_max, cur.rows);
+            if (rnew < pred) spec = false;             // rank-deficient: no more running ahead
+            else if (pred == r_max) trust = true;      // the cap is reached
         }
         st.nsig = nsig;
         st.rank = rnew;
@@ -1484,21 +1496,19 @@ int run_chain_impl(ttsvd_cu_ctx* ctx, WorkView cur, const std::vector<int64_t>& 
         }
     }
     TT_CUDA(cudaStreamSynchronize(ctx->stream));
-    if (spec) {
-        // the device's ranks against the predictions the chain ran with
+    if (!spec_steps.empty()) {
+        // the device's ranks against the predictions those steps ran with
         const double* base = as<double>(ctx->host_sig);
-        for (size_t k = 0; k < spec_steps.size(); ++k) {
-            const SpecStep& ss = spec_steps[k];
+        for (const SpecStep& ss : spec_steps) {
             const double* hs = base + ss.off;
             if ((int64_t)hs[ss.nsig] != ss.pred) {
                 pending.clear();
                 return kMispredict;
             }
-            out->sigmas[k].assign(hs, hs + ss.nsig);
-            if (k == 0 && first_sigma_norm_out) *first_sigma_norm_out = std::sqrt(hs[ss.nsig + 1]);
+            out->sigmas[ss.step].assign(hs, hs + ss.nsig);
         }
-        if (delta_io) *delta_io = delta;
     }
+    if (delta_io && delta >= 0.0) *delta_io = delta;
     flush_cores();
     out->cores[0] = std::move(first);
     out->ranks[0] = 1;
