@@ -41,13 +41,7 @@ int main() {
     cudaMalloc(&X, (size_t)n16 * 16 * 8);
     cudaMalloc(&out, (size_t)148 * 2 * 8 * 32 * 32 * 32 * 8);
     fill<<<1184, 256>>>(X, (size_t)n16 * 16);
-    run<16, 4, 8, 1, 3>(X, n16, 16, out);
     run<16, 4, 8, 1, 2>(X, n16, 16, out);
-    run<16, 2, 4, 1, 2>(X, n16, 16, out);
-    run<16, 4, 4, 2, 2>(X, n16, 16, out);
-    run<16, 8, 8, 2, 3>(X, n16, 16, out);
-    run<32, 8, 8, 1, 3>(X, n32, 32, out);
-    run<32, 8, 4, 1, 3>(X, n32, 32, out);
-    run<32, 16, 8, 2, 3>(X, n32, 32, out);
+    run<32, 8, 8, 1, 2>(X, n32, 32, out);
     return 0;
 }
