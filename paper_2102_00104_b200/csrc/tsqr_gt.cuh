@@ -27,11 +27,12 @@
 namespace ttsvd_b200 {
 
 constexpr int kGtStages = 2;
-constexpr int kGtWarps = kPtThreads / 32;
 
-template <int M, int P, int U, int ST = kGtStages>
+// NTH: threads per CTA (8 warps; 12 for m <= 16, where a third warp per
+// scheduler gains more than the 168-register cap's spills cost)
+template <int M, int P, int U, int ST = kGtStages, int NTH = kPtThreads>
 constexpr size_t gt_smem_bytes() {
-    return (size_t)kGtWarps * ST * M * ((32 / P) * U + 32 / P) * sizeof(double);
+    return (size_t)(NTH / 32) * ST * M * ((32 / P) * U + 32 / P) * sizeof(double);
 }
 
 __device__ __forceinline__ void gt_mbar_init(unsigned bar, unsigned count) {
@@ -54,8 +55,9 @@ __device__ __forceinline__ void gt_bulk_g2s(unsigned dst, const void* src, unsig
                  : "memory");
 }
 
-template <int M, int P, int U, int MB = 1, int ST = kGtStages>
-__global__ void __launch_bounds__(kPtThreads, MB) tsqr_gt_kernel(GsArgs a) {
+template <int M, int P, int U, int MB = 1, int ST = kGtStages, int NTH = kPtThreads>
+__global__ void __launch_bounds__(NTH, MB) tsqr_gt_kernel(GsArgs a) {
+    constexpr int kGtWarps = NTH / 32;
     constexpr int MC = M / P;
     constexpr int G = 32 / P;
     constexpr int SR = G * U;   // rows per slice

@@ -557,20 +557,24 @@ int tsqr_gs_levels(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t
 
 // Tall and 16-byte aligned: the same streams fed by the bulk-copy engine
 // (tsqr_gt.cuh), one 8-warp CTA per SM, every warp at least one full slice.
+constexpr int gt_threads(int M) { return M <= 16 ? 384 : kPtThreads; }
+constexpr int kGtMaxWarps = 12;
+
 template <int M, int P, int U>
 int tsqr_gt_levels(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t ld, double* R, ColSplit cs) {
-    constexpr int G = 32 / P, SR = G * U;
-    const void* fn = (const void*)tsqr_gt_kernel<M, P, U>;
-    TT_TRY(kattr(ctx, fn, (int)gt_smem_bytes<M, P, U>()));
+    constexpr int G = 32 / P, SR = G * U, NTH = gt_threads(M), NWp = NTH / 32;
+    const void* fn = (const void*)tsqr_gt_kernel<M, P, U, 1, kGtStages, NTH>;
+    TT_TRY(kattr(ctx, fn, (int)gt_smem_bytes<M, P, U, kGtStages, NTH>()));
     const int64_t slices = (n + SR - 1) / SR;
-    const int64_t ctas = std::min<int64_t>(ctx->num_sms, slices / kGtWarps);
-    const int64_t T = ctas * kGtWarps * G;
+    const int64_t ctas = std::min<int64_t>(ctx->num_sms, slices / NWp);
+    const int64_t T = ctas * NWp * G;
     DevBuf& ob = ctx->ws_gs;
     TT_TRY(ensure(ob, (size_t)T * m * m * 8));
     double* out = as<double>(ob);
     GsArgs ga{X, n, ld, m, T, out, T * m, cs};
     kmark(ctx, 0, TTSVD_K_GT);
-    tsqr_gt_kernel<M, P, U><<<(unsigned)ctas, kPtThreads, gt_smem_bytes<M, P, U>(), ctx->stream>>>(ga);
+    tsqr_gt_kernel<M, P, U, 1, kGtStages, NTH>
+        <<<(unsigned)ctas, NTH, gt_smem_bytes<M, P, U, kGtStages, NTH>(), ctx->stream>>>(ga);
     TT_TRY(check_launch(ctx, "tsqr_gt_kernel"));
     kmark(ctx, 1, TTSVD_K_GT);
     return tsqr_ws_device(ctx, out, T * m, m, T * m, R, false);
@@ -583,12 +587,12 @@ int tsqr_gt_levels(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t
 template <int M, int P, int U, class Before>
 int tsqr_gt_chunked(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t ld, double* R, int chunks,
                     Before before) {
-    constexpr int G = 32 / P, SR = G * U, MC = M / P;
-    const void* fn = (const void*)tsqr_gt_kernel<M, P, U>;
-    TT_TRY(kattr(ctx, fn, (int)gt_smem_bytes<M, P, U>()));
+    constexpr int G = 32 / P, SR = G * U, MC = M / P, NTH = gt_threads(M), NWp = NTH / 32;
+    const void* fn = (const void*)tsqr_gt_kernel<M, P, U, 1, kGtStages, NTH>;
+    TT_TRY(kattr(ctx, fn, (int)gt_smem_bytes<M, P, U, kGtStages, NTH>()));
     const int64_t slices = (n + SR - 1) / SR;
-    const int64_t ctas = std::min<int64_t>(ctx->num_sms, slices / kGtWarps);
-    const int64_t Wt = ctas * kGtWarps, T = Wt * G;
+    const int64_t ctas = std::min<int64_t>(ctx->num_sms, slices / NWp);
+    const int64_t Wt = ctas * NWp, T = Wt * G;
     TT_TRY(ensure(ctx->ws_gs, (size_t)T * m * m * 8));
     TT_TRY(ensure(ctx->ws_gt_state, (size_t)Wt * 32 * M * MC * 8));
     double* out = as<double>(ctx->ws_gs);
@@ -599,7 +603,8 @@ int tsqr_gt_chunked(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_
         TT_TRY(before(lo * SR, std::min(n, hi * SR)));
         GsArgs ga{X, n, ld, m, T, out, T * m, ColSplit{0, 0}, lo, hi, as<double>(ctx->ws_gt_state),
                   (c > 0 ? 1 : 0) | (hi < slices ? 2 : 0)};
-        tsqr_gt_kernel<M, P, U><<<(unsigned)ctas, kPtThreads, gt_smem_bytes<M, P, U>(), ctx->stream>>>(ga);
+        tsqr_gt_kernel<M, P, U, 1, kGtStages, NTH>
+            <<<(unsigned)ctas, NTH, gt_smem_bytes<M, P, U, kGtStages, NTH>(), ctx->stream>>>(ga);
         TT_TRY(check_launch(ctx, "tsqr_gt_kernel"));
     }
     kmark(ctx, 1, TTSVD_K_GT);
@@ -608,14 +613,13 @@ int tsqr_gt_chunked(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_
 
 // tsqr_gs_device dispatches a shape to the TMA-staged kernel under these conditions
 bool gt_eligible(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t ld) {
-    return m > 8 && m <= kSmallM && n >= (int64_t)ctx->num_sms * kGtWarps * 64 * 4 && (ld & 1) == 0 &&
+    return m > 8 && m <= kSmallM && n >= (int64_t)ctx->num_sms * kGtMaxWarps * 64 * 4 && (ld & 1) == 0 &&
            ((uintptr_t)X & 15) == 0;
 }
 
 int tsqr_gs_device(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t ld, double* R,
                    ColSplit cs = ColSplit{0, 0}) {
-    if (n >= (int64_t)ctx->num_sms * kGtWarps * 64 * 4 && (ld & 1) == 0 && ((uintptr_t)X & 15) == 0 &&
-        (cs.q == 0 || (cs.ld_lo & 1) == 0))
+    if (gt_eligible(ctx, X, n, m, ld) && (cs.q == 0 || (cs.ld_lo & 1) == 0))
         return m <= 16 ? tsqr_gt_levels<16, 4, 8>(ctx, X, n, m, ld, R, cs)
                        : tsqr_gt_levels<32, 8, 8>(ctx, X, n, m, ld, R, cs);
     if (cs.q) return kNoView;
@@ -2217,7 +2221,7 @@ int ttsvd_cu_tt_svd_host(ttsvd_cu_ctx* ctx, const double* X_host, const int64_t*
     // has landed (the streams' running factors carried between the launches),
     // so the first TSQR hides under the H2D.  Same bits as the device entry.
     if (d >= 2 && ldx >= rows && gt_eligible(ctx, dX, rows, m1, ldx) &&
-        rows >= (int64_t)ctx->num_sms * kGtWarps * 64 * 8 && !ctx->timing) {
+        rows >= (int64_t)ctx->num_sms * kGtMaxWarps * 64 * 8 && !ctx->timing) {
         if (!ctx->copy_stream) {
             TT_CUDA(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
             TT_CUDA(cudaEventCreateWithFlags(&ctx->copy_ev, cudaEventDisableTiming));

@@ -24,7 +24,7 @@ void run(const double* X, int64_t n, int m, double* out) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kPtThreads, smem);
     cudaFuncAttributes fa; cudaFuncGetAttributes(&fa, fn);
     const int64_t ctas = 148 * (per_sm > 0 ? per_sm : 1);
-    const int64_t T = ctas * kGtWarps * G;
+    const int64_t T = ctas * (kPtThreads / 32) * G;
     GsArgs ga{X, n, n, m, T, out, T * m};
     cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
     fn<<<(unsigned)ctas, kPtThreads, smem>>>(ga);
