@@ -67,7 +67,7 @@ enum {
     TTSVD_K_GQR = 5,   /* cooperative whole-grid QR */
     TTSVD_K_PT = 6,    /* thread streams, m <= 8 */
     TTSVD_K_GS = 7,    /* lane-group streams, 8 < m <= 32 */
-    TTSVD_K_SQ = 8,    /* levels of 256-row register tile QRs, 32 < m <= 64 */
+    TTSVD_K_SQ = 8,    /* levels of single 256-row tiles (tsqr_t128_kernel), 32 < m <= 64, small n */
     TTSVD_K_GT = 9     /* lane-group streams fed by TMA bulk copies, 8 < m <= 32, tall */
 };
 

@@ -29,7 +29,7 @@ class Step(C.Structure):
 
 TSQR_KERNELS = {0: "none", 1: "tsqr_ws_kernel", 2: "tsqr_tile_kernel", 3: "tsqr_la_kernel", 4: "tsqr_t128_kernel",
                 5: "gqr_kernel", 6: "tsqr_pt_kernel",
-                7: "tsqr_gs_kernel", 8: "tsqr_sq_kernel", 9: "tsqr_gt_kernel"}
+                7: "tsqr_gs_kernel", 8: "tsqr_t128_kernel (tile levels)", 9: "tsqr_gt_kernel"}
 
 
 EXCHANGE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, i64, C.c_void_p)

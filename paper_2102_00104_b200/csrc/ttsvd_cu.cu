@@ -34,7 +34,6 @@
 #include "tsqr_pt.cuh"
 #include "tsqr_gt.cuh"
 #include "tsmm_dt.cuh"
-#include "tsqr_sq.cuh"
 
 using namespace ttsvd_b200;
 
@@ -238,6 +237,7 @@ int set_device(ttsvd_cu_ctx* ctx) {
 // internal: the kernel a shape dispatches to cannot read a split-column view
 // (ColSplit) in place; the caller materialises the view and calls again
 constexpr int kNoView = -2;
+constexpr int64_t kSqMaxRows = 1 << 16;  // 32 < m <= 64 up to here: levels of single tiles (tsqr_t2_levels)
 constexpr int kTsqrThreads = 256;
 constexpr int kSmemLimit = 227 * 1024;
 constexpr int kTsmmSmem = 200 * 1024;  // V block of tsmm_kernel (m x KC doubles)
@@ -628,31 +628,6 @@ int tsqr_gs_device(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t
     return m <= 16 ? tsqr_gs_levels<16, 4, 8>(ctx, X, n, m, ld, R) : tsqr_gs_levels<32, 8, 8>(ctx, X, n, m, ld, R);
 }
 
-// 32 < m <= 64, small n: levels of 256-row register tile QRs (tsqr_sq.cuh),
-// each cutting the rows by 256 / m, until one tile is left.
-int tsqr_sq_levels(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t ld, double* R) {
-    const double* src = X;
-    int64_t rows = n, sld = ld;
-    int flip = 0;
-    for (;;) {
-        const int64_t T = (rows + kSqRows - 1) / kSqRows;
-        if (T > 1) {
-            TT_TRY(ensure(ctx->ws_R, (size_t)T * m * m * 8));
-            TT_TRY(ensure(ctx->ws_R2, (size_t)T * m * m * 8));
-        }
-        double* out = (T == 1) ? R : as<double>(flip ? ctx->ws_R2 : ctx->ws_R);
-        const int64_t ldo = (T == 1) ? m : T * m;
-        SqArgs sa{src, rows, sld, m, T, out, ldo};
-        tsqr_sq_kernel<<<(unsigned)T, kSqThreads, 0, ctx->stream>>>(sa);
-        TT_TRY(check_launch(ctx, "tsqr_sq_kernel"));
-        if (T == 1) return TTSVD_OK;
-        src = out;
-        rows = T * m;
-        sld = T * m;
-        flip ^= 1;
-    }
-}
-
 // Tall tiles (tsqr_t128_kernel, one CTA per SM) + one cooperative QR of the
 // 148 stacked factors.  chunk_rows > 0: the sweep runs in launches over
 // consecutive row ranges, the per-CTA factors carried from launch to launch;
@@ -694,6 +669,41 @@ int tsqr_t128_run(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t 
     return copy_leading(ctx, as<double>(ctx->ws_P), M, m, R);
 }
 
+// 32 < m <= 64, small n (config 1's m = 64 steps): levels of 256-row tiles on
+// the tall-tile kernel, one tile per CTA (register-tile panels, phase A on
+// DMMA), the packed factors re-stacked densely for the next level until one
+// tile is left (a 4-ary combine tree in index order, tsqr.hpp:204-240).
+// ~60 us per level against ~90 us for the former column-per-lane tile kernel
+// (two CTA barriers and 64 shared-memory loads per thread and reflector) and
+// ~5 us per reflector for the cooperative grid on these shapes.
+int tsqr_t2_levels(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t ld, double* R) {
+    const int M = (m + 31) / 32 * 32;
+    const int64_t RS = blk_rsize(M);
+    TT_TRY(kattr(ctx, (const void*)tsqr_t128_kernel<256>, (int)t2_smem_bytes(256)));
+    const double* src = X;
+    int64_t rows = n, sld = ld;
+    int mm = m;
+    for (;;) {
+        const int64_t T = (rows + 255) / 256;
+        TT_TRY(ensure(ctx->ws_R, (size_t)T * RS * 8));
+        TT_TRY(ensure(ctx->ws_Scr, (size_t)T * 256 * M * 8));
+        double* parts = as<double>(ctx->ws_R);
+        T2Args ta{src, rows, sld, parts, as<double>(ctx->ws_Scr), mm, M, nullptr, ColSplit{0, 0}, 0, 0, 0};
+        tsqr_t128_kernel<256><<<(unsigned)T, kT2Threads, t2_smem_bytes(256), ctx->stream>>>(ta);
+        TT_TRY(check_launch(ctx, "tsqr_t128_kernel"));
+        if (T == 1) return copy_leading(ctx, parts, M, m, R);
+        TT_TRY(ensure(ctx->ws_G, (size_t)T * M * M * 8));
+        double* Aw = as<double>(ctx->ws_G);
+        const int64_t tot = T * M * M;
+        stack_packed_kernel<<<(unsigned)std::min<int64_t>((tot + 255) / 256, 8192), 256, 0, ctx->stream>>>(parts, T, M, Aw);
+        TT_TRY(check_launch(ctx, "stack_packed_kernel"));
+        src = Aw;
+        rows = T * M;
+        sld = T * M;
+        mm = M;  // the stacked factors are M wide (columns m .. M-1 zero)
+    }
+}
+
 // the shapes tsqr_device sends to tsqr_t128_run
 bool t128_eligible(ttsvd_cu_ctx* ctx, int64_t n, int m) {
     const int M = (m + 31) / 32 * 32;
@@ -713,7 +723,7 @@ int tsqr_device(ttsvd_cu_ctx* ctx, const double* X, int64_t n, int m, int64_t ld
             return kNoView;
         if (!R_init && m <= 64 && n <= kSqMaxRows) {
             kmark(ctx, 0, TTSVD_K_SQ);
-            const int rc = tsqr_sq_levels(ctx, X, n, m, ld, R);
+            const int rc = tsqr_t2_levels(ctx, X, n, m, ld, R);
             kmark(ctx, 1, TTSVD_K_SQ);
             return rc;
         }

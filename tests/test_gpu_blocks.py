@@ -112,7 +112,7 @@ def test_tsqr_wide_kernels(tt, n, m, kind):
     assert np.array_equal(host(tt.tsqr(X)), R)
 
 
-# The register tile levels (tsqr_sq_kernel, 32 < m <= 64, n <= 2^16: 256-row
+# The register tile levels (tsqr_t128_kernel with one tile per CTA, 32 < m <= 64, n <= 2^16: 256-row
 # tile QRs, their stacked factors the next level's rows): partial tiles, one to five levels, zero / duplicated columns, low
 # rank and subnormal squares.
 @pytest.mark.parametrize("n,m,kind", [(40, 33, "dense"), (64, 64, "dense"), (65, 33, "dup"), (256, 64, "dense"),
